@@ -1,0 +1,205 @@
+/* include/moe_cuda.h -- C-ABI of libmoe_cuda.so, the B200 (sm_100a) MoE-layer
+ * hot path.
+ *
+ * Plain pointers, int64 sizes, cudaStream_t passed as void*, int status.
+ * Every *device* argument is a device pointer unless the name ends in _host.
+ * No torch types.  Status codes:
+ *   MOE_OK 0, MOE_EINVAL 1 (argument / data validation; message mirrors the
+ *   reference's std::invalid_argument text), MOE_ECUDA 2, MOE_ENCCL 3,
+ *   MOE_ERANGE 4 (index out of range, reference std::out_of_range).
+ * moe_cuda_last_error() returns the thread-local message of the last failure.
+ *
+ * Each entry point names the reference interface it replaces
+ * (paths relative to /root/reference/proj).  The C++ drop-in
+ * (include/moeinfer/*.hpp, libmoeinfer_b200.so) and the Python module
+ * (_moeinfer) are thin layers over these.
+ *
+ * Numerics modes:
+ *   MOE_MODE_EXACT -- CUDA-core kernels that reproduce the reference bit for
+ *                     bit (k-sequential f32 accumulation, RN16(q*s) weights).
+ *   MOE_MODE_FAST  -- tcgen05/TMEM tensor-core grouped GEMM (f32 accumulate,
+ *                     per-channel scale applied in the epilogue); gating,
+ *                     routing and combine stay bit-exact.
+ */
+#ifndef MOE_CUDA_H
+#define MOE_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MOE_OK 0
+#define MOE_EINVAL 1
+#define MOE_ECUDA 2
+#define MOE_ENCCL 3
+#define MOE_ERANGE 4
+
+#define MOE_MODE_EXACT 0
+#define MOE_MODE_FAST 1
+
+/* weight formats: fp16 experts, or reference-quantized codes */
+#define MOE_W16 16
+#define MOE_W8 8
+#define MOE_W4 4
+
+typedef void* moe_stream_t; /* a cudaStream_t */
+
+const char* moe_cuda_last_error(void);
+/* library / device info: 0 ok; fills sm count and compute capability */
+int moe_cuda_device_info(int* sm_count, int* cc_major, int* cc_minor);
+/* Number of this library's kernels launched since load (all entry points).
+ * bench.py reports the delta as gpu_launches. */
+uint64_t moe_cuda_launch_count(void);
+
+/* Memory / stream plumbing for host-side callers that do not link the CUDA
+ * runtime themselves (the C++ drop-in, ctypes).  kind: 0 H2D, 1 D2H, 2 D2D. */
+int moe_cuda_malloc(void** ptr, size_t bytes);
+int moe_cuda_free(void* ptr);
+int moe_cuda_host_alloc(void** ptr, size_t bytes); /* pinned */
+int moe_cuda_host_free(void* ptr);
+int moe_cuda_memcpy(void* dst, const void* src, size_t bytes, int kind, moe_stream_t stream);
+int moe_cuda_memset(void* dst, int value, size_t bytes, moe_stream_t stream);
+int moe_cuda_sync(moe_stream_t stream);
+
+/* Debias constants of the magic I2F path (include/moeinfer/dequant.hpp:35-36,
+ * src/dequant.cpp:45-53).  Initialised from MOE_FAULT_INJECT exactly like
+ * src/dequant.cpp:12-30 ("i2f4" -> 0x6409 for u4, other non-empty -> 0x6481
+ * for u8); tests may override. */
+void moe_cuda_debias(uint16_t* u8c, uint16_t* u4c);
+void moe_cuda_set_debias(uint16_t u8c, uint16_t u4c);
+
+/* ---- K1: quantizer -- replaces moe::quantize (include/moeinfer/quantize.hpp:56-57,
+ * src/quantize.cpp:74-122).  w: (e,m,n) fp16; packed: reference layout
+ * (e*m*n bytes for 8-bit, e*m*n/2 interleaved nibbles for 4-bit);
+ * scales: (e,n) fp16.  Synchronises the stream (validation result). */
+int moe_quantize(const uint16_t* w, int64_t e, int64_t m, int64_t n, int bits,
+                 uint8_t* packed, uint16_t* scales, moe_stream_t stream);
+
+/* pack_int4_interleaved / unpack_int4_interleaved
+ * (include/moeinfer/quantize.hpp:62-65, src/quantize.cpp:34-72). */
+int moe_pack_int4(const uint8_t* values, int64_t count, uint8_t* packed,
+                  moe_stream_t stream);
+int moe_unpack_int4(const uint8_t* packed, int64_t count, uint8_t* values,
+                    moe_stream_t stream);
+
+/* ---- K0: dequantizer -- replaces dequantize_naive / dequantize_fast
+ * (include/moeinfer/dequant.hpp:73-74, src/dequant.cpp:55-112). */
+int moe_dequantize(const uint8_t* packed, const uint16_t* scales, int64_t e,
+                   int64_t m, int64_t n, int bits, int fast, uint16_t* out,
+                   moe_stream_t stream);
+
+/* ---- device weight tiles (new) ----
+ * Re-tiles one expert tensor (e,m,n) from the reference layout into the
+ * GEMM layout: [e][n/128][m/64][block], block = 128 output columns x 64
+ * inputs, each column's 64 codes contiguous (16-byte chunks).  Sizes are
+ * padded to 128 (n) and 64 (m) with zero codes. */
+int64_t moe_tiled_bytes(int64_t e, int64_t m, int64_t n, int bits);
+int moe_tile_weights(const void* src, int64_t e, int64_t m, int64_t n, int bits,
+                     void* tiled, moe_stream_t stream);
+
+/* ---- K2: gating ----
+ * layer_norm (src/model.cpp:175-205); gate_logits_f32 (src/model.cpp:273-297);
+ * gate_top1 (src/routing.cpp:11-41) generalised to top-k. */
+int moe_layer_norm(const uint16_t* x, int64_t T, int64_t d, const uint16_t* gamma,
+                   const uint16_t* beta, uint16_t* out, moe_stream_t stream);
+int moe_gate_logits(const uint16_t* xn, int64_t T, int64_t d, const uint16_t* gw,
+                    const uint16_t* gb, int64_t E, float* logits, moe_stream_t stream);
+/* expert, scale: (T,k).  Non-finite logits are reported (lowest bad row) and
+ * the call synchronises to raise MOE_EINVAL with the reference's message. */
+int moe_gate_topk(const float* logits, int64_t T, int64_t E, int k, uint32_t* expert,
+                  uint16_t* scale, moe_stream_t stream);
+
+/* ---- K3: routing plan -- build_routing_plan (src/routing.cpp:43-87) over
+ * S = T*k slots.  finished may be NULL (no finished rows).  offsets: E+1.
+ * problems (may be NULL): E triples (expert, row_begin, row_end).
+ * active (device u32, may be NULL).  Validates expert < E (synchronises). */
+int moe_routing_plan(const uint32_t* expert, const uint8_t* finished, int64_t T,
+                     int k, int64_t E, uint32_t* perm, uint32_t* inv,
+                     uint32_t* offsets, uint32_t* problems, uint32_t* active,
+                     moe_stream_t stream);
+/* permute_rows (src/routing.cpp:89-97): xp[p] = x[perm[p]/k]. */
+int moe_permute_rows(const uint16_t* x, int64_t cols, const uint32_t* perm,
+                     int64_t S, int k, uint16_t* xp, moe_stream_t stream);
+/* unpermute_and_scale (src/routing.cpp:99-116), top-1 plan. */
+int moe_unpermute_scale(const uint16_t* y, int64_t T, int64_t cols,
+                        const uint32_t* perm, const uint32_t* active,
+                        const uint16_t* scale, uint16_t* out, moe_stream_t stream);
+/* K6 combine: out[r] = finished ? x[r] : fold_s half_add(., half_mul(y[inv[r*k+s]], scale[r,s]))
+ * (src/model.cpp:334-346 + src/routing.cpp:106-114, slot-ordered for k>1). */
+int moe_combine(const uint16_t* x, const uint16_t* y, const uint32_t* inv,
+                const uint16_t* scale, const uint8_t* finished, int64_t T,
+                int64_t d, int k, uint16_t* out, moe_stream_t stream);
+
+/* ---- K4/K5: grouped expert GEMM -- grouped_gemm_f16 / grouped_gemm_quant
+ * (include/moeinfer/grouped_gemm.hpp:65-82, src/grouped_gemm.cpp:140-214).
+ * x: (rows, m) fp16 row-major (expert-sorted).  problems: np triples on the
+ * device.  tiled: moe_tile_weights output; scales (E,n) fp16 (NULL for W16).
+ * bias (E,n) fp16.  out (rows, n): rows outside every problem are left
+ * untouched (callers zero them when the reference semantics need it). */
+int moe_grouped_gemm(const uint16_t* x, int64_t rows, int64_t m,
+                     const uint32_t* problems, int64_t np, const void* tiled,
+                     const uint16_t* scales, int bits, int64_t E, int64_t n,
+                     const uint16_t* bias, int relu, int mode, uint16_t* out,
+                     moe_stream_t stream);
+
+/* ---- whole MoE layer -- replaces moe::moe_ffn_forward
+ * (include/moeinfer/model.hpp:154-156, src/model.cpp:299-349) with a
+ * device-resident layer object (weights uploaded and tiled once). */
+typedef struct moe_layer moe_layer;
+
+typedef struct {
+  int64_t d, f, E;
+  int bits;                       /* 16, 8 or 4 */
+  /* host pointers, reference layouts (model.hpp:73-84) */
+  const uint16_t *ln_g, *ln_b;    /* d */
+  const uint16_t *gate_w;         /* (d, E) */
+  const uint16_t *gate_b;         /* E */
+  const uint16_t *b1, *b2;        /* (E, f), (E, d) */
+  const uint16_t *w1, *w2;        /* bits 16: (E,d,f), (E,f,d) */
+  const uint8_t *q1, *q2;         /* bits 8/4: quantize() payloads */
+  const uint16_t *s1, *s2;        /* (E,f), (E,d) scales */
+} moe_layer_desc;
+
+int moe_layer_create(const moe_layer_desc* desc, moe_layer** out);
+/* Same, with every pointer in desc a DEVICE pointer (e.g. quantized on the
+ * GPU by moe_quantize); weights are still copied/tiled into the layer. */
+int moe_layer_create_device(const moe_layer_desc* desc, moe_layer** out);
+int moe_layer_destroy(moe_layer* L);
+/* Device-resident forward: x, finished (nullable), out on the device.
+ * Graph-capturable (no host synchronisation, no allocation once the
+ * workspace for (T,k) exists -- call moe_layer_reserve first).
+ * Non-finite gate logits are flagged on the device; see moe_layer_status. */
+int moe_layer_reserve(moe_layer* L, int64_t T, int k);
+int moe_layer_forward(moe_layer* L, const uint16_t* x, const uint8_t* finished,
+                      int64_t T, int k, int mode, uint16_t* out, moe_stream_t stream);
+/* Host-buffer forward (the drop-in / e2e path): copies x and finished in,
+ * runs, copies out back, synchronises, and raises validation errors. */
+int moe_layer_forward_host(moe_layer* L, const uint16_t* x_host,
+                           const uint8_t* finished_host, int64_t T, int k, int mode,
+                           uint16_t* out_host, moe_stream_t stream);
+/* Synchronises and reports device-side validation (non-finite logits). */
+int moe_layer_status(moe_layer* L, moe_stream_t stream);
+/* Routing diagnostics of the last forward (device pointers owned by L):
+ * expert/scale (T,k), perm/inv (T*k), offsets (E+1), active (1). */
+int moe_layer_routing(moe_layer* L, const uint32_t** expert, const uint16_t** scale,
+                      const uint32_t** perm, const uint32_t** inv,
+                      const uint32_t** offsets, const uint32_t** active);
+/* Analytic traffic of the last forward, reference accounting
+ * (src/grouped_gemm.cpp:155-160, 201-211; src/model.cpp:303-347):
+ * out6 = {expert.weight, expert.activation, expert.written,
+ *         other.weight, other.activation, other.written}.  Synchronises. */
+int moe_layer_traffic(moe_layer* L, uint64_t* out6, moe_stream_t stream);
+
+/* ---- expert-parallel helpers (new) ----
+ * Per-destination-rank slot counts for EP dispatch: experts are owned in
+ * contiguous blocks of E/G; counts[g] = #active slots routed to rank g. */
+int moe_ep_rank_counts(const uint32_t* offsets, int64_t E, int G, int64_t* counts,
+                       moe_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,570 @@
+// abi.cu -- the extern "C" boundary (include/moe_cuda.h) and the device-
+// resident MoE layer that replaces moe::moe_ffn_forward
+// (proj/src/model.cpp:299-349).
+//
+// Layer forward on one stream, no host synchronisation, graph-capturable:
+//   layer_norm -> gate_logits -> gate_topk -> plan(count, scan, place+gather)
+//   -> grouped GEMM FFN1 (ReLU) -> grouped GEMM FFN2 -> combine
+// GEMM problems are read from device memory (the plan writes them), so the
+// host never needs the routing result.
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+
+namespace moecu {
+
+static thread_local std::string g_err;
+static std::atomic<uint64_t> g_launches{0};
+
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+int set_error(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int set_cuda_error(cudaError_t e, const char* what) {
+  return set_error(MOE_ECUDA, "CUDA error %s (%s) at %s", cudaGetErrorName(e),
+                   cudaGetErrorString(e), what);
+}
+
+int check_launch(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error(e, what);
+  return MOE_OK;
+}
+
+int sm_count() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+// MOE_FAULT_INJECT, read once (proj/src/dequant.cpp:12-30)
+struct Debias {
+  uint16_t u8 = 0x6480, u4 = 0x6408;
+  Debias() {
+    const char* v = std::getenv("MOE_FAULT_INJECT");
+    if (v != nullptr && *v != '\0') {
+      if (std::strcmp(v, "i2f4") == 0)
+        u4 = 0x6409;
+      else
+        u8 = 0x6481;
+    }
+  }
+};
+static Debias& debias() {
+  static Debias d;
+  return d;
+}
+static uint16_t debias_for(int bits) { return bits == 8 ? debias().u8 : debias().u4; }
+
+// RAII device scratch for the synchronous helpers
+struct DevBuf {
+  void* p = nullptr;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+};
+
+}  // namespace moecu
+
+using namespace moecu;
+
+static cudaStream_t S(moe_stream_t s) { return static_cast<cudaStream_t>(s); }
+
+extern "C" {
+
+const char* moe_cuda_last_error(void) { return g_err.c_str(); }
+
+int moe_cuda_device_info(int* sm, int* major, int* minor) {
+  int dev = 0;
+  MOE_CUDA_TRY(cudaGetDevice(&dev));
+  cudaDeviceProp p;
+  MOE_CUDA_TRY(cudaGetDeviceProperties(&p, dev));
+  if (sm) *sm = p.multiProcessorCount;
+  if (major) *major = p.major;
+  if (minor) *minor = p.minor;
+  return MOE_OK;
+}
+
+uint64_t moe_cuda_launch_count(void) { return g_launches.load(); }
+
+int moe_cuda_malloc(void** p, size_t bytes) {
+  MOE_CUDA_TRY(cudaMalloc(p, bytes ? bytes : 16));
+  return MOE_OK;
+}
+int moe_cuda_free(void* p) {
+  if (p) MOE_CUDA_TRY(cudaFree(p));
+  return MOE_OK;
+}
+int moe_cuda_host_alloc(void** p, size_t bytes) {
+  MOE_CUDA_TRY(cudaMallocHost(p, bytes ? bytes : 16));
+  return MOE_OK;
+}
+int moe_cuda_host_free(void* p) {
+  if (p) MOE_CUDA_TRY(cudaFreeHost(p));
+  return MOE_OK;
+}
+int moe_cuda_memcpy(void* dst, const void* src, size_t bytes, int kind, moe_stream_t stream) {
+  if (bytes == 0) return MOE_OK;
+  const cudaMemcpyKind k = kind == 0   ? cudaMemcpyHostToDevice
+                           : kind == 1 ? cudaMemcpyDeviceToHost
+                                       : cudaMemcpyDeviceToDevice;
+  MOE_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, k, S(stream)));
+  if (kind == 1) MOE_CUDA_TRY(cudaStreamSynchronize(S(stream)));
+  return MOE_OK;
+}
+int moe_cuda_memset(void* dst, int value, size_t bytes, moe_stream_t stream) {
+  if (bytes == 0) return MOE_OK;
+  MOE_CUDA_TRY(cudaMemsetAsync(dst, value, bytes, S(stream)));
+  return MOE_OK;
+}
+int moe_cuda_sync(moe_stream_t stream) {
+  MOE_CUDA_TRY(cudaStreamSynchronize(S(stream)));
+  return MOE_OK;
+}
+
+void moe_cuda_debias(uint16_t* u8c, uint16_t* u4c) {
+  if (u8c) *u8c = debias().u8;
+  if (u4c) *u4c = debias().u4;
+}
+void moe_cuda_set_debias(uint16_t u8c, uint16_t u4c) {
+  debias().u8 = u8c;
+  debias().u4 = u4c;
+}
+
+// ------------------------------------------------------------------- K1 / K0
+int moe_quantize(const uint16_t* w, int64_t e, int64_t m, int64_t n, int bits, uint8_t* packed,
+                 uint16_t* scales, moe_stream_t stream) {
+  if (bits != 4 && bits != 8) return set_error(MOE_EINVAL, "bits must be 4 or 8");
+  if (!(e > 0 && m > 0 && n > 0)) return set_error(MOE_EINVAL, "quantize: empty weight tensor");
+  if (bits == 4 && n % 8 != 0)
+    return set_error(MOE_EINVAL, "quantize: 4-bit packing needs the column count divisible by 8");
+  DevBuf bad;
+  MOE_CUDA_TRY(cudaMallocAsync(&bad.p, 8, S(stream)));
+  MOE_CUDA_TRY(cudaMemsetAsync(bad.p, 0xFF, 8, S(stream)));
+  int st = launch_quantize(w, e, m, n, bits, packed, scales,
+                           static_cast<unsigned long long*>(bad.p), S(stream));
+  if (st) return st;
+  unsigned long long h = 0;
+  MOE_CUDA_TRY(cudaMemcpyAsync(&h, bad.p, 8, cudaMemcpyDeviceToHost, S(stream)));
+  MOE_CUDA_TRY(cudaStreamSynchronize(S(stream)));
+  if (h != ~0ull)
+    return set_error(MOE_EINVAL, "quantize: non-finite weight at flat index %llu", h);
+  return MOE_OK;
+}
+
+int moe_pack_int4(const uint8_t* values, int64_t count, uint8_t* packed, moe_stream_t stream) {
+  if (count % 8 != 0)
+    return set_error(MOE_EINVAL, "pack_int4_interleaved: length must be a multiple of 8");
+  DevBuf bad;
+  MOE_CUDA_TRY(cudaMallocAsync(&bad.p, 8, S(stream)));
+  MOE_CUDA_TRY(cudaMemsetAsync(bad.p, 0xFF, 8, S(stream)));
+  int st = launch_pack_int4(values, count, packed, static_cast<unsigned long long*>(bad.p),
+                            S(stream));
+  if (st) return st;
+  unsigned long long h = 0;
+  MOE_CUDA_TRY(cudaMemcpyAsync(&h, bad.p, 8, cudaMemcpyDeviceToHost, S(stream)));
+  MOE_CUDA_TRY(cudaStreamSynchronize(S(stream)));
+  if (h != ~0ull)
+    return set_error(MOE_EINVAL, "pack_int4_interleaved: value does not fit a nibble");
+  return MOE_OK;
+}
+
+int moe_unpack_int4(const uint8_t* packed, int64_t count, uint8_t* values, moe_stream_t stream) {
+  if (count % 8 != 0)
+    return set_error(MOE_EINVAL, "unpack_int4_interleaved: count must be a multiple of 8");
+  return launch_unpack_int4(packed, count, values, S(stream));
+}
+
+int moe_dequantize(const uint8_t* packed, const uint16_t* scales, int64_t e, int64_t m,
+                   int64_t n, int bits, int fast, uint16_t* out, moe_stream_t stream) {
+  if (!(e > 0 && m > 0 && n > 0)) return set_error(MOE_EINVAL, "dequantize: empty tensor");
+  if (bits != 4 && bits != 8) return set_error(MOE_EINVAL, "bits must be 4 or 8");
+  if (bits == 4 && n % 8 != 0)
+    return set_error(MOE_EINVAL, "dequantize: 4-bit column count not a multiple of 8");
+  return launch_dequantize(packed, scales, e, m, n, bits, fast, debias_for(bits), out,
+                           S(stream));
+}
+
+int64_t moe_tiled_bytes(int64_t e, int64_t m, int64_t n, int bits) {
+  return tiled_bytes(e, m, n, bits);
+}
+
+int moe_tile_weights(const void* src, int64_t e, int64_t m, int64_t n, int bits, void* tiled,
+                     moe_stream_t stream) {
+  if (bits != 4 && bits != 8 && bits != 16) return set_error(MOE_EINVAL, "bits must be 4, 8 or 16");
+  if (bits == 4 && n % 8 != 0)
+    return set_error(MOE_EINVAL, "tile_weights: 4-bit column count not a multiple of 8");
+  return launch_tile_weights(src, e, m, n, bits, tiled, S(stream));
+}
+
+// ------------------------------------------------------------------------ K2
+int moe_layer_norm(const uint16_t* x, int64_t T, int64_t d, const uint16_t* g,
+                   const uint16_t* b, uint16_t* out, moe_stream_t stream) {
+  return launch_layer_norm(x, T, d, g, b, out, S(stream));
+}
+
+int moe_gate_logits(const uint16_t* xn, int64_t T, int64_t d, const uint16_t* gw,
+                    const uint16_t* gb, int64_t E, float* logits, moe_stream_t stream) {
+  return launch_gate_logits(xn, T, d, gw, gb, E, logits, S(stream));
+}
+
+int moe_gate_topk(const float* logits, int64_t T, int64_t E, int k, uint32_t* expert,
+                  uint16_t* scale, moe_stream_t stream) {
+  if (!(T > 0 && E > 0)) return set_error(MOE_EINVAL, "gate_top1: empty input");
+  DevBuf bad;
+  MOE_CUDA_TRY(cudaMallocAsync(&bad.p, 4, S(stream)));
+  MOE_CUDA_TRY(cudaMemsetAsync(bad.p, 0xFF, 4, S(stream)));
+  int st = launch_gate_topk(logits, T, E, k, expert, scale, static_cast<uint32_t*>(bad.p),
+                            S(stream));
+  if (st) return st;
+  uint32_t h = 0;
+  MOE_CUDA_TRY(cudaMemcpyAsync(&h, bad.p, 4, cudaMemcpyDeviceToHost, S(stream)));
+  MOE_CUDA_TRY(cudaStreamSynchronize(S(stream)));
+  if (h != 0xFFFFFFFFu) return set_error(MOE_EINVAL, "gate_top1: non-finite logit at row %u", h);
+  return MOE_OK;
+}
+
+// ------------------------------------------------------------------------ K3
+int moe_routing_plan(const uint32_t* expert, const uint8_t* finished, int64_t T, int k,
+                     int64_t E, uint32_t* perm, uint32_t* inv, uint32_t* offsets,
+                     uint32_t* problems, uint32_t* active, moe_stream_t stream) {
+  if (T <= 0) return set_error(MOE_EINVAL, "build_routing_plan: no rows");
+  if (E <= 0) return set_error(MOE_EINVAL, "build_routing_plan: no experts");
+  const int64_t S_ = T * k, nblk = plan_blocks(S_);
+  DevBuf ws;
+  const size_t cnt = (size_t)nblk * (E + 1);
+  MOE_CUDA_TRY(cudaMallocAsync(&ws.p, (2 * cnt + 1) * 4, S(stream)));
+  PlanWork w{static_cast<uint32_t*>(ws.p), static_cast<uint32_t*>(ws.p) + cnt,
+             static_cast<uint32_t*>(ws.p) + 2 * cnt};
+  MOE_CUDA_TRY(cudaMemsetAsync(w.bad, 0xFF, 4, S(stream)));
+  int st = launch_routing_plan(expert, finished, T, k, E, perm, inv, offsets, problems, active, w,
+                               nullptr, 0, nullptr, S(stream));
+  if (st) return st;
+  uint32_t h = 0;
+  MOE_CUDA_TRY(cudaMemcpyAsync(&h, w.bad, 4, cudaMemcpyDeviceToHost, S(stream)));
+  MOE_CUDA_TRY(cudaStreamSynchronize(S(stream)));
+  if (h != 0xFFFFFFFFu) return set_error(MOE_EINVAL, "build_routing_plan: expert out of range");
+  return MOE_OK;
+}
+
+int moe_permute_rows(const uint16_t* x, int64_t cols, const uint32_t* perm, int64_t S_, int k,
+                     uint16_t* xp, moe_stream_t stream) {
+  return launch_permute(x, cols, perm, S_, k, xp, S(stream));
+}
+
+int moe_unpermute_scale(const uint16_t* y, int64_t T, int64_t cols, const uint32_t* perm,
+                        const uint32_t* active, const uint16_t* scale, uint16_t* out,
+                        moe_stream_t stream) {
+  return launch_unpermute_scale(y, T, cols, perm, active, scale, out, S(stream));
+}
+
+int moe_combine(const uint16_t* x, const uint16_t* y, const uint32_t* inv, const uint16_t* scale,
+                const uint8_t* finished, int64_t T, int64_t d, int k, uint16_t* out,
+                moe_stream_t stream) {
+  return launch_combine(x, y, inv, scale, finished, T, d, k, out, S(stream));
+}
+
+// ---------------------------------------------------------------------- K4/K5
+int moe_grouped_gemm(const uint16_t* x, int64_t rows, int64_t m, const uint32_t* problems,
+                     int64_t np, const void* tiled, const uint16_t* scales, int bits, int64_t E,
+                     int64_t n, const uint16_t* bias, int relu, int mode, uint16_t* out,
+                     moe_stream_t stream) {
+  if (bits != 4 && bits != 8 && bits != 16) return set_error(MOE_EINVAL, "bits must be 4, 8 or 16");
+  GemmArgs a{x, rows, m, problems, np, tiled, scales, bits, E, n, bias, relu, out,
+             debias_for(bits), np > 0 ? rows / np : rows};
+  if (mode == MOE_MODE_FAST) return launch_gemm_tc(a, S(stream));
+  return launch_gemm_exact(a, S(stream));
+}
+
+int moe_ep_rank_counts(const uint32_t* offsets, int64_t E, int G, int64_t* counts,
+                       moe_stream_t stream) {
+  return launch_ep_rank_counts(offsets, E, G, counts, S(stream));
+}
+
+}  // extern "C"
+
+// ======================================================================= layer
+struct moe_layer {
+  int64_t d = 0, f = 0, E = 0;
+  int bits = 16;
+  // weights (device)
+  uint16_t *ln_g = nullptr, *ln_b = nullptr, *gw = nullptr, *gb = nullptr;
+  uint16_t *b1 = nullptr, *b2 = nullptr, *s1 = nullptr, *s2 = nullptr;
+  void *w1t = nullptr, *w2t = nullptr;
+  // workspace, sized for (cap_S slots, cap_T rows)
+  int64_t cap_T = 0, cap_S = 0;
+  uint16_t *xn = nullptr, *xp = nullptr, *h = nullptr, *y = nullptr;
+  float* logits = nullptr;
+  uint32_t *expert = nullptr, *perm = nullptr, *inv = nullptr, *offsets = nullptr,
+           *problems = nullptr, *active = nullptr, *bad_row = nullptr;
+  uint16_t* scale = nullptr;
+  uint32_t *blockcnt = nullptr, *blockbase = nullptr, *bad_expert = nullptr;
+  // host-path staging
+  uint16_t *dx = nullptr, *dout = nullptr;
+  uint8_t* dfin = nullptr;
+  int64_t last_T = 0;
+  int last_k = 1;
+  std::vector<void*> allocs;
+
+  ~moe_layer() {
+    for (void* p : allocs) cudaFree(p);
+  }
+  template <class T>
+  int alloc(T** p, size_t bytes) {
+    void* q = nullptr;
+    const cudaError_t e = cudaMalloc(&q, bytes ? bytes : 16);
+    if (e != cudaSuccess) return set_cuda_error(e, "layer alloc");
+    allocs.push_back(q);
+    *p = static_cast<T*>(q);
+    return MOE_OK;
+  }
+  void release(void* p) {
+    for (auto& q : allocs)
+      if (q == p) {
+        cudaFree(q);
+        q = nullptr;
+      }
+  }
+};
+
+#define TRY(x)                \
+  do {                        \
+    const int s__ = (x);      \
+    if (s__ != MOE_OK) return s__; \
+  } while (0)
+
+static int layer_create_impl(const moe_layer_desc* D, moe_layer** out, bool device_src) {
+  if (D == nullptr || out == nullptr) return set_error(MOE_EINVAL, "layer: null argument");
+  if (!(D->d > 0 && D->f > 0 && D->E > 0)) return set_error(MOE_EINVAL, "layer: empty shape");
+  if (D->bits != 16 && D->bits != 8 && D->bits != 4)
+    return set_error(MOE_EINVAL, "layer: bits must be 16, 8 or 4");
+  if (D->bits == 4 && (D->f % 8 != 0 || D->d % 8 != 0))
+    return set_error(MOE_EINVAL, "layer: 4-bit experts need d and f divisible by 8");
+  auto* L = new moe_layer;
+  L->d = D->d;
+  L->f = D->f;
+  L->E = D->E;
+  L->bits = D->bits;
+  const int64_t d = D->d, f = D->f, E = D->E;
+  const cudaMemcpyKind kind = device_src ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  auto up = [&](uint16_t** dst, const uint16_t* src, int64_t count) -> int {
+    TRY(L->alloc(dst, count * 2));
+    MOE_CUDA_TRY(cudaMemcpy(*dst, src, count * 2, kind));
+    return MOE_OK;
+  };
+  int st = MOE_OK;
+  auto fail = [&](int s) {
+    delete L;
+    return s;
+  };
+  if ((st = up(&L->ln_g, D->ln_g, d)) || (st = up(&L->ln_b, D->ln_b, d)) ||
+      (st = up(&L->gw, D->gate_w, d * E)) || (st = up(&L->gb, D->gate_b, E)) ||
+      (st = up(&L->b1, D->b1, E * f)) || (st = up(&L->b2, D->b2, E * d)))
+    return fail(st);
+  // experts: upload the reference-layout payload once, tile, drop the source
+  auto tile = [&](void** dst, const void* src, int64_t m, int64_t n) -> int {
+    const int64_t src_bytes = D->bits == 16 ? E * m * n * 2 : D->bits == 8 ? E * m * n : E * m * n / 2;
+    void* tmp = nullptr;
+    if (!device_src) {
+      MOE_CUDA_TRY(cudaMalloc(&tmp, src_bytes));
+      MOE_CUDA_TRY(cudaMemcpy(tmp, src, src_bytes, cudaMemcpyHostToDevice));
+    }
+    TRY(L->alloc(dst, tiled_bytes(E, m, n, D->bits)));
+    const int s2 = launch_tile_weights(device_src ? src : tmp, E, m, n, D->bits, *dst, nullptr);
+    MOE_CUDA_TRY(cudaDeviceSynchronize());
+    if (tmp) cudaFree(tmp);
+    return s2;
+  };
+  if (D->bits == 16) {
+    if (!D->w1 || !D->w2) return fail(set_error(MOE_EINVAL, "layer: fp16 experts missing"));
+    if ((st = tile(&L->w1t, D->w1, d, f)) || (st = tile(&L->w2t, D->w2, f, d))) return fail(st);
+  } else {
+    if (!D->q1 || !D->q2 || !D->s1 || !D->s2)
+      return fail(set_error(MOE_EINVAL, "layer: quantized experts missing"));
+    if ((st = tile(&L->w1t, D->q1, d, f)) || (st = tile(&L->w2t, D->q2, f, d)) ||
+        (st = up(&L->s1, D->s1, E * f)) || (st = up(&L->s2, D->s2, E * d)))
+      return fail(st);
+  }
+  *out = L;
+  return MOE_OK;
+}
+
+static int layer_reserve(moe_layer* L, int64_t T, int k) {
+  const int64_t S_ = T * k;
+  if (T <= L->cap_T && S_ <= L->cap_S) return MOE_OK;
+  const int64_t cT = std::max(T, L->cap_T), cS = std::max(S_, L->cap_S);
+  for (void* p : {(void*)L->xn, (void*)L->xp, (void*)L->h, (void*)L->y, (void*)L->logits,
+                  (void*)L->expert, (void*)L->perm, (void*)L->inv, (void*)L->scale,
+                  (void*)L->blockcnt, (void*)L->dx, (void*)L->dout, (void*)L->dfin})
+    if (p) L->release(p);
+  const int64_t d = L->d, f = L->f, E = L->E;
+  const int64_t nblk = plan_blocks(cS);
+  TRY(L->alloc(&L->xn, cT * d * 2));
+  TRY(L->alloc(&L->xp, cS * d * 2));
+  TRY(L->alloc(&L->h, cS * f * 2));
+  TRY(L->alloc(&L->y, cS * d * 2));
+  TRY(L->alloc(&L->logits, cT * E * 4));
+  TRY(L->alloc(&L->expert, cS * 4));
+  TRY(L->alloc(&L->perm, cS * 4));
+  TRY(L->alloc(&L->inv, cS * 4));
+  TRY(L->alloc(&L->scale, cS * 2));
+  TRY(L->alloc(&L->blockcnt, (2 * nblk * (E + 1)) * 4));
+  L->blockbase = L->blockcnt + nblk * (E + 1);
+  TRY(L->alloc(&L->dx, cT * d * 2));
+  TRY(L->alloc(&L->dout, cT * d * 2));
+  TRY(L->alloc(&L->dfin, cT));
+  if (!L->offsets) {
+    uint32_t* small = nullptr;
+    TRY(L->alloc(&small, ((E + 1) + 3 * E + 4) * 4));
+    L->offsets = small;
+    L->problems = small + (E + 1);
+    L->active = L->problems + 3 * E;
+    L->bad_row = L->active + 1;
+    L->bad_expert = L->active + 2;
+  }
+  L->cap_T = cT;
+  L->cap_S = cS;
+  return MOE_OK;
+}
+
+static int layer_forward(moe_layer* L, const uint16_t* x, const uint8_t* fin, int64_t T, int k,
+                         int mode, uint16_t* out, cudaStream_t st) {
+  if (T <= 0) return set_error(MOE_EINVAL, "moe_ffn: no rows");
+  if (k < 1 || k > L->E) return set_error(MOE_EINVAL, "moe_ffn: k must be in [1, n_experts]");
+  TRY(layer_reserve(L, T, k));
+  const int64_t d = L->d, f = L->f, E = L->E, S_ = T * k;
+  L->last_T = T;
+  L->last_k = k;
+  MOE_CUDA_TRY(cudaMemsetAsync(L->bad_row, 0xFF, 8, st));  // bad_row + bad_expert
+  TRY(launch_layer_norm(x, T, d, L->ln_g, L->ln_b, L->xn, st));
+  TRY(launch_gate_logits(L->xn, T, d, L->gw, L->gb, E, L->logits, st));
+  TRY(launch_gate_topk(L->logits, T, E, k, L->expert, L->scale, L->bad_row, st));
+  PlanWork w{L->blockcnt, L->blockbase, L->bad_expert};
+  TRY(launch_routing_plan(L->expert, fin, T, k, E, L->perm, L->inv, L->offsets, L->problems,
+                          L->active, w, L->xn, d, L->xp, st));
+  const uint16_t db = debias_for(L->bits);
+  const int64_t hint = S_ / std::max<int64_t>(1, std::min<int64_t>(E, S_));
+  GemmArgs g1{L->xp, S_, d, L->problems, E, L->w1t, L->s1, L->bits, E, f, L->b1, 1, L->h, db, hint};
+  GemmArgs g2{L->h, S_, f, L->problems, E, L->w2t, L->s2, L->bits, E, d, L->b2, 0, L->y, db, hint};
+  if (mode == MOE_MODE_FAST) {
+    TRY(launch_gemm_tc(g1, st));
+    TRY(launch_gemm_tc(g2, st));
+  } else {
+    TRY(launch_gemm_exact(g1, st));
+    TRY(launch_gemm_exact(g2, st));
+  }
+  TRY(launch_combine(x, L->y, L->inv, L->scale, fin, T, d, k, out, st));
+  return MOE_OK;
+}
+
+static int layer_status(moe_layer* L, cudaStream_t st) {
+  uint32_t h[2];
+  MOE_CUDA_TRY(cudaMemcpyAsync(h, L->bad_row, 8, cudaMemcpyDeviceToHost, st));
+  MOE_CUDA_TRY(cudaStreamSynchronize(st));
+  if (h[0] != 0xFFFFFFFFu) return set_error(MOE_EINVAL, "gate_top1: non-finite logit at row %u", h[0]);
+  if (h[1] != 0xFFFFFFFFu) return set_error(MOE_EINVAL, "build_routing_plan: expert out of range");
+  return MOE_OK;
+}
+
+extern "C" {
+
+int moe_layer_create(const moe_layer_desc* desc, moe_layer** out) {
+  return layer_create_impl(desc, out, false);
+}
+int moe_layer_create_device(const moe_layer_desc* desc, moe_layer** out) {
+  return layer_create_impl(desc, out, true);
+}
+int moe_layer_destroy(moe_layer* L) {
+  delete L;
+  return MOE_OK;
+}
+int moe_layer_reserve(moe_layer* L, int64_t T, int k) {
+  if (!L) return set_error(MOE_EINVAL, "layer: null");
+  return layer_reserve(L, T, k);
+}
+int moe_layer_forward(moe_layer* L, const uint16_t* x, const uint8_t* finished, int64_t T, int k,
+                      int mode, uint16_t* out, moe_stream_t stream) {
+  if (!L) return set_error(MOE_EINVAL, "layer: null");
+  return layer_forward(L, x, finished, T, k, mode, out, S(stream));
+}
+int moe_layer_forward_host(moe_layer* L, const uint16_t* x_host, const uint8_t* fin_host,
+                           int64_t T, int k, int mode, uint16_t* out_host, moe_stream_t stream) {
+  if (!L) return set_error(MOE_EINVAL, "layer: null");
+  if (T <= 0) return set_error(MOE_EINVAL, "moe_ffn: no rows");
+  TRY(layer_reserve(L, T, k));
+  cudaStream_t st = S(stream);
+  MOE_CUDA_TRY(cudaMemcpyAsync(L->dx, x_host, T * L->d * 2, cudaMemcpyHostToDevice, st));
+  if (fin_host) MOE_CUDA_TRY(cudaMemcpyAsync(L->dfin, fin_host, T, cudaMemcpyHostToDevice, st));
+  TRY(layer_forward(L, L->dx, fin_host ? L->dfin : nullptr, T, k, mode, L->dout, st));
+  MOE_CUDA_TRY(cudaMemcpyAsync(out_host, L->dout, T * L->d * 2, cudaMemcpyDeviceToHost, st));
+  return layer_status(L, st);
+}
+int moe_layer_status(moe_layer* L, moe_stream_t stream) {
+  if (!L) return set_error(MOE_EINVAL, "layer: null");
+  return layer_status(L, S(stream));
+}
+int moe_layer_routing(moe_layer* L, const uint32_t** expert, const uint16_t** scale,
+                      const uint32_t** perm, const uint32_t** inv, const uint32_t** offsets,
+                      const uint32_t** active) {
+  if (!L) return set_error(MOE_EINVAL, "layer: null");
+  if (expert) *expert = L->expert;
+  if (scale) *scale = L->scale;
+  if (perm) *perm = L->perm;
+  if (inv) *inv = L->inv;
+  if (offsets) *offsets = L->offsets;
+  if (active) *active = L->active;
+  return MOE_OK;
+}
+
+int moe_layer_traffic(moe_layer* L, uint64_t* t6, moe_stream_t stream) {
+  if (!L || !t6) return set_error(MOE_EINVAL, "layer: null");
+  std::vector<uint32_t> off(L->E + 1);
+  MOE_CUDA_TRY(cudaMemcpyAsync(off.data(), L->offsets, (L->E + 1) * 4, cudaMemcpyDeviceToHost,
+                               S(stream)));
+  MOE_CUDA_TRY(cudaStreamSynchronize(S(stream)));
+  const uint64_t d = L->d, f = L->f, E = L->E, T = L->last_T, Sl = T * L->last_k;
+  uint64_t ew = 0, ea = 0, eo = 0;
+  auto gemm = [&](uint64_t m, uint64_t n) {
+    for (uint64_t e = 0; e < E; ++e) {
+      const uint64_t rows = off[e + 1] - off[e];
+      if (rows == 0) continue;
+      ew += L->bits == 16 ? m * n * 2 : (L->bits == 8 ? m * n : m * n / 2) + n * 2;
+      ea += (rows * m + n) * 2;
+      eo += rows * n * 2;
+    }
+  };
+  gemm(d, f);
+  gemm(f, d);
+  // other: LN, gate, permute, unpermute, residual (model.cpp:303-347)
+  uint64_t ow = d * E * 2;
+  uint64_t oa = (T * d + 2 * d) * 2 + (T * d + E) * 2 + Sl * d * 2 + Sl * d * 2 + 2 * T * d * 2;
+  uint64_t oo = T * d * 2 + T * E * 4 + Sl * d * 2 + Sl * d * 2 + T * d * 2;
+  t6[0] = ew;
+  t6[1] = ea;
+  t6[2] = eo;
+  t6[3] = ow;
+  t6[4] = oa;
+  t6[5] = oo;
+  return MOE_OK;
+}
+
+}  // extern "C"

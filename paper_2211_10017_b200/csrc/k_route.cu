@@ -1,0 +1,298 @@
+// k_route.cu -- K3 routing plan + gather, unpermute, K6 combine.
+//
+// build_routing_plan (proj/src/routing.cpp:43-87) is a STABLE counting sort
+// of S = T*k slots by key = finished ? E : expert.  GPU form, three passes:
+//   1. count : per 256-slot block, a shared-memory histogram of keys;
+//   2. scan  : one CTA turns the (block x key) histogram into global key
+//              offsets (= expert_offsets, active_rows) and per-block bases,
+//              and emits the per-expert problem list for the grouped GEMMs;
+//   3. place : per block, each slot's rank among equal keys in slot order is
+//              (rank inside its warp via __match_any_sync + popc) + (equal
+//              keys in earlier warps) -> pos = base + rank; writes perm/inv
+//              and gathers the activation row into expert-sorted order with
+//              16-byte vector copies (permute_rows, routing.cpp:89-97).
+// Everything is integer and order-deterministic: bit-identical to the
+// reference counting sort.
+#include "kernels.cuh"
+
+namespace moecu {
+
+constexpr int kPlanBlock = 256;
+
+int64_t plan_blocks(int64_t S) { return (S + kPlanBlock - 1) / kPlanBlock; }
+
+__device__ __forceinline__ uint32_t slot_key(const uint32_t* expert, const uint8_t* finished,
+                                             int64_t slot, int k, int64_t E, uint32_t* bad) {
+  const uint32_t e = expert[slot];
+  if (e >= (uint32_t)E) atomicMin(bad, (uint32_t)slot);
+  if (finished != nullptr && finished[slot / k] != 0) return (uint32_t)E;
+  return e >= (uint32_t)E ? (uint32_t)E : e;
+}
+
+__global__ void __launch_bounds__(kPlanBlock) plan_count_kernel(
+    const uint32_t* __restrict__ expert, const uint8_t* __restrict__ finished, int64_t S, int k,
+    int64_t E, uint32_t* __restrict__ blockcnt, uint32_t* bad) {
+  extern __shared__ uint32_t hist[];
+  for (int64_t i = threadIdx.x; i <= E; i += kPlanBlock) hist[i] = 0;
+  __syncthreads();
+  const int64_t slot = (int64_t)blockIdx.x * kPlanBlock + threadIdx.x;
+  if (slot < S) atomicAdd(&hist[slot_key(expert, finished, slot, k, E, bad)], 1u);
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i <= E; i += kPlanBlock)
+    blockcnt[(int64_t)blockIdx.x * (E + 1) + i] = hist[i];
+}
+
+// One CTA of 1024 threads; thread j owns key j (keys E+1 <= 1024*ITER).
+__global__ void __launch_bounds__(1024) plan_scan_kernel(
+    const uint32_t* __restrict__ blockcnt, int64_t nblk, int64_t E,
+    uint32_t* __restrict__ blockbase, uint32_t* __restrict__ offsets,
+    uint32_t* __restrict__ problems, uint32_t* __restrict__ active) {
+  __shared__ uint32_t tot[1024 + 1];
+  __shared__ uint32_t warp_sum[32];
+  const int tid = threadIdx.x;
+  const int64_t keys = E + 1;
+  uint32_t t = 0;
+  if (tid < keys)
+    for (int64_t b = 0; b < nblk; ++b) t += blockcnt[b * keys + tid];
+  // exclusive scan of t over tid (block-wide)
+  const int lane = tid & 31, warp = tid >> 5;
+  uint32_t incl = t;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) warp_sum[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t ws = warp_sum[lane];
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, ws, o);
+      if (lane >= o) ws += v;
+    }
+    warp_sum[lane] = ws;  // inclusive over warps
+  }
+  __syncthreads();
+  const uint32_t excl = incl - t + (warp > 0 ? warp_sum[warp - 1] : 0);
+  if (tid < keys) {
+    tot[tid] = excl;
+    uint32_t run = excl;
+    for (int64_t b = 0; b < nblk; ++b) {
+      blockbase[b * keys + tid] = run;
+      run += blockcnt[b * keys + tid];
+    }
+    offsets[tid] = excl;  // offsets[E] = start of the finished tail = active_rows
+  }
+  __syncthreads();
+  if (tid < E && problems != nullptr) {
+    problems[3 * tid] = (uint32_t)tid;
+    problems[3 * tid + 1] = tot[tid];
+    problems[3 * tid + 2] = tot[tid + 1];
+  }
+  if (tid == 0 && active != nullptr) *active = tot[E];
+}
+
+__global__ void __launch_bounds__(kPlanBlock) plan_place_kernel(
+    const uint32_t* __restrict__ expert, const uint8_t* __restrict__ finished, int64_t S, int k,
+    int64_t E, const uint32_t* __restrict__ blockbase, uint32_t* __restrict__ perm,
+    uint32_t* __restrict__ inv, const uint16_t* __restrict__ src, int64_t cols,
+    uint16_t* __restrict__ dst, uint32_t* bad) {
+  extern __shared__ uint32_t wcnt[];  // [8 warps][E+1], then pos/slot lists
+  const int64_t keys = E + 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t i = threadIdx.x; i < 8 * keys; i += kPlanBlock) wcnt[i] = 0;
+  __syncthreads();
+  const int64_t slot = (int64_t)blockIdx.x * kPlanBlock + threadIdx.x;
+  const bool live = slot < S;
+  const uint32_t key = live ? slot_key(expert, finished, slot, k, E, bad) : 0xFFFFFFFFu;
+  const uint32_t peers = __match_any_sync(0xffffffffu, key);
+  const uint32_t lt = (1u << lane) - 1u;
+  const uint32_t rank_w = __popc(peers & lt);
+  if (live && (peers >> lane) == 1u) wcnt[warp * keys + key] = __popc(peers);  // highest peer
+  __syncthreads();
+  uint32_t* pos_l = wcnt + 8 * keys;
+  if (live) {
+    uint32_t before = 0;
+    for (int w = 0; w < warp; ++w) before += wcnt[w * keys + key];
+    const uint32_t pos = blockbase[(int64_t)blockIdx.x * keys + key] + before + rank_w;
+    perm[pos] = (uint32_t)slot;
+    inv[slot] = pos;
+    pos_l[threadIdx.x] = pos;
+  }
+  if (dst == nullptr) return;
+  __syncthreads();
+  // gather: dst[pos] = src[slot / k], one warp per row, 16-byte vectors
+  const int64_t nslots = ::min((int64_t)kPlanBlock, S - (int64_t)blockIdx.x * kPlanBlock);
+  const bool vec = (cols % 8) == 0;
+  for (int64_t i = warp; i < nslots; i += kPlanBlock / 32) {
+    const int64_t s = (int64_t)blockIdx.x * kPlanBlock + i;
+    const uint16_t* a = src + (s / k) * cols;
+    uint16_t* b = dst + (int64_t)pos_l[i] * cols;
+    if (vec) {
+      const uint4* a4 = reinterpret_cast<const uint4*>(a);
+      uint4* b4 = reinterpret_cast<uint4*>(b);
+      for (int64_t c = lane; c < cols / 8; c += 32) b4[c] = a4[c];
+    } else {
+      for (int64_t c = lane; c < cols; c += 32) b[c] = a[c];
+    }
+  }
+}
+
+int launch_routing_plan(const uint32_t* expert, const uint8_t* finished, int64_t T, int k,
+                        int64_t E, uint32_t* perm, uint32_t* inv, uint32_t* offsets,
+                        uint32_t* problems, uint32_t* active, const PlanWork& w,
+                        const uint16_t* gather_src, int64_t cols, uint16_t* gather_dst,
+                        cudaStream_t st) {
+  const int64_t S = T * k;
+  if (S == 0) return MOE_OK;
+  if (E + 1 > 1024) return set_error(MOE_EINVAL, "routing plan: at most 1023 experts");
+  const int64_t nblk = plan_blocks(S);
+  plan_count_kernel<<<(unsigned)nblk, kPlanBlock, (E + 1) * 4, st>>>(expert, finished, S, k, E,
+                                                                      w.blockcnt, w.bad);
+  note_launch();
+  plan_scan_kernel<<<1, 1024, 0, st>>>(w.blockcnt, nblk, E, w.blockbase, offsets, problems,
+                                       active);
+  note_launch();
+  const size_t smem = (8 * (E + 1) + kPlanBlock) * 4;
+  plan_place_kernel<<<(unsigned)nblk, kPlanBlock, smem, st>>>(
+      expert, finished, S, k, E, w.blockbase, perm, inv, gather_src, cols, gather_dst, w.bad);
+  note_launch();
+  return check_launch("routing_plan");
+}
+
+// ------------------------------------------------------------------ permute
+__global__ void permute_kernel(const uint16_t* __restrict__ x, int64_t cols,
+                               const uint32_t* __restrict__ perm, int64_t S, int k,
+                               uint16_t* __restrict__ xp) {
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= S) return;
+  const uint16_t* a = x + (int64_t)(perm[row] / k) * cols;
+  uint16_t* b = xp + row * cols;
+  if (cols % 8 == 0) {
+    for (int64_t c = lane; c < cols / 8; c += 32)
+      reinterpret_cast<uint4*>(b)[c] = reinterpret_cast<const uint4*>(a)[c];
+  } else {
+    for (int64_t c = lane; c < cols; c += 32) b[c] = a[c];
+  }
+}
+
+int launch_permute(const uint16_t* x, int64_t cols, const uint32_t* perm, int64_t S, int k,
+                   uint16_t* xp, cudaStream_t st) {
+  if (S == 0) return MOE_OK;
+  permute_kernel<<<(unsigned)((S + 7) / 8), 256, 0, st>>>(x, cols, perm, S, k, xp);
+  note_launch();
+  return check_launch("permute");
+}
+
+// ---------------------------------------------------------------- unpermute
+// out[perm[i]] = half_mul(y[i], scale[perm[i]]) for i < active, other rows 0
+// (routing.cpp:99-116).  Rows are zeroed by the caller.
+__global__ void unpermute_kernel(const uint16_t* __restrict__ y, int64_t T, int64_t cols,
+                                 const uint32_t* __restrict__ perm,
+                                 const uint32_t* __restrict__ active,
+                                 const uint16_t* __restrict__ scale, uint16_t* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (i >= T || i >= (int64_t)*active) return;
+  const uint32_t r = perm[i];
+  const uint16_t s = scale[r];
+  for (int64_t c = lane; c < cols; c += 32) out[(int64_t)r * cols + c] = hmul(y[i * cols + c], s);
+}
+
+int launch_unpermute_scale(const uint16_t* y, int64_t T, int64_t cols, const uint32_t* perm,
+                           const uint32_t* active, const uint16_t* scale, uint16_t* out,
+                           cudaStream_t st) {
+  if (T == 0) return MOE_OK;
+  MOE_CUDA_TRY(cudaMemsetAsync(out, 0, (size_t)T * cols * 2, st));
+  unpermute_kernel<<<(unsigned)((T + 7) / 8), 256, 0, st>>>(y, T, cols, perm, active, scale, out);
+  note_launch();
+  return check_launch("unpermute");
+}
+
+// ------------------------------------------------------------------ combine
+// out[r] = finished[r] ? x[r]
+//        : (((x[r] (+) y[inv[r,0]]*s0) (+) y[inv[r,1]]*s1) ...)  fp16 RN each op
+// (model.cpp:334-346 with routing.cpp:106-114; slot order for k > 1).
+__global__ void combine_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict__ y,
+                               const uint32_t* __restrict__ inv,
+                               const uint16_t* __restrict__ scale,
+                               const uint8_t* __restrict__ finished, int64_t T, int64_t d, int k,
+                               uint16_t* __restrict__ out) {
+  const int64_t chunks = d / 8;
+  const int64_t total = T * chunks;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / chunks, c = i % chunks;
+    uint4 acc = reinterpret_cast<const uint4*>(x + r * d)[c];
+    if (finished == nullptr || finished[r] == 0) {
+      for (int s = 0; s < k; ++s) {
+        const uint32_t p = inv[r * k + s];
+        const uint32_t sc = scale[r * k + s];
+        const uint32_t s2 = sc | (sc << 16);
+        const uint4 yv = reinterpret_cast<const uint4*>(y + (int64_t)p * d)[c];
+        uint32_t* a = reinterpret_cast<uint32_t*>(&acc);
+        const uint32_t* b = reinterpret_cast<const uint32_t*>(&yv);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint32_t prod, sum;
+          asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(prod) : "r"(b[q]), "r"(s2));
+          asm("add.rn.f16x2 %0, %1, %2;" : "=r"(sum) : "r"(a[q]), "r"(prod));
+          a[q] = sum;
+        }
+      }
+    }
+    reinterpret_cast<uint4*>(out + r * d)[c] = acc;
+  }
+}
+
+__global__ void combine_scalar_kernel(const uint16_t* __restrict__ x,
+                                      const uint16_t* __restrict__ y,
+                                      const uint32_t* __restrict__ inv,
+                                      const uint16_t* __restrict__ scale,
+                                      const uint8_t* __restrict__ finished, int64_t T, int64_t d,
+                                      int k, uint16_t* __restrict__ out) {
+  const int64_t total = T * d;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / d, c = i % d;
+    uint16_t acc = x[i];
+    if (finished == nullptr || finished[r] == 0)
+      for (int s = 0; s < k; ++s)
+        acc = hadd(acc, hmul(y[(int64_t)inv[r * k + s] * d + c], scale[r * k + s]));
+    out[i] = acc;
+  }
+}
+
+int launch_combine(const uint16_t* x, const uint16_t* y, const uint32_t* inv,
+                   const uint16_t* scale, const uint8_t* finished, int64_t T, int64_t d, int k,
+                   uint16_t* out, cudaStream_t st) {
+  if (T == 0) return MOE_OK;
+  const int64_t work = d % 8 == 0 ? T * d / 8 : T * d;
+  const unsigned blocks = (unsigned)std::min<int64_t>((work + 255) / 256, 148 * 16);
+  if (d % 8 == 0)
+    combine_kernel<<<blocks, 256, 0, st>>>(x, y, inv, scale, finished, T, d, k, out);
+  else
+    combine_scalar_kernel<<<blocks, 256, 0, st>>>(x, y, inv, scale, finished, T, d, k, out);
+  note_launch();
+  return check_launch("combine");
+}
+
+// --------------------------------------------------------------- EP counts
+__global__ void ep_counts_kernel(const uint32_t* __restrict__ offsets, int64_t E, int G,
+                                 int64_t* __restrict__ counts) {
+  const int g = threadIdx.x;
+  if (g >= G) return;
+  const int64_t per = E / G;
+  counts[g] = (int64_t)offsets[(g + 1) * per] - (int64_t)offsets[g * per];
+}
+
+int launch_ep_rank_counts(const uint32_t* offsets, int64_t E, int G, int64_t* counts,
+                          cudaStream_t st) {
+  if (G < 1 || G > 1024 || E % G != 0)
+    return set_error(MOE_EINVAL, "ep: n_experts must be divisible by the world size");
+  ep_counts_kernel<<<1, 1024, 0, st>>>(offsets, E, G, counts);
+  note_launch();
+  return check_launch("ep_rank_counts");
+}
+
+}  // namespace moecu

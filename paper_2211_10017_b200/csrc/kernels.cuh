@@ -1,0 +1,85 @@
+// kernels.cuh -- internal launch interface between the C-ABI (abi.cu) and the
+// kernel translation units.  Every launcher returns a moe_cuda.h status.
+#pragma once
+
+#include <algorithm>
+
+#include "../../include/moe_cuda.h"
+#include "common.cuh"
+
+namespace moecu {
+
+constexpr int kFeatTile = 128;  // output columns per GEMM tile (MMA M)
+constexpr int kKBlock = 64;     // inputs per k-block (one 128-byte fp16 row)
+
+__host__ __device__ constexpr int wblock_bytes(int bits) {
+  return bits == 4 ? 4096 : bits == 8 ? 8192 : 16384;
+}
+
+int sm_count();
+
+// k_quant.cu
+int launch_quantize(const uint16_t* w, int64_t e, int64_t m, int64_t n, int bits,
+                    uint8_t* packed, uint16_t* scales, unsigned long long* bad,
+                    cudaStream_t st);
+int launch_pack_int4(const uint8_t* v, int64_t count, uint8_t* out, unsigned long long* bad,
+                     cudaStream_t st);
+int launch_unpack_int4(const uint8_t* p, int64_t count, uint8_t* out, cudaStream_t st);
+int launch_dequantize(const uint8_t* packed, const uint16_t* scales, int64_t e, int64_t m,
+                      int64_t n, int bits, int fast, uint16_t debias, uint16_t* out,
+                      cudaStream_t st);
+int64_t tiled_bytes(int64_t e, int64_t m, int64_t n, int bits);
+int launch_tile_weights(const void* src, int64_t e, int64_t m, int64_t n, int bits,
+                        void* tiled, cudaStream_t st);
+
+// k_gate.cu
+int launch_layer_norm(const uint16_t* x, int64_t T, int64_t d, const uint16_t* g,
+                      const uint16_t* b, uint16_t* out, cudaStream_t st);
+int launch_gate_logits(const uint16_t* xn, int64_t T, int64_t d, const uint16_t* gw,
+                       const uint16_t* gb, int64_t E, float* logits, cudaStream_t st);
+int launch_gate_topk(const float* logits, int64_t T, int64_t E, int k, uint32_t* expert,
+                     uint16_t* scale, uint32_t* bad_row, cudaStream_t st);
+
+// k_route.cu
+struct PlanWork {
+  uint32_t* blockcnt;   // nblk * (E+1)
+  uint32_t* blockbase;  // nblk * (E+1)
+  uint32_t* bad;        // 1 (expert out of range: lowest slot)
+};
+int64_t plan_blocks(int64_t S);
+int launch_routing_plan(const uint32_t* expert, const uint8_t* finished, int64_t T, int k,
+                        int64_t E, uint32_t* perm, uint32_t* inv, uint32_t* offsets,
+                        uint32_t* problems, uint32_t* active, const PlanWork& w,
+                        const uint16_t* gather_src, int64_t cols, uint16_t* gather_dst,
+                        cudaStream_t st);
+int launch_permute(const uint16_t* x, int64_t cols, const uint32_t* perm, int64_t S, int k,
+                   uint16_t* xp, cudaStream_t st);
+int launch_unpermute_scale(const uint16_t* y, int64_t T, int64_t cols, const uint32_t* perm,
+                           const uint32_t* active, const uint16_t* scale, uint16_t* out,
+                           cudaStream_t st);
+int launch_combine(const uint16_t* x, const uint16_t* y, const uint32_t* inv,
+                   const uint16_t* scale, const uint8_t* finished, int64_t T, int64_t d, int k,
+                   uint16_t* out, cudaStream_t st);
+int launch_ep_rank_counts(const uint32_t* offsets, int64_t E, int G, int64_t* counts,
+                          cudaStream_t st);
+
+// k_gemm_exact.cu / k_gemm_tc.cu
+struct GemmArgs {
+  const uint16_t* x;
+  int64_t rows, m;
+  const uint32_t* problems;
+  int64_t np;
+  const void* tiled;
+  const uint16_t* scales;
+  int bits;
+  int64_t E, n;
+  const uint16_t* bias;
+  int relu;
+  uint16_t* out;
+  uint16_t debias;  // 0x6408 (W4) / 0x6480 (W8), MOE_FAULT_INJECT aware
+  int64_t rows_hint;  // expected rows per problem (tile-size choice)
+};
+int launch_gemm_exact(const GemmArgs& a, cudaStream_t st);
+int launch_gemm_tc(const GemmArgs& a, cudaStream_t st);
+
+}  // namespace moecu

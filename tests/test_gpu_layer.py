@@ -1,0 +1,126 @@
+"""GPU parity for the whole MoE layer (moe_ffn_forward replacement).
+
+EXACT mode must equal the oracle's batched forward AND the per-token oracle
+bit for bit (test_model.cpp:303-330 contract), at fp16/int8/int4 and top-1/
+top-2, with finished rows.  FAST mode: routing (expert indices, scales,
+perm, inv, offsets) bit-exact, outputs within TOL_FAST (normalized max error
+of the MoE contribution out - x)."""
+import numpy as np
+import pytest
+
+from conftest import bits16, norm_err, to_dev, to_np
+
+pytestmark = pytest.mark.gpu
+
+TOL_FAST = 1e-2
+
+
+def _layer(lw, bits, q=None):
+    from paper_2211_10017_b200.ops import MoELayer
+    return MoELayer(lw.ln_g, lw.ln_b, lw.gw, lw.gb, lw.w1, lw.b1, lw.w2, lw.b2, bits=bits, q=q)
+
+
+def _case(d, f, E, T, seed, fin_frac=0.25):
+    from oracle.oracle import random_layer
+    lw = random_layer(d, f, E, seed=seed)
+    rng = np.random.default_rng(seed + 1)
+    x = rng.standard_normal((T, d)).astype(np.float16)
+    fin = (rng.random(T) < fin_frac).astype(np.uint8)
+    return lw, x, fin
+
+
+@pytest.mark.parametrize("bits", [16, 8, 4])
+@pytest.mark.parametrize("k", [1, 2])
+def test_layer_exact_bit_exact(cuda, oracle, bits, k):
+    lw, x, fin = _case(64, 96, 8, 33, seed=404 + bits + k)
+    L = _layer(lw, bits)
+    q = tuple(to_np(t) for t in L.quant) if bits != 16 else None
+    want, diag = oracle.moe_forward(lw, x, fin, k=k, bits=bits, q=q, diagnostics=True)
+    got = to_np(L.forward(to_dev(x), to_dev(fin), k=k, mode=0))
+    assert np.array_equal(bits16(got), bits16(want))
+    per_tok = oracle.moe_per_token(lw, x, fin, k=k, bits=bits, q=q)
+    assert np.array_equal(bits16(got), bits16(per_tok))
+    r = L.routing(33, k)
+    for key in ("expert", "perm", "inv", "offsets"):
+        assert np.array_equal(r[key].reshape(-1), diag[key].reshape(-1)), key
+    assert np.array_equal(r["scale"].reshape(-1), diag["scale"].reshape(-1))
+    assert r["active"] == diag["active"]
+    # finished rows pass through exactly
+    assert np.array_equal(bits16(got)[fin == 1], bits16(x)[fin == 1])
+
+
+def test_layer_quantized_on_gpu_matches_oracle_quantizer(cuda, oracle):
+    lw, x, fin = _case(128, 256, 8, 20, seed=7)
+    L = _layer(lw, 4)
+    q1, s1 = oracle.quantize(lw.w1, 4)
+    assert np.array_equal(to_np(L.quant[0]), q1)
+    assert np.array_equal(bits16(to_np(L.quant[1])), bits16(s1))
+
+
+@pytest.mark.parametrize("bits", [4, 8, 16])
+@pytest.mark.parametrize("k", [1, 2])
+def test_layer_fast_routing_exact_output_tolerance(cuda, oracle, bits, k):
+    lw, x, fin = _case(256, 512, 8, 200, seed=11 + bits + k, fin_frac=0.1)
+    L = _layer(lw, bits)
+    q = tuple(to_np(t) for t in L.quant) if bits != 16 else None
+    want, diag = oracle.moe_forward(lw, x, fin, k=k, bits=bits, q=q, diagnostics=True)
+    got = to_np(L.forward(to_dev(x), to_dev(fin), k=k, mode=1))
+    r = L.routing(200, k)
+    for key in ("expert", "perm", "inv", "offsets", "scale"):
+        assert np.array_equal(r[key].reshape(-1), diag[key].reshape(-1)), key
+    xf = x.astype(np.float64)
+    err = norm_err(got.astype(np.float64) - xf, want.astype(np.float64) - xf)
+    assert err <= TOL_FAST, err
+    assert np.array_equal(bits16(got)[fin == 1], bits16(x)[fin == 1])
+
+
+def test_layer_host_path_equals_device_path(cuda):
+    lw, x, fin = _case(128, 256, 16, 77, seed=21)
+    L = _layer(lw, 4)
+    for mode in (0, 1):
+        a = to_np(L.forward(to_dev(x), to_dev(fin), k=2, mode=mode))
+        b = L.forward_host(x, fin, k=2, mode=mode)
+        assert np.array_equal(bits16(a), bits16(b))
+
+
+def test_layer_rejects_non_finite(cuda):
+    lw, x, fin = _case(64, 64, 4, 8, seed=3)
+    L = _layer(lw, 4)
+    x[5, 3] = np.inf
+    with pytest.raises(ValueError, match="non-finite logit at row 5"):
+        L.forward_host(x, fin, k=1, mode=1)
+
+
+def test_layer_traffic_matches_reference_accounting(cuda, oracle):
+    lw, x, fin = _case(64, 96, 8, 40, seed=5)
+    L = _layer(lw, 4)
+    L.forward(to_dev(x), to_dev(fin), k=1, mode=0)
+    t = L.traffic()
+    _, diag = oracle.moe_forward(lw, x, fin, k=1, bits=4,
+                                 q=tuple(to_np(a) for a in L.quant), diagnostics=True)
+    off = diag["offsets"]
+    d, f, E, T = 64, 96, 8, 40
+    active = [e for e in range(E) if off[e + 1] > off[e]]
+    rows = [int(off[e + 1] - off[e]) for e in active]
+    ew = sum((d * f // 2 + f * 2) + (f * d // 2 + d * 2) for _ in active)
+    ea = sum((r * d + f) * 2 + (r * f + d) * 2 for r in rows)
+    eo = sum(r * f * 2 + r * d * 2 for r in rows)
+    assert t["expert"] == (ew, ea, eo)
+
+
+@pytest.mark.parametrize("T,k", [(4096, 2), (1, 1), (64, 1)])
+def test_c2_c3_shapes_fast_vs_exact_and_per_token_rows(cuda, oracle, T, k):
+    """BASELINE config 2 (E=8, d=512, f=2048, int4, top-2, T=4096) and
+    decode-shaped rows at the same width: fast within tolerance of exact
+    (exact == reference semantics); 16 sampled rows vs the per-token oracle."""
+    lw, x, fin = _case(512, 2048, 8, T, seed=1234, fin_frac=0.0)
+    L = _layer(lw, 4)
+    q = tuple(to_np(a) for a in L.quant)
+    xd = to_dev(x)
+    ex = to_np(L.forward(xd, None, k=k, mode=0))
+    fa = to_np(L.forward(xd, None, k=k, mode=1))
+    xf = x.astype(np.float64)
+    assert norm_err(fa.astype(np.float64) - xf, ex.astype(np.float64) - xf) <= TOL_FAST
+    rows = np.random.default_rng(0).choice(T, size=min(T, 16), replace=False)
+    want = oracle.moe_per_token(lw, x[rows], None, k=k, bits=4, q=q)
+    assert np.array_equal(bits16(ex[rows]), bits16(want))
