@@ -23,7 +23,8 @@
 
 #ifdef __CUDACC__
 #define MOE_HD __host__ __device__ __forceinline__
-#define MOE_EXPF_TAB_QUAL __device__ __constant__
+// global (L1-cached), not __constant__: lanes index the table divergently
+#define MOE_EXPF_TAB_QUAL __device__ const
 #else
 #define MOE_HD static inline
 #define MOE_EXPF_TAB_QUAL static const

@@ -62,9 +62,105 @@ __global__ void __launch_bounds__(128) layer_norm_kernel(const uint16_t* __restr
   }
 }
 
+// Row-per-thread form for d % 8 == 0 (the hot path).  The serial chains are
+// the latency floor, so each thread owns one row's chain and the block
+// streams 64 rows x 64 columns at a time through a 4-deep cp.async ring;
+// three passes (sum, centred sum of squares, normalise) re-stream the rows
+// (the second and third hit L2).  Reading 8 fp16 per LDS.128 from 144-byte
+// row pitches is bank-conflict free per quarter warp.
+constexpr int LN_R = 64, LN_KC = 64, LN_NS = 4, LN_PITCH = LN_KC + 8;
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__global__ void __launch_bounds__(LN_R) layer_norm_rows_kernel(const uint16_t* __restrict__ x,
+                                                               int64_t T, int64_t d,
+                                                               const uint16_t* __restrict__ g,
+                                                               const uint16_t* __restrict__ b,
+                                                               uint16_t* __restrict__ out) {
+  __shared__ __align__(16) uint16_t buf[LN_NS][LN_R][LN_PITCH];
+  const int tid = threadIdx.x;
+  const int64_t r0 = (int64_t)blockIdx.x * LN_R, row = r0 + tid;
+  const int nch = (int)((d + LN_KC - 1) / LN_KC);
+  auto issue = [&](int c) {
+    if (c < nch) {
+      uint16_t(*dst)[LN_PITCH] = buf[c % LN_NS];
+      for (int i = tid; i < LN_R * (LN_KC / 8); i += LN_R) {
+        const int rr = i / (LN_KC / 8), ch = i % (LN_KC / 8);
+        const int64_t gr = r0 + rr, col = (int64_t)c * LN_KC + ch * 8;
+        const bool ok = gr < T && col < d;
+        cp_async16(&dst[rr][ch * 8], ok ? x + gr * d + col : x, ok);
+      }
+    }
+    cp_async_commit();
+  };
+  float mean = 0.f, inv = 0.f;
+  for (int pass = 0; pass < 3; ++pass) {
+    float acc = 0.f;
+    for (int c = 0; c < LN_NS - 1; ++c) issue(c);
+    for (int c = 0; c < nch; ++c) {
+      cp_async_wait<LN_NS - 2>();
+      __syncthreads();
+      issue(c + LN_NS - 1);
+      const uint16_t* rp = buf[c % LN_NS][tid];
+      const int kc = (int)::min((int64_t)LN_KC, d - (int64_t)c * LN_KC);
+      for (int j = 0; j < kc; j += 8) {
+        const uint4 v = *reinterpret_cast<const uint4*>(rp + j);
+        const uint16_t* h = reinterpret_cast<const uint16_t*>(&v);
+        if (pass == 0) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc = __fadd_rn(acc, h2f(h[i]));
+        } else if (pass == 1) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float dx = __fsub_rn(h2f(h[i]), mean);
+            acc = __fadd_rn(acc, __fmul_rn(dx, dx));
+          }
+        } else if (row < T) {
+          const int64_t col = (int64_t)c * LN_KC + j;
+          const uint4 gv = *reinterpret_cast<const uint4*>(g + col);
+          const uint4 bv = *reinterpret_cast<const uint4*>(b + col);
+          const uint16_t* gh = reinterpret_cast<const uint16_t*>(&gv);
+          const uint16_t* bh = reinterpret_cast<const uint16_t*>(&bv);
+          uint4 o;
+          uint16_t* oh = reinterpret_cast<uint16_t*>(&o);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            oh[i] = f2h(__fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(h2f(h[i]), mean), inv), h2f(gh[i])),
+                                  h2f(bh[i])));
+          *reinterpret_cast<uint4*>(out + row * d + col) = o;
+        }
+      }
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+    if (pass == 0) {
+      mean = __fdiv_rn(acc, (float)d);
+    } else if (pass == 1) {
+      const float var = __fdiv_rn(acc, (float)d);
+      inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(var, 1e-5f)));
+    }
+  }
+}
+
 int launch_layer_norm(const uint16_t* x, int64_t T, int64_t d, const uint16_t* g,
                       const uint16_t* b, uint16_t* out, cudaStream_t st) {
   if (T == 0) return MOE_OK;
+  if (d % 8 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+      (reinterpret_cast<uintptr_t>(out) & 15) == 0 && (reinterpret_cast<uintptr_t>(g) & 15) == 0 &&
+      (reinterpret_cast<uintptr_t>(b) & 15) == 0) {
+    layer_norm_rows_kernel<<<(unsigned)((T + LN_R - 1) / LN_R), LN_R, 0, st>>>(x, T, d, g, b, out);
+    note_launch();
+    return check_launch("layer_norm");
+  }
   const size_t smem = (size_t)4 * ((d + 3) & ~int64_t(3)) * sizeof(float);
   if (smem > 48 * 1024) {
     static bool set = false;
@@ -80,80 +176,72 @@ int launch_layer_norm(const uint16_t* x, int64_t T, int64_t d, const uint16_t* g
 }
 
 // ----------------------------------------------------------------- gate logits
-// Each thread owns a 4-row x 4-expert block of serial chains (16 independent
-// accumulators, so the FMA latency of one chain is hidden by the others).
-// A 64-thread block covers (64/EB)*4 rows x EB*4 experts, EB = expert groups
-// chosen so small E does not waste lanes; x rows and gate-weight columns are
-// staged in shared memory 32 k at a time (padded rows: conflict-free).
-constexpr int GL_THREADS = 64;
-constexpr int GL_KC = 32;
+// One thread per row holding EC expert chains (EC in {1,2,4,8}, picked so
+// T*E/EC threads fill the GPU: the serial k-chain latency is the floor).  The
+// thread streams its own xn row with 16-byte loads; the block's EC gate
+// columns are staged as f32 in shared memory and read as warp broadcasts.
+constexpr int GL_ROWS = 128, GL_KCH = 256;
 
-__global__ void __launch_bounds__(GL_THREADS) gate_logits_kernel(
+template <int EC>
+__global__ void __launch_bounds__(GL_ROWS) gate_logits_kernel(
     const uint16_t* __restrict__ xn, int64_t T, int64_t d, const uint16_t* __restrict__ gw,
-    const uint16_t* __restrict__ gb, int64_t E, int EB, float* __restrict__ logits) {
-  extern __shared__ float gl_sm[];
-  const int RB = GL_THREADS / EB;
-  float* xs = gl_sm;                          // [RB*4][GL_KC+1]
-  float* ws = gl_sm + RB * 4 * (GL_KC + 1);   // [EB*4][GL_KC+1]
+    const uint16_t* __restrict__ gb, int64_t E, int vec, float* __restrict__ logits) {
+  __shared__ __align__(16) float ws[GL_KCH][EC];
   const int tid = threadIdx.x;
-  const int rg = tid / EB, eg = tid % EB;
-  const int64_t r0 = (int64_t)blockIdx.x * RB * 4;
-  const int64_t e0 = (int64_t)blockIdx.y * EB * 4;
-  float acc[4][4];
+  const int64_t row = (int64_t)blockIdx.x * GL_ROWS + tid;
+  const int64_t e0 = (int64_t)blockIdx.y * EC;
+  const bool live = row < T;
+  const uint16_t* xr = xn + (live ? row : 0) * d;
+  float acc[EC];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
-
-  for (int64_t k0 = 0; k0 < d; k0 += GL_KC) {
-    const int kc = (int)::min((int64_t)GL_KC, d - k0);
+  for (int j = 0; j < EC; ++j) acc[j] = 0.f;
+  for (int64_t k0 = 0; k0 < d; k0 += GL_KCH) {
+    const int kc = (int)::min((int64_t)GL_KCH, d - k0);
     __syncthreads();
-    for (int i = tid; i < RB * 4 * GL_KC; i += GL_THREADS) {
-      const int rr = i / GL_KC, kk = i % GL_KC;
-      const int64_t r = r0 + rr;
-      xs[rr * (GL_KC + 1) + kk] = (r < T && kk < kc) ? h2f(xn[r * d + k0 + kk]) : 0.f;
-    }
-    for (int i = tid; i < EB * 4 * GL_KC; i += GL_THREADS) {
-      const int kk = i / (EB * 4), ee = i % (EB * 4);
-      const int64_t e = e0 + ee;
-      ws[ee * (GL_KC + 1) + kk] = (e < E && kk < kc) ? h2f(gw[(k0 + kk) * E + e]) : 0.f;
+    for (int i = tid; i < GL_KCH * EC; i += GL_ROWS) {
+      const int kk = i / EC, j = i % EC;
+      ws[kk][j] = (kk < kc && e0 + j < E) ? h2f(gw[(k0 + kk) * E + e0 + j]) : 0.f;
     }
     __syncthreads();
-    const float* xr = xs + rg * 4 * (GL_KC + 1);
-    const float* wr = ws + eg * 4 * (GL_KC + 1);
-    for (int kk = 0; kk < kc; ++kk) {
-      float xv[4], wv[4];
+    if (!live) continue;
+    if (vec) {
+      for (int kk = 0; kk < kc; kk += 8) {
+        const uint4 v = *reinterpret_cast<const uint4*>(xr + k0 + kk);
+        const uint16_t* h = reinterpret_cast<const uint16_t*>(&v);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) xv[i] = xr[i * (GL_KC + 1) + kk];
+        for (int i = 0; i < 8; ++i) {
+          const float xv = h2f(h[i]);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) wv[j] = wr[j * (GL_KC + 1) + kk];
+          for (int j = 0; j < EC; ++j) acc[j] = fmaf(xv, ws[kk + i][j], acc[j]);  // exact product
+        }
+      }
+    } else {
+      for (int kk = 0; kk < kc; ++kk) {
+        const float xv = h2f(xr[k0 + kk]);
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(xv[i], wv[j], acc[i][j]);  // exact product
+        for (int j = 0; j < EC; ++j) acc[j] = fmaf(xv, ws[kk][j], acc[j]);
+      }
     }
   }
+  if (!live) return;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int64_t r = r0 + rg * 4 + i;
-    if (r >= T) continue;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int64_t e = e0 + eg * 4 + j;
-      if (e < E) logits[r * E + e] = __fadd_rn(acc[i][j], h2f(gb[e]));
-    }
-  }
+  for (int j = 0; j < EC; ++j)
+    if (e0 + j < E) logits[row * E + e0 + j] = __fadd_rn(acc[j], h2f(gb[e0 + j]));
 }
 
 int launch_gate_logits(const uint16_t* xn, int64_t T, int64_t d, const uint16_t* gw,
                        const uint16_t* gb, int64_t E, float* logits, cudaStream_t st) {
   if (T == 0) return MOE_OK;
-  int EB = 1;
-  while (EB < 8 && EB * 4 < E) EB *= 2;
-  const int RB = GL_THREADS / EB;
-  const size_t smem = (size_t)(RB * 4 + EB * 4) * (GL_KC + 1) * sizeof(float);
-  dim3 grid((unsigned)((T + RB * 4 - 1) / (RB * 4)), (unsigned)((E + EB * 4 - 1) / (EB * 4)));
-  gate_logits_kernel<<<grid, GL_THREADS, smem, st>>>(xn, T, d, gw, gb, E, EB, logits);
+  int EC = 8;
+  while (EC > 1 && (EC > E || T * ((E + EC - 1) / EC) < 16384)) EC >>= 1;
+  const int vec = (d % 8 == 0) && (reinterpret_cast<uintptr_t>(xn) & 15) == 0;
+  dim3 grid((unsigned)((T + GL_ROWS - 1) / GL_ROWS), (unsigned)((E + EC - 1) / EC));
+  switch (EC) {
+    case 8: gate_logits_kernel<8><<<grid, GL_ROWS, 0, st>>>(xn, T, d, gw, gb, E, vec, logits); break;
+    case 4: gate_logits_kernel<4><<<grid, GL_ROWS, 0, st>>>(xn, T, d, gw, gb, E, vec, logits); break;
+    case 2: gate_logits_kernel<2><<<grid, GL_ROWS, 0, st>>>(xn, T, d, gw, gb, E, vec, logits); break;
+    default: gate_logits_kernel<1><<<grid, GL_ROWS, 0, st>>>(xn, T, d, gw, gb, E, vec, logits); break;
+  }
   note_launch();
   return check_launch("gate_logits");
 }

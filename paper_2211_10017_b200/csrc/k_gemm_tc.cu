@@ -5,30 +5,38 @@
 //
 //   D[feature, token] = sum_k  Wq[k, feature] * X[token, k]
 //
-// * The MMA's M side is 128 output features of one expert; A = dequantised
-//   weights living in TMEM (tcgen05 "TS" form), B = a BN-token x 64-k
-//   activation tile in shared memory (TMA, 128-byte swizzle, K-major).
-//   Putting the weights in TMEM keeps the dequantised tile out of shared
-//   memory entirely: shared memory only carries the packed int4/int8 codes
-//   (bulk copies) and the activation tile.
-// * Dequant warps (one per TMEM sub-partition) turn each feature's 64 codes
-//   into 32 fp16x2 registers with the magic I2F trick (lop3 + hsub2 per 2
-//   values; proj/include/moeinfer/dequant.hpp:39-63) and tcgen05.st them.
-//   The per-channel scale is NOT applied here -- the MMA runs on the exact
-//   small integers (code - offset) and the epilogue multiplies the f32
-//   accumulator by s[feature] (the reference instead rounds q*s to fp16
-//   before the dot product; both are within the stated tolerance, see
+// * MMA M = 128 output features of one expert, N = BN tokens (up to 256),
+//   K = 16 per instruction, kind::f16 with f32 accumulation in TMEM
+//   (double-buffered: 2 x BN columns), both operands in shared memory
+//   (128-byte swizzle, K-major): A = the dequantised weight tile, B = the
+//   activation tile (TMA).
+// * Dequant warps (one per 32-feature slice, two groups alternating
+//   k-blocks) turn each feature's 64 codes -- bulk-copied into shared memory
+//   packed -- into fp16 with the magic I2F trick
+//   (proj/include/moeinfer/dequant.hpp:39-63; 9 ops per 8 int4 codes) and
+//   store them swizzled as the A tile.  The per-channel scale is applied to
+//   the f32 accumulator in the epilogue instead of to each weight (the
+//   reference rounds q*s to fp16 first; both stay inside the tolerance,
 //   DESIGN.md §4).
-// * One elected thread issues tcgen05.mma kind::f16 (M=128, N=BN, K=16)
-//   into a double-buffered TMEM accumulator; epilogue warps tcgen05.ld it,
-//   apply scale, bias, ReLU, round to fp16 and store through a shared-memory
-//   transpose (16-byte global stores).
+// * ONE thread runs the MMA loop.  Measured on this B200
+//   (scripts/mma_bench{2,3}.cu): issuing a tcgen05.mma costs ~90 cycles of
+//   the issuing thread, so an instruction must carry >= 128 tensor cycles
+//   (M=128 x N=256) to stay tensor-bound; a warp-wide wait + lane-0 issue
+//   costs ~650 cycles per 4-MMA k-block; and SS-mode N=256 MMAs keep full
+//   rate while shared memory also absorbs ~130 B/clk of stores plus ~60
+//   B/clk of TMA fills (this kernel needs ~100 B/clk).
+// * Shared-memory stages (TMA + bulk) and A stages are separate rings.
 //
-// Roles (384 threads): warp 0 TMA/bulk producer, warp 1 MMA issuer, warp 2
-// TMEM allocator, warp 3 tile-table builder, warps 4-7 dequant, warps 8-11
-// epilogue.  Tiles: (problem, token tile of BN, feature tile of 128), token
-// tile major so concurrently running CTAs share activation tiles in L2.
+// Roles (512 threads): warp 0 TMA/bulk producer, warp 1 MMA issuer, warp 2
+// TMEM allocator, warp 3 tile-table builder, warps 4-11 dequant (two groups
+// of four), warps 12-15 epilogue.  Tiles: (problem, token tile of BN,
+// feature tile of 128), token-tile major so concurrently running CTAs share
+// activation tiles in L2.
 #include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 
 #include "kernels.cuh"
 
@@ -36,30 +44,37 @@ namespace moecu {
 
 namespace tc {
 
-constexpr int kThreads = 384;
+constexpr int kDqGroups = 2;                            // dequant warp groups
+constexpr int kEpiGroups = 2;                           // epilogue warp groups
+constexpr int kThreads = 32 * (4 + 4 * kDqGroups + 4 * kEpiGroups);
 constexpr int kMaxProblems = 1024;
 
 template <int BITS, int BN>
 struct Cfg {
   static constexpr int WBYTES = wblock_bytes(BITS);
-  static constexpr int BBYTES = BN * 128;  // BN rows x 64 fp16
+  static constexpr int BBYTES = BN * 128;   // BN rows x 64 fp16
+  static constexpr int ABYTES = 128 * 128;  // 128 features x 64 fp16
   static constexpr int STAGE = BBYTES + WBYTES;
-  static constexpr int BUDGET = 176 * 1024;
-  static constexpr int NST_SMEM = BUDGET / STAGE;
-  static constexpr int NST_TMEM = (512 - 2 * BN) / 32;
-  static constexpr int NST0 = NST_SMEM < NST_TMEM ? NST_SMEM : NST_TMEM;
-  static constexpr int NST = NST0 > 12 ? 12 : NST0;
-  static constexpr int ACOL0 = 2 * BN;  // first TMEM column of the A stages
-  static constexpr int EPI = 4 * 32 * 32 * 2;
-  // [stages][B | W] | epilogue staging | barriers | tile table
-  static constexpr int OFF_EPI = NST * STAGE;
+  static constexpr int EPI_WBUF = 32 * 32 * 2;                   // per warp: [32][32] fp16
+  static constexpr int EPI = kEpiGroups * 4 * EPI_WBUF;
+  static constexpr int BUDGET = 220 * 1024 - EPI;                // stages + A ring
+  static constexpr int NA = 2;                                   // A stages
+  static constexpr int NS0 = (BUDGET - NA * ABYTES) / STAGE;
+  static constexpr int NS = NS0 > 8 ? 8 : NS0;                   // TMA stages
+  // [TMA stages][B | W] | [A stages] | epilogue staging | barriers | table
+  static constexpr int OFF_A = NS * STAGE;
+  static constexpr int OFF_EPI = OFF_A + NA * ABYTES;
   static constexpr int OFF_BAR = OFF_EPI + EPI;
-  static constexpr int NBAR = 3 * NST + 4;
+  static constexpr int NBAR = 2 * NS + 2 * NA + 4;
   static constexpr int OFF_TMEMPTR = OFF_BAR + NBAR * 8;
   static constexpr int OFF_TABLE = OFF_TMEMPTR + 16;
   static constexpr int SMEM = OFF_TABLE + (kMaxProblems + 1) * 4 + 1024;  // + align slack
-  static_assert(NST >= 2, "pipeline too shallow");
-  static_assert(2 * BN + NST * 32 <= 512, "TMEM overflow");
+  static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128
+                                 : 2 * BN <= 256 ? 256 : 512;
+  static_assert(NS >= 2, "pipeline too shallow");
+  static_assert(2 * BN <= 512, "TMEM overflow");
+  static_assert(BBYTES % 1024 == 0 && WBYTES % 1024 == 0, "stage alignment");
+  static_assert(SMEM <= 227 * 1024, "shared memory");
 };
 
 struct Tile {
@@ -85,6 +100,11 @@ __device__ __forceinline__ Tile decode(const uint32_t* table, int np, const uint
   return x;
 }
 
+// Output tensor maps: box {32 features, 32 >> i rows}, i = 0..5.
+struct OutMaps {
+  CUtensorMap map[6];
+};
+
 struct Params {
   const uint8_t* tiled;
   const uint16_t* scales;
@@ -94,21 +114,34 @@ struct Params {
   int64_t m, n, np, nft, nkb;
   int relu;
   uint32_t debias2;
+  uint32_t hibias2;  // -(64 + debias - 1024) in both halves (i2f_u4_fast)
+  unsigned long long* trace;  // dev-only role timestamps of CTA 0 (MOE_TC_TRACE), else null
+  int dbg;  // dev-only ablation bits (MOE_TC_DBG): 1 no epilogue, 2 no A stores, 4 no W load
 };
+
+constexpr int kTraceN = 1024;  // events per role slot
+#define TC_TRACE(slot, idx)                                                      \
+  do {                                                                           \
+    if (P.trace != nullptr && blockIdx.x == 0 && (idx) < kTraceN)               \
+      P.trace[(slot) * kTraceN + (idx)] = clock64();                             \
+  } while (0)
 
 template <int BITS, int BN>
 __global__ void __launch_bounds__(kThreads, 1)
-    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const Params P) {
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ OutMaps O,
+                   const Params P) {
   using C = Cfg<BITS, BN>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-byte alignment for the 128B-swizzle atoms, by pointer arithmetic on
+  // the shared array so the compiler keeps shared-space (LDS/STS) accesses.
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
-  uint64_t* full = bars;               // TMA+bulk landed      (count 1 + tx)
-  uint64_t* afull = bars + C::NST;     // A stage in TMEM      (count 4)
-  uint64_t* empty = bars + 2 * C::NST; // MMA done with stage  (count 1, commit)
-  uint64_t* tfull = bars + 3 * C::NST; // accumulator ready    (count 1, commit)
-  uint64_t* tempty = tfull + 2;        // accumulator drained  (count 4)
+  uint64_t* full = bars;                 // smem stage landed  (1 arrive + tx)
+  uint64_t* empty = full + C::NS;        // smem stage free    (MMA commit)
+  uint64_t* afull = empty + C::NS;       // A stage written    (4 dequant warps)
+  uint64_t* aempty = afull + C::NA;      // A stage free       (MMA commit)
+  uint64_t* tfull = aempty + C::NA;      // accumulator ready  (MMA commit)
+  uint64_t* tempty = tfull + 2;          // accumulator drained (4 epilogue warps)
   uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + C::OFF_TMEMPTR);
   uint32_t* table = reinterpret_cast<uint32_t*>(smem + C::OFF_TABLE);
 
@@ -119,14 +152,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) tma_prefetch_desc(&tmap_x);
   } else if (warp == 1) {
     if (lane == 0) {
-      for (int i = 0; i < C::NST; ++i) {
+      for (int i = 0; i < C::NS; ++i) {
         mbar_init(&full[i], 1);
-        mbar_init(&afull[i], 4);
         mbar_init(&empty[i], 1);
+      }
+      for (int i = 0; i < C::NA; ++i) {
+        mbar_init(&afull[i], 4);
+        mbar_init(&aempty[i], 1);
       }
       for (int i = 0; i < 2; ++i) {
         mbar_init(&tfull[i], 1);
-        mbar_init(&tempty[i], 4);
+        mbar_init(&tempty[i], 4 * kEpiGroups);
       }
       fence_barrier_init();
     }
@@ -163,65 +199,73 @@ __global__ void __launch_bounds__(kThreads, 1)
         const Tile T = decode(table, np, P.problems, t, P.nft, BN);
         const uint8_t* wsrc = P.tiled + ((T.e * P.nft + T.ft) * P.nkb) * (int64_t)C::WBYTES;
         for (int64_t kb = 0; kb < P.nkb; ++kb, ++it) {
-          const int s = it % C::NST;
-          const uint32_t ph = (it / C::NST) & 1;
-          mbar_wait(&empty[s], ph ^ 1);
+          const int s = it % C::NS;
+          mbar_wait(&empty[s], ((it / C::NS) & 1) ^ 1);
+          TC_TRACE(0, it);
           uint8_t* sb = smem + s * C::STAGE;
-          mbar_arrive_expect_tx(&full[s], C::STAGE);
+          mbar_arrive_expect_tx(&full[s], (P.dbg & 4) ? C::BBYTES : C::STAGE);
           tma_load_2d(sb, &tmap_x, &full[s], (int)(kb * 64), (int)T.row0);
-          bulk_load(sb + C::BBYTES, wsrc + kb * C::WBYTES, C::WBYTES, &full[s]);
+          if (!(P.dbg & 4)) bulk_load(sb + C::BBYTES, wsrc + kb * C::WBYTES, C::WBYTES, &full[s]);
         }
       }
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------- MMA issuer
-    constexpr uint32_t idesc = umma_idesc_f16(128, BN);
-    uint32_t it = 0, local = 0;
-    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
-      const int acc = local & 1;
-      const uint32_t aph = (local >> 1) & 1;
-      mbar_wait(&tempty[acc], aph ^ 1);
-      tc_fence_after();
-      const uint32_t d_tmem = tmem + acc * BN;
-      for (int64_t kb = 0; kb < P.nkb; ++kb, ++it) {
-        const int s = it % C::NST;
-        const uint32_t ph = (it / C::NST) & 1;
-        mbar_wait(&full[s], ph);
-        mbar_wait(&afull[s], ph);
+    // The whole loop (waits included) runs on one thread: see header.
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_f16(128, BN);
+      const uint32_t smem_base = smem_u32(smem);
+      uint32_t it = 0, local = 0;
+      for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
+        const int acc = local & 1;
+        mbar_wait(&tempty[acc], ((local >> 1) & 1) ^ 1);
         tc_fence_after();
-        if (lane == 0) {  // the same thread issues and commits (commit tracks its own MMAs)
-          const uint64_t bdesc = umma_desc_sw128(smem_u32(smem + s * C::STAGE));
+        const uint32_t d_tmem = tmem + acc * BN;
+        for (int64_t kb = 0; kb < P.nkb; ++kb, ++it) {
+          const int s = it % C::NS, a = it % C::NA;
+          mbar_wait(&full[s], (it / C::NS) & 1);
+          TC_TRACE(1, it);
+          mbar_wait(&afull[a], (it / C::NA) & 1);
+          tc_fence_after();
+          TC_TRACE(2, it);
+          const uint64_t bdesc = umma_desc_sw128(smem_base + s * C::STAGE);
+          const uint64_t adesc = umma_desc_sw128(smem_base + C::OFF_A + a * C::ABYTES);
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            tc_mma_ts(d_tmem, tmem + C::ACOL0 + s * 32 + kk * 8, bdesc + (uint64_t)(kk * 2),
-                      idesc, (kb | kk) != 0 ? 1u : 0u);
+          for (int kk = 0; kk < 4; ++kk)  // K advance of 16 fp16 = 32 bytes = 2 descriptor units
+            tc_mma_ss(d_tmem, adesc + (uint64_t)(kk * 2), bdesc + (uint64_t)(kk * 2), idesc,
+                      (kb | kk) != 0 ? 1u : 0u);
           tc_commit(&empty[s]);
+          tc_commit(&aempty[a]);
+          TC_TRACE(3, it);
         }
-        __syncwarp();
+        tc_commit(&tfull[acc]);
       }
-      if (lane == 0) tc_commit(&tfull[acc]);
-      __syncwarp();
     }
-  } else if (warp >= 4 && warp < 8) {
+  } else if (warp >= 4 && warp < 4 + 4 * kDqGroups) {
     // ------------------------------------------------------------ dequant
-    const int q = warp - 4;
+    // kDqGroups groups of 4 warps (one warp per TMEM sub-partition) take
+    // alternate k-blocks, so one group's shared-memory/ALU latency overlaps
+    // the other's tcgen05.st.
+    const int q = (warp - 4) & 3, grp = (warp - 4) >> 2;
     const int feat = q * 32 + lane;
-    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
     uint32_t it = 0;
     for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
       for (int64_t kb = 0; kb < P.nkb; ++kb, ++it) {
-        const int s = it % C::NST;
-        const uint32_t ph = (it / C::NST) & 1;
-        mbar_wait(&full[s], ph);
+        if ((int)(it % kDqGroups) != grp) continue;
+        const int s = it % C::NS, a = it % C::NA;
+        mbar_wait(&full[s], (it / C::NS) & 1);
+        mbar_wait(&aempty[a], ((it / C::NA) & 1) ^ 1);
+        if (lane == 0 && q == 0) TC_TRACE(4, it);
         const uint4* wblk = reinterpret_cast<const uint4*>(smem + s * C::STAGE + C::BBYTES);
-        uint32_t a[32];
+        uint32_t v[32];
         if constexpr (BITS == 4) {
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const uint4 c = wblk[h * 128 + feat];
             const uint32_t wd[4] = {c.x, c.y, c.z, c.w};
 #pragma unroll
-            for (int w = 0; w < 4; ++w) i2f_u4(wd[w], P.debias2, &a[h * 16 + w * 4]);
+            for (int w = 0; w < 4; ++w)
+              i2f_u4_fast(wd[w], P.debias2, P.hibias2, &v[h * 16 + w * 4]);
           }
         } else if constexpr (BITS == 8) {
 #pragma unroll
@@ -229,34 +273,49 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint4 c = wblk[c4 * 128 + feat];
             const uint32_t wd[4] = {c.x, c.y, c.z, c.w};
 #pragma unroll
-            for (int w = 0; w < 4; ++w) i2f_u8(wd[w], P.debias2, &a[c4 * 8 + w * 2]);
+            for (int w = 0; w < 4; ++w) i2f_u8(wd[w], P.debias2, &v[c4 * 8 + w * 2]);
           }
         } else {
 #pragma unroll
           for (int c8 = 0; c8 < 8; ++c8) {
             const uint4 c = wblk[c8 * 128 + feat];
-            a[c8 * 4 + 0] = c.x;
-            a[c8 * 4 + 1] = c.y;
-            a[c8 * 4 + 2] = c.z;
-            a[c8 * 4 + 3] = c.w;
+            v[c8 * 4 + 0] = c.x;
+            v[c8 * 4 + 1] = c.y;
+            v[c8 * 4 + 2] = c.z;
+            v[c8 * 4 + 3] = c.w;
           }
         }
-        tmem_st_32x32b_x32(tmem + lane_addr + C::ACOL0 + s * 32, a);
-        tc_wait_st();
-        tc_fence_before();
+        // A tile row `feat`: 128 bytes, 16-byte chunk c (k = 8c..8c+7) stored at
+        // chunk position c ^ (feat & 7) -- the 128B-swizzle K-major atom layout
+        // (conflict-free: a quarter warp covers 8 rows x distinct chunk slots).
+        if (!(P.dbg & 2)) {
+          uint8_t* arow = smem + C::OFF_A + a * C::ABYTES + feat * 128;
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            *reinterpret_cast<uint4*>(arow + ((c ^ (feat & 7)) << 4)) =
+                make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+        }
+        fence_proxy_async_smem();  // generic-proxy stores -> visible to tcgen05.mma
         __syncwarp();
-        if (lane == 0) mbar_arrive(&afull[s]);
+        if (lane == 0) mbar_arrive(&afull[a]);
+        if (lane == 0 && q == 0) TC_TRACE(5, it);
       }
     }
-  } else if (warp >= 8) {
+  } else if (warp >= 4 + 4 * kDqGroups) {
     // ----------------------------------------------------------- epilogue
-    const int q = warp - 8;
+    // kEpiGroups groups of 4 warps take alternate 32-token chunks of a tile.
+    // Every warp works alone: it drains its 32 features x 32 tokens from TMEM,
+    // stages them as [token][32 features] fp16 (one 64-byte row per token),
+    // and lane 0 TMA-stores the block -- one box per power-of-two run of
+    // valid rows, so a problem's last chunk never writes the next expert's
+    // rows.  Staging is double-buffered per warp; no cross-warp barriers.
+    const int q = warp & 3, ew = warp - 4 - 4 * kDqGroups, eg = ew >> 2;
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
-    uint16_t* stage = reinterpret_cast<uint16_t*>(smem + C::OFF_EPI) + q * 32 * 32;
+    uint16_t* stage0 = reinterpret_cast<uint16_t*>(smem + C::OFF_EPI + ew * C::EPI_WBUF);
+    uint32_t cc = 0;  // chunks processed by this warp
     uint32_t local = 0;
     for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
       const int acc = local & 1;
-      const uint32_t aph = (local >> 1) & 1;
       const Tile T = decode(table, np, P.problems, t, P.nft, BN);
       const int64_t col = T.ft * 128 + q * 32 + lane;
       float sc = 1.0f, bi = 0.0f;
@@ -264,34 +323,58 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (BITS != 16) sc = h2f(P.scales[T.e * P.n + col]);
         bi = h2f(P.bias[T.e * P.n + col]);
       }
-      mbar_wait(&tfull[acc], aph);
+      mbar_wait(&tfull[acc], (local >> 1) & 1);
       tc_fence_after();
+      if (lane == 0 && ew == 0) TC_TRACE(6, local);
+      // only the columns holding this tile's rows need draining
+      const int64_t live = T.r1 - T.row0;
+      const int ncols = (int)(live < BN ? (live + 31) / 32 * 32 : BN);
+      const bool slice_live = T.ft * 128 + q * 32 < P.n;
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
+      for (int c0 = eg * 32; c0 < ((P.dbg & 1) ? 0 : ncols); c0 += 32 * kEpiGroups, ++cc) {
+        uint16_t* stg = stage0;  // read back before the next chunk overwrites it
         uint32_t v[32];
         tmem_ld_32x32b_x32(tmem + lane_addr + acc * BN + c0, v);
         tc_wait_ld();
+        if (lane == 0 && ew == 0) TC_TRACE(9, cc);
+        // two tokens per cvt (f16x2, ReLU folded in), then a 2x2 transpose with
+        // the neighbour lane so each 32-bit store holds two adjacent features
+        // of one token: even lanes write row j, odd lanes row j+1.
+        uint32_t* srow = reinterpret_cast<uint32_t*>(stg + (lane & 1) * 32 + (lane & ~1));
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          float h = fmaf(__uint_as_float(v[j]), sc, bi);
-          if (P.relu && !(h > 0.0f)) h = 0.0f;
-          stage[j * 32 + lane] = f2h(h);
+        for (int j = 0; j < 32; j += 2) {
+          const float h0 = fmaf(__uint_as_float(v[j]), sc, bi);
+          const float h1 = fmaf(__uint_as_float(v[j + 1]), sc, bi);
+          uint32_t own;
+          if (P.relu)
+            asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(own) : "f"(h1), "f"(h0));
+          else
+            asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(own) : "f"(h1), "f"(h0));
+          const uint32_t other = __shfl_xor_sync(0xffffffffu, own, 1);
+          srow[j * 16] = (lane & 1) ? __byte_perm(other, own, 0x7632)
+                                    : __byte_perm(own, other, 0x5410);
         }
         __syncwarp();
+        if (lane == 0 && ew == 0) TC_TRACE(10, cc);
+        // read back as 16-byte vectors: lane -> (row lane/4 + 8i, 8 features)
+        const int nrow = (int)::min((int64_t)32, T.r1 - (T.row0 + c0));
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int row = i * 8 + (lane >> 2), ch = lane & 3;
-          const int64_t pos = T.row0 + c0 + row;
-          const int64_t c8 = T.ft * 128 + q * 32 + ch * 8;
-          const uint4 val = *reinterpret_cast<const uint4*>(stage + row * 32 + ch * 8);
-          if (pos < T.r1 && c8 < P.n) *reinterpret_cast<uint4*>(P.out + pos * P.n + c8) = val;
+          const uint4 val = *reinterpret_cast<const uint4*>(stg + row * 32 + ch * 8);
+          if (row < nrow && slice_live)
+            *reinterpret_cast<uint4*>(P.out + (T.row0 + c0 + row) * P.n + T.ft * 128 + q * 32 +
+                                      ch * 8) = val;
         }
         __syncwarp();
+        if (lane == 0 && ew == 0) TC_TRACE(11, cc);
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0 && ew == 0) TC_TRACE(7, local);
     }
+    if (lane == 0) bulk_wait<0>();  // all output rows written before the CTA retires
   }
   tc_fence_before();
   __syncthreads();
@@ -331,6 +414,17 @@ static int run_tc(const GemmArgs& a, cudaStream_t st) {
                       CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(MOE_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  tc::OutMaps O;
+  for (int i = 0; i < 6; ++i) {
+    const cuuint64_t odims[2] = {(cuuint64_t)a.n, (cuuint64_t)a.rows};
+    const cuuint64_t ostr[1] = {(cuuint64_t)a.n * 2};
+    const cuuint32_t obox[2] = {32, (cuuint32_t)(32 >> i)};
+    r = encode(&O.map[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a.out, odims, ostr, obox, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+      return set_error(MOE_ECUDA, "cuTensorMapEncodeTiled(out) failed (%d)", (int)r);
+  }
   tc::Params P;
   P.tiled = static_cast<const uint8_t*>(a.tiled);
   P.scales = a.scales;
@@ -344,19 +438,46 @@ static int run_tc(const GemmArgs& a, cudaStream_t st) {
   P.nkb = (a.m + 63) / 64;
   P.relu = a.relu;
   P.debias2 = (uint32_t)a.debias | ((uint32_t)a.debias << 16);
+  {
+    // value of the debias constant minus 1024 (8 healthy, 9 under MOE_FAULT_INJECT)
+    const int off = (int)(a.debias & 0x3FF);
+    const uint16_t hb = (uint16_t)(0x8000 | (21 << 10) | (off << 4));  // -(64 + off), 2^6 binade
+    P.hibias2 = (uint32_t)hb | ((uint32_t)hb << 16);
+  }
   static bool attr_set = false;
   if (!attr_set) {
     MOE_CUDA_TRY(cudaFuncSetAttribute(tc::gemm_tc_kernel<BITS, BN>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr_set = true;
   }
-  tc::gemm_tc_kernel<BITS, BN><<<sm_count(), tc::kThreads, C::SMEM, st>>>(tmap, P);
+  const char* trace_path = std::getenv("MOE_TC_TRACE");  // development instrumentation
+  P.trace = nullptr;
+  P.dbg = std::getenv("MOE_TC_DBG") ? std::atoi(std::getenv("MOE_TC_DBG")) : 0;
+  if (trace_path) MOE_CUDA_TRY(cudaMalloc(&P.trace, 12 * tc::kTraceN * 8));
+  if (P.trace) MOE_CUDA_TRY(cudaMemset(P.trace, 0, 12 * tc::kTraceN * 8));
+  tc::gemm_tc_kernel<BITS, BN><<<sm_count(), tc::kThreads, C::SMEM, st>>>(tmap, O, P);
   note_launch();
-  return check_launch("gemm_tc");
+  const int rc = check_launch("gemm_tc");
+  if (P.trace) {
+    std::vector<unsigned long long> h(12 * tc::kTraceN);
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h.data(), P.trace, h.size() * 8, cudaMemcpyDeviceToHost);
+    cudaFree(P.trace);
+    if (FILE* f = std::fopen(trace_path, "ab")) {
+      const int64_t hdr[4] = {BITS, BN, C::NS * 100 + C::NA, P.nkb};
+      std::fwrite(hdr, 8, 4, f);
+      std::fwrite(h.data(), 8, h.size(), f);
+      std::fclose(f);
+    }
+  }
+  return rc;
 }
 
 template <int BITS>
 static int run_tc_bits(const GemmArgs& a, cudaStream_t st) {
+  // token-tile width from the expected rows per problem (wider MMAs amortise
+  // the per-instruction issue cost; narrower ones waste less on small experts)
+  if (a.rows_hint >= 160) return run_tc<BITS, 256>(a, st);
   if (a.rows_hint >= 96) return run_tc<BITS, 128>(a, st);
   if (a.rows_hint >= 40) return run_tc<BITS, 64>(a, st);
   return run_tc<BITS, 32>(a, st);

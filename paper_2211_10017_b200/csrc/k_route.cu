@@ -153,10 +153,14 @@ int launch_routing_plan(const uint32_t* expert, const uint8_t* finished, int64_t
                                        active);
   note_launch();
   const size_t smem = (8 * (E + 1) + kPlanBlock) * 4;
+  // The row gather runs as its own wide launch (one warp per row): folding
+  // it into plan_place left only S/256 CTAs to move S*cols*2 bytes.
   plan_place_kernel<<<(unsigned)nblk, kPlanBlock, smem, st>>>(
-      expert, finished, S, k, E, w.blockbase, perm, inv, gather_src, cols, gather_dst, w.bad);
+      expert, finished, S, k, E, w.blockbase, perm, inv, nullptr, 0, nullptr, w.bad);
   note_launch();
-  return check_launch("routing_plan");
+  const int s1 = check_launch("routing_plan");
+  if (s1 != MOE_OK || gather_dst == nullptr) return s1;
+  return launch_permute(gather_src, cols, perm, S, k, gather_dst, st);
 }
 
 // ------------------------------------------------------------------ permute

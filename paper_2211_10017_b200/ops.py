@@ -197,7 +197,10 @@ class MoELayer:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h:
-            abi.lib().moe_layer_destroy(h)
+            try:
+                abi.lib().moe_layer_destroy(h)
+            except Exception:  # interpreter shutdown
+                pass
             self._h = None
 
     def reserve(self, T, k=1):

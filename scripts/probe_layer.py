@@ -9,7 +9,7 @@ lw = random_layer(d, f, E, seed=1)
 L = MoELayer(lw.ln_g, lw.ln_b, lw.gw, lw.gb, lw.w1, lw.b1, lw.w2, lw.b2, bits=4)
 x = torch.randn(T, d, device="cuda").half()
 L.reserve(T, k)
-for mode in (1, 0):
+for mode in [int(m) for m in os.environ.get('MODES', '1,0').split(',')]:
     for _ in range(3): L.forward(x, None, k=k, mode=mode)
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
