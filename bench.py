@@ -1,0 +1,398 @@
+"""MoE-layer inference benchmark (BASELINE.json metric) -- driver contract.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference]
+                    [--workload c2|c3_1|c3_8|c3_64|c4|c5]
+
+A "step" is one MoE-layer forward (LayerNorm -> gate -> top-k -> routing plan
+-> FFN1 -> FFN2 -> combine + residual) over one batch of synthetic tokens.
+Default workload = BASELINE.json configs[1] (C2): E=8, d_model=512,
+d_ff=2048, int4 per-channel weight-only experts, top-2, 4096 tokens/GPU.
+
+* value   -- device time (CUDA events on the launching stream, max over
+             ranks) of K steps with inputs resident in HBM; weights and inputs
+             rotate over R distinct layer copies whose footprint exceeds 2x L2,
+             so weights stream from HBM every step.
+* e2e     -- the same metric through the C-ABI host-buffer entry point
+             (moe_layer_forward_host): pinned host x -> device, forward,
+             device -> host out, every step.
+* roofline -- the grouped tcgen05 GEMMs (FFN1+FFN2), timed with CUDA events
+             recorded around them inside the forward (moe_layer_profile).
+* cpu_baseline -- the reference engine (oracle/_ref, compiled from the
+             reference sources) on a bounded token sample, rank 0, N=1 only.
+
+--impl reference times the reference CPU implementation (oracle/_ref if
+built, else the oracle port) on the same workload; rank 0 prints, the other
+ranks exit 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MoE-layer tokens/sec (int4 experts) at 1/2/4/8 B200; % of HBM/TC roofline"
+L2_BYTES = 126 * 1024 * 1024
+
+WORKLOADS = {
+    # name: (E, d, f, T per GPU, k, label)
+    "c2": (8, 512, 2048, 4096, 2, "C2: E=8 d_model=512 d_ff=2048 int4 top-2 4096 tokens"),
+    "c1i4": (8, 512, 2048, 256, 1, "C1 shape with int4 experts: E=8 d_model=512 d_ff=2048 top-1 256 tokens"),
+    "c3_1": (32, 1024, 4096, 1, 1, "C3 decode: E=32 d_model=1024 d_ff=4096 int4 top-1 1 token"),
+    "c3_8": (32, 1024, 4096, 8, 1, "C3 decode: E=32 d_model=1024 d_ff=4096 int4 top-1 8 tokens"),
+    "c3_64": (32, 1024, 4096, 64, 1, "C3 decode: E=32 d_model=1024 d_ff=4096 int4 top-1 64 tokens"),
+    "c4": (64, 1024, 4096, 16384, 1, "C4 MoE layer: E=64 d_model=1024 d_ff=4096 int4 top-1 16384 tokens"),
+    "c5": (128, 2048, 8192, 4096, 2, "C5 EP layer: E=128 d_model=2048 d_ff=8192 int4 top-2 4096 tokens/GPU"),
+}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        try:
+            j = json.load(open(p))
+            hbm = j.get("hbm_gbs") or j.get("hbm_GBs")
+            tc = j.get("bf16_tflops")
+            tcs = j.get("bf16_tflops_sustained", tc)
+            if hbm and tc:
+                return float(hbm), float(tc), float(tcs), "measured (MEASURED_PEAKS.json)"
+        except Exception:
+            pass
+    return 6650.0, 1590.0, 1400.0, "fallback (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """NVML sampling of SM clock + throttle reasons during the timed region."""
+
+    REASONS = {
+        "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+        "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80,
+    }
+
+    def __init__(self, index):
+        self.index, self.samples, self.reasons = index, [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # no NVML: record why
+            self.nv, self.err = None, str(e)
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for name, bit in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.nv:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "note": self.err}
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------ distributed
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ------------------------------------------------------------ CPU baseline
+def cpu_reference_rate(E, d, f, k, sample_T, seconds=10.0, max_runs=3, seed=11):
+    """Tokens/s of the reference CPU layer (oracle/_ref) on sample_T tokens,
+    all host threads; falls back to the C oracle port (1 thread)."""
+    import numpy as np
+    from oracle.oracle import Oracle, Reference, random_layer, reference_available
+    lw = random_layer(d, f, E, seed=seed)
+    x = np.random.default_rng(seed + 1).standard_normal((sample_T, d)).astype(np.float16)
+    cores = os.cpu_count() or 1
+    if reference_available():
+        R = Reference().layer(lw, 4, threads=cores)
+        run = lambda: R.forward(x, None, threads=cores, k=k)  # noqa: E731
+        kind, used = "reference", cores
+    else:
+        orc = Oracle()
+        q = (*orc.quantize(lw.w1, 4), *orc.quantize(lw.w2, 4))
+        run = lambda: orc.moe_forward(lw, x, None, k=k, bits=4, q=q)  # noqa: E731
+        kind, used = "port", 1
+    times, t_end = [], time.perf_counter() + seconds
+    while len(times) < max_runs and (not times or time.perf_counter() < t_end):
+        t0 = time.perf_counter()
+        run()
+        times.append(time.perf_counter() - t0)
+    med = statistics.median(times)
+    return sample_T / med, kind, used, med, len(times)
+
+
+def run_reference_arm(args, wl):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import numpy as np
+    from oracle.oracle import Oracle, Reference, random_layer, reference_available
+    E, d, f, T, k, label = wl
+    cores = os.cpu_count() or 1
+    # bounded sample per step: ~1 s of reference CPU work (config C2 at 8 cores)
+    sample_T = int(os.environ.get("MOE_REF_SAMPLE_T", max(1, min(T, 1024 if d * f <= 2 ** 21 else 16))))
+    lw = random_layer(d, f, E, seed=11)
+    x = np.random.default_rng(12).standard_normal((sample_T, d)).astype(np.float16)
+    if reference_available():
+        R = Reference().layer(lw, 4, threads=cores)
+        run = lambda: R.forward(x, None, threads=cores, k=k)  # noqa: E731
+        kind, used = "reference", cores
+    else:
+        orc = Oracle()
+        q = (*orc.quantize(lw.w1, 4), *orc.quantize(lw.w2, 4))
+        run = lambda: orc.moe_forward(lw, x, None, k=k, bits=4, q=q)  # noqa: E731
+        kind, used = "port", 1
+    for _ in range(args.warmup):
+        run()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        run()
+    dt = time.perf_counter() - t0
+    value = args.steps * sample_T / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f16 storage, f32 accumulate (software fp16)",
+        "data": "synthetic (random_model init distributions, seeded)",
+        "config": {"workload": label, "E": E, "d_model": d, "d_ff": f, "tokens": T,
+                   "top_k": k, "bits": 4},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": used, "kind": kind,
+                         "sample": f"{sample_T} of {T} tokens per step, moe_ffn_forward "
+                                   f"(top-{k} via reference functions), threads={used}"},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------ native arm
+def make_layers(E, d, f, T, k, R, device, seed):
+    import torch
+    from paper_2211_10017_b200.ops import MoELayer
+    g = torch.Generator(device=device)
+    layers, xs = [], []
+    for r in range(R):
+        g.manual_seed(seed * 1000 + r)
+        n = lambda shape, s: (torch.randn(shape, generator=g, device=device) * s).half()  # noqa
+        L = MoELayer(
+            ln_g=(1 + 0.1 * torch.randn(d, generator=g, device=device)).half(),
+            ln_b=n((d,), 0.05), gate_w=n((d, E), 1 / math.sqrt(d)), gate_b=n((E,), 0.02),
+            w1=n((E, d, f), 1 / math.sqrt(d)), b1=n((E, f), 0.02),
+            w2=n((E, f, d), 1 / math.sqrt(f)), b2=n((E, d), 0.02), bits=4, device=device)
+        L.quant = None  # keep only the tiled device copy
+        L.reserve(T, k)
+        layers.append(L)
+        xs.append(torch.randn((T, d), generator=g, device=device).half())
+    torch.cuda.synchronize()
+    return layers, xs
+
+
+def run_native(args, wl):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2211_10017_b200 import abi
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    E, d, f, T, k, label = wl
+    per_copy = E * d * f + 2 * T * d * 2 + T * k * (d + f) * 2  # weights + x/out + xp/h
+    R = max(2, min(64, math.ceil(2 * L2_BYTES / per_copy)))
+    layers, xs = make_layers(E, d, f, T, k, R, dev, seed=1 + rank)
+    outs = [torch.empty_like(x) for x in xs]
+    stream = torch.cuda.current_stream()
+
+    def step(i):
+        layers[i % R].forward(xs[i % R], None, k=k, mode=1, out=outs[i % R])
+
+    for i in range(args.warmup):
+        step(i)
+    for L in layers:
+        L.profile(True)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n0 = abi.launch_count()
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for i in range(args.steps):
+            step(i)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = abi.launch_count() - n0
+    if ws > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    stage = {s: 0.0 for s in layers[0].STAGES}
+    nfw = 0
+    for L in layers:
+        st, n = L.profile_read()
+        L.profile(False)
+        nfw += n
+        for s in stage:
+            stage[s] += st[s]
+    if ws > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = ws * args.steps * T / (ms / 1e3)
+
+    # ---- e2e through the C-ABI host-buffer entry point (pinned host memory)
+    xh = [torch.empty((T, d), dtype=torch.float16, pin_memory=True) for _ in range(min(R, 4))]
+    oh = [torch.empty((T, d), dtype=torch.float16, pin_memory=True) for _ in range(min(R, 4))]
+    for i, t in enumerate(xh):
+        t.copy_(xs[i])
+    xh_np = [t.view(torch.int16).numpy().view(np.float16) for t in xh]
+    oh_np = [t.view(torch.int16).numpy().view(np.float16) for t in oh]
+
+    def e2e_step(i):
+        j = i % len(xh)
+        layers[i % R].forward_host(xh_np[j], None, k=k, mode=1, out_host=oh_np[j])
+
+    for i in range(args.warmup):
+        e2e_step(i)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(args.steps):
+        e2e_step(i)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ems = e0.elapsed_time(e1)
+    if ws > 1:
+        t = torch.tensor([ems], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ems = float(t.item())
+    e2e_value = ws * args.steps * T / (ems / 1e3)
+
+    # ---- roofline of the dominant kernel (grouped tcgen05 GEMM, FFN1+FFN2)
+    hbm, tc_burst, tc_sus, peak_src = load_peaks()
+    S = T * k
+    gemm_ms = (stage["ffn1"] + stage["ffn2"]) / max(nfw, 1)
+    flops = 4.0 * S * d * f
+    # decode-shaped workloads are bounded by streaming the active experts' weights
+    active = E * (1 - (1 - 1 / E) ** S)
+    wbytes = active * (d * f + 4 * (f + d)) + S * (d + f) * 2 * 2
+    t_tc, t_hbm = flops / (tc_burst * 1e12), wbytes / (hbm * 1e9)
+    if t_tc >= t_hbm:
+        roof = {"bound": "tensor", "achieved": flops / (gemm_ms * 1e-3) / 1e12, "peak": tc_burst,
+                "unit": "TFLOP/s"}
+        alg = f"4*S*d*f = {flops:.4g} FLOP per step over 2 launches (S=T*k={S})"
+    else:
+        roof = {"bound": "hbm", "achieved": wbytes / (gemm_ms * 1e-3) / 1e9, "peak": hbm,
+                "unit": "GB/s"}
+        alg = (f"active*(d*f + 4(f+d)) + S*(d+f)*4 = {wbytes:.4g} B per step over 2 launches "
+               f"(expected active experts {active:.1f})")
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = load_traffic(args.workload)
+    roof.update({"kernel": "moe_gemm_tc (FFN1 + FFN2, tcgen05 kind::f16, TMEM accumulators)",
+                 "algorithmic": alg, "peak_source": peak_src,
+                 "kernel_ms_per_step": gemm_ms})
+    layer_roof_t = max(t_tc, (active * (d * f + 4 * (f + d)) + 4 * T * d) / (hbm * 1e9))
+    stage_ms = {s: v / max(nfw, 1) for s, v in stage.items()}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f16 (int4 weight-only experts, f32 accumulate)",
+        "data": "synthetic (random_model init distributions, seeded, generated on device)",
+        "config": {"workload": label, "E": E, "d_model": d, "d_ff": f, "tokens_per_gpu": T,
+                   "top_k": k, "bits": 4, "mode": "fast (tcgen05)",
+                   "parallelism": "single" if ws == 1 else f"replicas{ws}",
+                   "l2": f"inputs larger than L2: {R} distinct layer copies + inputs rotated "
+                         f"({R * per_copy / 2**20:.0f} MiB > 2x L2)"},
+        "roofline": roof,
+        "layer_roofline_frac": layer_roof_t / (ms / args.steps * 1e-3),
+        "stage_ms": stage_ms,
+        "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": T * d * 2,
+                "d2h_bytes_per_step": T * d * 2 + 8,
+                "path": "moe_layer_forward_host (C-ABI, pinned host buffers)"},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        sample_T = min(T, 512 if d * f <= 2 ** 21 else 8)
+        rate, kind, cores, med, nrun = cpu_reference_rate(E, d, f, k, sample_T)
+        line["cpu_baseline"] = {"value": rate, "unit": "tokens/s", "cores": cores, "kind": kind,
+                                "sample": f"{sample_T} tokens x {nrun} runs (median "
+                                          f"{med:.2f} s), same E/d/f/top-{k}, int4"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def load_traffic(workload):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        return json.load(open(p)).get(workload)
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    wl = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        run_reference_arm(args, wl)
+    else:
+        run_native(args, wl)
+
+
+if __name__ == "__main__":
+    main()

@@ -187,6 +187,13 @@ int moe_layer_status(moe_layer* L, moe_stream_t stream);
 int moe_layer_routing(moe_layer* L, const uint32_t** expert, const uint16_t** scale,
                       const uint32_t** perm, const uint32_t** inv,
                       const uint32_t** offsets, const uint32_t** active);
+/* Stage timing with CUDA events recorded on the forward's own stream
+ * (bench.py's roofline).  enable != 0 starts (and resets) recording for up
+ * to 512 forwards; read returns the summed milliseconds of the 7 stages
+ * {layer_norm, gate_logits, gate_topk, routing_plan+gather, ffn1, ffn2,
+ * combine} over the recorded forwards (synchronises on the last one). */
+int moe_layer_profile(moe_layer* L, int enable);
+int moe_layer_profile_read(moe_layer* L, double* stage_ms, int* forwards);
 /* Analytic traffic of the last forward, reference accounting
  * (src/grouped_gemm.cpp:155-160, 201-211; src/model.cpp:303-347):
  * out6 = {expert.weight, expert.activation, expert.written,

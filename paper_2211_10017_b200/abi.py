@@ -55,6 +55,8 @@ _SIGS = {
     "moe_layer_status": (_int, [_vp, _vp]),
     "moe_layer_routing": (_int, [_vp] + [_vp] * 6),
     "moe_layer_traffic": (_int, [_vp, _vp, _vp]),
+    "moe_layer_profile": (_int, [_vp, _int]),
+    "moe_layer_profile_read": (_int, [_vp, _vp, _vp]),
     "moe_ep_rank_counts": (_int, [_vp, _i64, _int, _vp, _vp]),
 }
 

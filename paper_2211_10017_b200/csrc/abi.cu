@@ -324,9 +324,15 @@ struct moe_layer {
   int64_t last_T = 0;
   int last_k = 1;
   std::vector<void*> allocs;
+  // stage profiling (moe_layer_profile): kStages+1 events per forward
+  static constexpr int kStages = 7, kProfCap = 512;
+  bool prof = false;
+  int prof_n = 0;
+  std::vector<cudaEvent_t> ev;
 
   ~moe_layer() {
     for (void* p : allocs) cudaFree(p);
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
   }
   template <class T>
   int alloc(T** p, size_t bytes) {
@@ -454,25 +460,44 @@ static int layer_forward(moe_layer* L, const uint16_t* x, const uint8_t* fin, in
   const int64_t d = L->d, f = L->f, E = L->E, S_ = T * k;
   L->last_T = T;
   L->last_k = k;
+  // stage events (profiling only): ev[slot*(kStages+1) + i] before stage i
+  const bool prof = L->prof && L->prof_n < moe_layer::kProfCap;
+  cudaEvent_t* evs = prof ? &L->ev[(size_t)L->prof_n * (moe_layer::kStages + 1)] : nullptr;
+  int stage = 0;
+  auto mark = [&]() -> int {
+    if (evs) MOE_CUDA_TRY(cudaEventRecord(evs[stage], st));
+    ++stage;
+    return MOE_OK;
+  };
   MOE_CUDA_TRY(cudaMemsetAsync(L->bad_row, 0xFF, 8, st));  // bad_row + bad_expert
+  TRY(mark());
   TRY(launch_layer_norm(x, T, d, L->ln_g, L->ln_b, L->xn, st));
+  TRY(mark());
   TRY(launch_gate_logits(L->xn, T, d, L->gw, L->gb, E, L->logits, st));
+  TRY(mark());
   TRY(launch_gate_topk(L->logits, T, E, k, L->expert, L->scale, L->bad_row, st));
+  TRY(mark());
   PlanWork w{L->blockcnt, L->blockbase, L->bad_expert};
   TRY(launch_routing_plan(L->expert, fin, T, k, E, L->perm, L->inv, L->offsets, L->problems,
                           L->active, w, L->xn, d, L->xp, st));
+  TRY(mark());
   const uint16_t db = debias_for(L->bits);
   const int64_t hint = S_ / std::max<int64_t>(1, std::min<int64_t>(E, S_));
   GemmArgs g1{L->xp, S_, d, L->problems, E, L->w1t, L->s1, L->bits, E, f, L->b1, 1, L->h, db, hint};
   GemmArgs g2{L->h, S_, f, L->problems, E, L->w2t, L->s2, L->bits, E, d, L->b2, 0, L->y, db, hint};
   if (mode == MOE_MODE_FAST) {
     TRY(launch_gemm_tc(g1, st));
+    TRY(mark());
     TRY(launch_gemm_tc(g2, st));
   } else {
     TRY(launch_gemm_exact(g1, st));
+    TRY(mark());
     TRY(launch_gemm_exact(g2, st));
   }
+  TRY(mark());
   TRY(launch_combine(x, L->y, L->inv, L->scale, fin, T, d, k, out, st));
+  TRY(mark());
+  if (evs) ++L->prof_n;
   return MOE_OK;
 }
 
@@ -532,6 +557,33 @@ int moe_layer_routing(moe_layer* L, const uint32_t** expert, const uint16_t** sc
   if (inv) *inv = L->inv;
   if (offsets) *offsets = L->offsets;
   if (active) *active = L->active;
+  return MOE_OK;
+}
+
+int moe_layer_profile(moe_layer* L, int enable) {
+  if (!L) return set_error(MOE_EINVAL, "layer: null");
+  if (enable && L->ev.empty()) {
+    L->ev.resize((size_t)moe_layer::kProfCap * (moe_layer::kStages + 1));
+    for (auto& e : L->ev) MOE_CUDA_TRY(cudaEventCreate(&e));
+  }
+  L->prof = enable != 0;
+  L->prof_n = 0;
+  return MOE_OK;
+}
+
+int moe_layer_profile_read(moe_layer* L, double* stage_ms, int* forwards) {
+  if (!L || !stage_ms) return set_error(MOE_EINVAL, "layer: null");
+  for (int i = 0; i < moe_layer::kStages; ++i) stage_ms[i] = 0.0;
+  for (int f = 0; f < L->prof_n; ++f) {
+    cudaEvent_t* e = &L->ev[(size_t)f * (moe_layer::kStages + 1)];
+    MOE_CUDA_TRY(cudaEventSynchronize(e[moe_layer::kStages]));
+    for (int i = 0; i < moe_layer::kStages; ++i) {
+      float ms = 0.f;
+      MOE_CUDA_TRY(cudaEventElapsedTime(&ms, e[i], e[i + 1]));
+      stage_ms[i] += ms;
+    }
+  }
+  if (forwards) *forwards = L->prof_n;
   return MOE_OK;
 }
 

@@ -251,6 +251,21 @@ class MoELayer:
                     offsets=get(ptrs[4], E + 1, np.uint32),
                     active=int(get(ptrs[5], 1, np.uint32)[0]))
 
+    STAGES = ("layer_norm", "gate_logits", "gate_topk", "routing_plan", "ffn1", "ffn2",
+              "combine")
+
+    def profile(self, enable=True):
+        """Start (reset) / stop per-stage CUDA-event timing (moe_layer_profile)."""
+        abi.call("moe_layer_profile", self._h, int(enable))
+
+    def profile_read(self):
+        """(summed ms per stage, forwards recorded) (moe_layer_profile_read)."""
+        import numpy as np
+        ms = np.zeros(len(self.STAGES), np.float64)
+        n = C.c_int()
+        abi.call("moe_layer_profile_read", self._h, C.c_void_p(ms.ctypes.data), C.byref(n))
+        return dict(zip(self.STAGES, ms.tolist())), n.value
+
     def traffic(self, stream=None):
         import numpy as np
         t = np.zeros(6, np.uint64)
