@@ -245,12 +245,15 @@ def run_native(args, wl):
     stream = torch.cuda.current_stream()
 
     def step(i):
-        layers[i % R].forward(xs[i % R], None, k=k, mode=1, out=outs[i % R])
+        # one cached CUDA graph per layer copy (moe_layer_forward_graph)
+        layers[i % R].forward(xs[i % R], None, k=k, mode=1, out=outs[i % R], graph=True)
 
+    for L in layers:  # stage events are captured into each layer's graph
+        L.profile(True)
+    for i in range(R):  # capture pass (untimed)
+        step(i)
     for i in range(args.warmup):
         step(i)
-    for L in layers:
-        L.profile(True)
     torch.cuda.synchronize()
     if ws > 1:
         dist.barrier()
@@ -267,6 +270,8 @@ def run_native(args, wl):
     if ws > 1:
         dist.barrier()
     ms = ev0.elapsed_time(ev1)
+    # each layer's graph carries its stage events: they hold that layer's LAST
+    # replay inside the timed region (R samples)
     stage = {s: 0.0 for s in layers[0].STAGES}
     nfw = 0
     for L in layers:
@@ -331,7 +336,9 @@ def run_native(args, wl):
                f"(expected active experts {active:.1f})")
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["traffic"] = load_traffic(args.workload)
-    roof.update({"kernel": "moe_gemm_tc (FFN1 + FFN2, tcgen05 kind::f16, TMEM accumulators)",
+    kname = ("gemv_kernel<4> (K5 FFN1 + FFN2, mma.sync over the tcgen05 weight tiles)"
+             if S <= 256 else "gemm_tc_kernel<4,BN> (FFN1 + FFN2, tcgen05 kind::f16, TMEM acc)")
+    roof.update({"kernel": kname,
                  "algorithmic": alg, "peak_source": peak_src,
                  "kernel_ms_per_step": gemm_ms})
     layer_roof_t = max(t_tc, (active * (d * f + 4 * (f + d)) + 4 * T * d) / (hbm * 1e9))
@@ -344,7 +351,9 @@ def run_native(args, wl):
         "dtype": "f16 (int4 weight-only experts, f32 accumulate)",
         "data": "synthetic (random_model init distributions, seeded, generated on device)",
         "config": {"workload": label, "E": E, "d_model": d, "d_ff": f, "tokens_per_gpu": T,
-                   "top_k": k, "bits": 4, "mode": "fast (tcgen05)",
+                   "top_k": k, "bits": 4,
+                   "mode": "fast (" + ("K5 dequant-GEMV" if T * k <= 256 else "tcgen05") +
+                           "), one CUDA graph per layer forward",
                    "parallelism": "single" if ws == 1 else f"replicas{ws}",
                    "l2": f"inputs larger than L2: {R} distinct layer copies + inputs rotated "
                          f"({R * per_copy / 2**20:.0f} MiB > 2x L2)"},
@@ -353,7 +362,7 @@ def run_native(args, wl):
         "stage_ms": stage_ms,
         "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": T * d * 2,
                 "d2h_bytes_per_step": T * d * 2 + 8,
-                "path": "moe_layer_forward_host (C-ABI, pinned host buffers)"},
+                "path": "moe_layer_forward_host (C-ABI, pinned host buffers, cached graph)"},
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }

@@ -17,9 +17,11 @@
  * Numerics modes:
  *   MOE_MODE_EXACT -- CUDA-core kernels that reproduce the reference bit for
  *                     bit (k-sequential f32 accumulation, RN16(q*s) weights).
- *   MOE_MODE_FAST  -- tcgen05/TMEM tensor-core grouped GEMM (f32 accumulate,
- *                     per-channel scale applied in the epilogue); gating,
- *                     routing and combine stay bit-exact.
+ *   MOE_MODE_FAST  -- tensor-core grouped GEMM (f32 accumulate, per-channel
+ *                     scale applied in the epilogue): tcgen05/TMEM tiles for
+ *                     prefill-sized batches, the K5 dequant-GEMV (mma.sync
+ *                     over the same weight tiles) when a layer routes at most
+ *                     256 rows; gating, routing and combine stay bit-exact.
  */
 #ifndef MOE_CUDA_H
 #define MOE_CUDA_H
@@ -39,6 +41,7 @@ extern "C" {
 
 #define MOE_MODE_EXACT 0
 #define MOE_MODE_FAST 1
+#define MOE_MODE_GEMV 2 /* moe_grouped_gemm only: force the decode (K5) kernel */
 
 /* weight formats: fp16 experts, or reference-quantized codes */
 #define MOE_W16 16
@@ -175,8 +178,16 @@ int moe_layer_destroy(moe_layer* L);
 int moe_layer_reserve(moe_layer* L, int64_t T, int k);
 int moe_layer_forward(moe_layer* L, const uint16_t* x, const uint8_t* finished,
                       int64_t T, int k, int mode, uint16_t* out, moe_stream_t stream);
+/* Same as moe_layer_forward, through a CUDA graph: the launch sequence for
+ * this exact argument set (pointers, T, k, mode) is captured once and
+ * replayed on later calls (no per-kernel launch cost).  Any stream, including
+ * the legacy default stream. */
+int moe_layer_forward_graph(moe_layer* L, const uint16_t* x, const uint8_t* finished,
+                            int64_t T, int k, int mode, uint16_t* out, moe_stream_t stream);
 /* Host-buffer forward (the drop-in / e2e path): copies x and finished in,
- * runs, copies out back, synchronises, and raises validation errors. */
+ * runs, copies out back, synchronises, and raises validation errors.  With
+ * pinned host buffers the whole sequence (H2D, kernels, D2H, status
+ * readback) is one cached CUDA graph. */
 int moe_layer_forward_host(moe_layer* L, const uint16_t* x_host,
                            const uint8_t* finished_host, int64_t T, int k, int mode,
                            uint16_t* out_host, moe_stream_t stream);

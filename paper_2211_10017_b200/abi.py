@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libmoe_cuda.so")
 
 MOE_OK, MOE_EINVAL, MOE_ECUDA, MOE_ENCCL, MOE_ERANGE = 0, 1, 2, 3, 4
-MODE_EXACT, MODE_FAST = 0, 1
+MODE_EXACT, MODE_FAST, MODE_GEMV = 0, 1, 2
 
 _vp, _i64, _int, _u16, _sz = C.c_void_p, C.c_int64, C.c_int, C.c_uint16, C.c_size_t
 
@@ -52,6 +52,7 @@ _SIGS = {
     "moe_layer_reserve": (_int, [_vp, _i64, _int]),
     "moe_layer_forward": (_int, [_vp, _vp, _vp, _i64, _int, _int, _vp, _vp]),
     "moe_layer_forward_host": (_int, [_vp, _vp, _vp, _i64, _int, _int, _vp, _vp]),
+    "moe_layer_forward_graph": (_int, [_vp, _vp, _vp, _i64, _int, _int, _vp, _vp]),
     "moe_layer_status": (_int, [_vp, _vp]),
     "moe_layer_routing": (_int, [_vp] + [_vp] * 6),
     "moe_layer_traffic": (_int, [_vp, _vp, _vp]),

@@ -8,6 +8,7 @@
 // GEMM problems are read from device memory (the plan writes them), so the
 // host never needs the routing result.
 #include <atomic>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -292,6 +293,19 @@ int moe_grouped_gemm(const uint16_t* x, int64_t rows, int64_t m, const uint32_t*
   GemmArgs a{x, rows, m, problems, np, tiled, scales, bits, E, n, bias, relu, out,
              debias_for(bits), np > 0 ? rows / np : rows};
   if (mode == MOE_MODE_FAST) return launch_gemm_tc(a, S(stream));
+  if (mode == MOE_MODE_GEMV) {
+    // decode path with its own split-K workspace (the layer keeps a persistent one)
+    const int ns = gemv_splits(m, n, (double)std::min<int64_t>(np, rows));
+    DevBuf part, ticket;
+    const int64_t nt = E * ((n + 127) / 128);
+    MOE_CUDA_TRY(cudaMallocAsync(&part.p, std::max<int64_t>(1, (int64_t)ns * rows * n * 4), S(stream)));
+    MOE_CUDA_TRY(cudaMallocAsync(&ticket.p, nt * 4, S(stream)));
+    MOE_CUDA_TRY(cudaMemsetAsync(ticket.p, 0, nt * 4, S(stream)));
+    GemvWork w{static_cast<float*>(part.p), static_cast<uint32_t*>(ticket.p), ns};
+    const int rc = launch_gemv(a, w, S(stream));
+    MOE_CUDA_TRY(cudaStreamSynchronize(S(stream)));
+    return rc;
+  }
   return launch_gemm_exact(a, S(stream));
 }
 
@@ -310,6 +324,8 @@ struct moe_layer {
   uint16_t *ln_g = nullptr, *ln_b = nullptr, *gw = nullptr, *gb = nullptr;
   uint16_t *b1 = nullptr, *b2 = nullptr, *s1 = nullptr, *s2 = nullptr;
   void *w1t = nullptr, *w2t = nullptr;
+  float* gw32 = nullptr;  // gate weights widened to f32, (d, gwp) (fused gate kernel)
+  int64_t gwp = 0;
   // workspace, sized for (cap_S slots, cap_T rows)
   int64_t cap_T = 0, cap_S = 0;
   uint16_t *xn = nullptr, *xp = nullptr, *h = nullptr, *y = nullptr;
@@ -318,6 +334,9 @@ struct moe_layer {
            *problems = nullptr, *active = nullptr, *bad_row = nullptr;
   uint16_t* scale = nullptr;
   uint32_t *blockcnt = nullptr, *blockbase = nullptr, *bad_expert = nullptr;
+  // decode GEMV split-K workspace (routed rows <= kGemvMaxRows)
+  float* gv_part = nullptr;
+  uint32_t* gv_ticket = nullptr;
   // host-path staging
   uint16_t *dx = nullptr, *dout = nullptr;
   uint8_t* dfin = nullptr;
@@ -329,8 +348,34 @@ struct moe_layer {
   bool prof = false;
   int prof_n = 0;
   std::vector<cudaEvent_t> ev;
+  // CUDA-graph cache (moe_layer_forward_graph / pinned-buffer host path):
+  // the launch sequence of one argument set, captured once, replayed after.
+  struct GraphKey {
+    const void *x = nullptr, *fin = nullptr, *out = nullptr;
+    int64_t T = 0;
+    int k = 0, mode = -1, host = 0, prof = 0;
+    bool operator==(const GraphKey& o) const {
+      return x == o.x && fin == o.fin && out == o.out && T == o.T && k == o.k && mode == o.mode &&
+             host == o.host && prof == o.prof;
+    }
+  };
+  struct Graph {
+    GraphKey key;
+    cudaGraphExec_t exec = nullptr;
+  };
+  std::vector<Graph> graphs;  // small LRU-less cache
+  cudaStream_t cap_stream = nullptr;
+  uint32_t* hstatus = nullptr;  // pinned: bad_row, bad_expert of the last host-path forward
 
+  void drop_graphs() {
+    for (auto& g : graphs)
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+    graphs.clear();
+  }
   ~moe_layer() {
+    drop_graphs();
+    if (cap_stream) cudaStreamDestroy(cap_stream);
+    if (hstatus) cudaFreeHost(hstatus);
     for (void* p : allocs) cudaFree(p);
     for (cudaEvent_t e : ev) cudaEventDestroy(e);
   }
@@ -386,6 +431,10 @@ static int layer_create_impl(const moe_layer_desc* D, moe_layer** out, bool devi
       (st = up(&L->gw, D->gate_w, d * E)) || (st = up(&L->gb, D->gate_b, E)) ||
       (st = up(&L->b1, D->b1, E * f)) || (st = up(&L->b2, D->b2, E * d)))
     return fail(st);
+  L->gwp = (E + 3) / 4 * 4;
+  if ((st = L->alloc(&L->gw32, d * L->gwp * 4)) ||
+      (st = launch_widen_gate(L->gw, d, E, L->gwp, L->gw32, nullptr)))
+    return fail(st);
   // experts: upload the reference-layout payload once, tile, drop the source
   auto tile = [&](void** dst, const void* src, int64_t m, int64_t n) -> int {
     const int64_t src_bytes = D->bits == 16 ? E * m * n * 2 : D->bits == 8 ? E * m * n : E * m * n / 2;
@@ -418,12 +467,13 @@ static int layer_reserve(moe_layer* L, int64_t T, int k) {
   const int64_t S_ = T * k;
   if (T <= L->cap_T && S_ <= L->cap_S) return MOE_OK;
   const int64_t cT = std::max(T, L->cap_T), cS = std::max(S_, L->cap_S);
+  L->drop_graphs();  // captured graphs point into the old workspace
   for (void* p : {(void*)L->xn, (void*)L->xp, (void*)L->h, (void*)L->y, (void*)L->logits,
                   (void*)L->expert, (void*)L->perm, (void*)L->inv, (void*)L->scale,
                   (void*)L->blockcnt, (void*)L->dx, (void*)L->dout, (void*)L->dfin})
     if (p) L->release(p);
   const int64_t d = L->d, f = L->f, E = L->E;
-  const int64_t nblk = plan_blocks(cS);
+  const int64_t nblk = std::max(plan_blocks(cS), (cT + 7) / 8);  // plan or fused-gate blocks
   TRY(L->alloc(&L->xn, cT * d * 2));
   TRY(L->alloc(&L->xp, cS * d * 2));
   TRY(L->alloc(&L->h, cS * f * 2));
@@ -438,6 +488,14 @@ static int layer_reserve(moe_layer* L, int64_t T, int k) {
   TRY(L->alloc(&L->dx, cT * d * 2));
   TRY(L->alloc(&L->dout, cT * d * 2));
   TRY(L->alloc(&L->dfin, cT));
+  if (!L->gv_part) {
+    const int64_t rmax = kGemvMaxRows;
+    const int64_t p1 = (int64_t)gemv_splits(d, f, 1.0) * f, p2 = (int64_t)gemv_splits(f, d, 1.0) * d;
+    TRY(L->alloc(&L->gv_part, rmax * std::max(p1, p2) * 4));
+    const int64_t nt = E * ((std::max(d, f) + 127) / 128);
+    TRY(L->alloc(&L->gv_ticket, nt * 4));
+    MOE_CUDA_TRY(cudaMemset(L->gv_ticket, 0, nt * 4));
+  }
   if (!L->offsets) {
     uint32_t* small = nullptr;
     TRY(L->alloc(&small, ((E + 1) + 3 * E + 4) * 4));
@@ -464,28 +522,55 @@ static int layer_forward(moe_layer* L, const uint16_t* x, const uint8_t* fin, in
   const bool prof = L->prof && L->prof_n < moe_layer::kProfCap;
   cudaEvent_t* evs = prof ? &L->ev[(size_t)L->prof_n * (moe_layer::kStages + 1)] : nullptr;
   int stage = 0;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (evs) MOE_CUDA_TRY(cudaStreamIsCapturing(st, &cap));
   auto mark = [&]() -> int {
-    if (evs) MOE_CUDA_TRY(cudaEventRecord(evs[stage], st));
+    // inside a graph capture only an *external* record becomes a real event
+    // record node (readable after each replay)
+    if (evs)
+      MOE_CUDA_TRY(cudaEventRecordWithFlags(
+          evs[stage], st, cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0));
     ++stage;
     return MOE_OK;
   };
   MOE_CUDA_TRY(cudaMemsetAsync(L->bad_row, 0xFF, 8, st));  // bad_row + bad_expert
   TRY(mark());
+  PlanWork w{L->blockcnt, L->blockbase, L->bad_expert};
+  if (gate_fused_supported(d, E, k) && (reinterpret_cast<uintptr_t>(x) & 15) == 0) {
+    // one kernel: LN + logits + top-k + key histogram; then scan/place/gather
+    GateFusedArgs ga{x, T, d, L->ln_g, L->ln_b, L->gw32, L->gwp, L->gb, E, k, fin, L->xn,
+                     L->expert, L->scale, L->blockcnt, L->bad_row, gate_fused_rows(T)};
+    TRY(launch_gate_fused(ga, st));
+    TRY(mark());
+    TRY(mark());
+    TRY(mark());
+    TRY(launch_plan_from_counts(L->expert, fin, T, k, E, (int64_t)ga.rows * k, w, L->perm,
+                                L->inv, L->offsets, L->problems, L->active, L->xn, d, L->xp,
+                                st));
+  } else {
   TRY(launch_layer_norm(x, T, d, L->ln_g, L->ln_b, L->xn, st));
   TRY(mark());
   TRY(launch_gate_logits(L->xn, T, d, L->gw, L->gb, E, L->logits, st));
   TRY(mark());
   TRY(launch_gate_topk(L->logits, T, E, k, L->expert, L->scale, L->bad_row, st));
   TRY(mark());
-  PlanWork w{L->blockcnt, L->blockbase, L->bad_expert};
   TRY(launch_routing_plan(L->expert, fin, T, k, E, L->perm, L->inv, L->offsets, L->problems,
                           L->active, w, L->xn, d, L->xp, st));
+  }
   TRY(mark());
   const uint16_t db = debias_for(L->bits);
   const int64_t hint = S_ / std::max<int64_t>(1, std::min<int64_t>(E, S_));
   GemmArgs g1{L->xp, S_, d, L->problems, E, L->w1t, L->s1, L->bits, E, f, L->b1, 1, L->h, db, hint};
   GemmArgs g2{L->h, S_, f, L->problems, E, L->w2t, L->s2, L->bits, E, d, L->b2, 0, L->y, db, hint};
-  if (mode == MOE_MODE_FAST) {
+  if (mode == MOE_MODE_FAST && S_ <= kGemvMaxRows) {
+    // decode regime: stream the active experts' weights (K5)
+    const double act = (double)E * (1.0 - std::pow(1.0 - 1.0 / (double)E, (double)S_));
+    GemvWork w1{L->gv_part, L->gv_ticket, gemv_splits(d, f, act)};
+    GemvWork w2{L->gv_part, L->gv_ticket, gemv_splits(f, d, act)};
+    TRY(launch_gemv(g1, w1, st));
+    TRY(mark());
+    TRY(launch_gemv(g2, w2, st));
+  } else if (mode == MOE_MODE_FAST) {
     TRY(launch_gemm_tc(g1, st));
     TRY(mark());
     TRY(launch_gemm_tc(g2, st));
@@ -510,7 +595,61 @@ static int layer_status(moe_layer* L, cudaStream_t st) {
   return MOE_OK;
 }
 
+// Capture `body` on the layer's private capture stream (thread-local mode:
+// nothing executes) and instantiate it; returns the cached exec for `key`.
+template <class F>
+static int layer_graph(moe_layer* L, const moe_layer::GraphKey& key, F&& body,
+                       cudaGraphExec_t* exec) {
+  for (auto& g : L->graphs)
+    if (g.key == key) {
+      *exec = g.exec;
+      return MOE_OK;
+    }
+  if (!L->cap_stream) MOE_CUDA_TRY(cudaStreamCreateWithFlags(&L->cap_stream, cudaStreamNonBlocking));
+  MOE_CUDA_TRY(cudaStreamBeginCapture(L->cap_stream, cudaStreamCaptureModeThreadLocal));
+  const int rc = body(L->cap_stream);
+  cudaGraph_t g = nullptr;
+  const cudaError_t e = cudaStreamEndCapture(L->cap_stream, &g);
+  if (rc != MOE_OK) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  if (e != cudaSuccess) return set_cuda_error(e, "graph capture");
+  cudaGraphExec_t x = nullptr;
+  const cudaError_t ie = cudaGraphInstantiate(&x, g, 0);
+  cudaGraphDestroy(g);
+  if (ie != cudaSuccess) return set_cuda_error(ie, "graph instantiate");
+  if (L->graphs.size() >= 16) L->drop_graphs();
+  L->graphs.push_back({key, x});
+  *exec = x;
+  return MOE_OK;
+}
+
+static bool is_pinned(const void* p) {
+  if (p == nullptr) return true;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
 extern "C" {
+
+int moe_layer_forward_graph(moe_layer* L, const uint16_t* x, const uint8_t* finished, int64_t T,
+                            int k, int mode, uint16_t* out, moe_stream_t stream) {
+  if (!L) return set_error(MOE_EINVAL, "layer: null");
+  if (T <= 0) return set_error(MOE_EINVAL, "moe_ffn: no rows");
+  if (k < 1 || k > L->E) return set_error(MOE_EINVAL, "moe_ffn: k must be in [1, n_experts]");
+  TRY(layer_reserve(L, T, k));
+  moe_layer::GraphKey key{x, finished, out, T, k, mode, 0, L->prof ? 1 : 0};
+  cudaGraphExec_t exec = nullptr;
+  TRY(layer_graph(L, key, [&](cudaStream_t cs) { return layer_forward(L, x, finished, T, k, mode, out, cs); },
+                  &exec));
+  MOE_CUDA_TRY(cudaGraphLaunch(exec, S(stream)));
+  return MOE_OK;
+}
 
 int moe_layer_create(const moe_layer_desc* desc, moe_layer** out) {
   return layer_create_impl(desc, out, false);
@@ -535,13 +674,35 @@ int moe_layer_forward_host(moe_layer* L, const uint16_t* x_host, const uint8_t* 
                            int64_t T, int k, int mode, uint16_t* out_host, moe_stream_t stream) {
   if (!L) return set_error(MOE_EINVAL, "layer: null");
   if (T <= 0) return set_error(MOE_EINVAL, "moe_ffn: no rows");
+  if (k < 1 || k > L->E) return set_error(MOE_EINVAL, "moe_ffn: k must be in [1, n_experts]");
   TRY(layer_reserve(L, T, k));
   cudaStream_t st = S(stream);
-  MOE_CUDA_TRY(cudaMemcpyAsync(L->dx, x_host, T * L->d * 2, cudaMemcpyHostToDevice, st));
-  if (fin_host) MOE_CUDA_TRY(cudaMemcpyAsync(L->dfin, fin_host, T, cudaMemcpyHostToDevice, st));
-  TRY(layer_forward(L, L->dx, fin_host ? L->dfin : nullptr, T, k, mode, L->dout, st));
-  MOE_CUDA_TRY(cudaMemcpyAsync(out_host, L->dout, T * L->d * 2, cudaMemcpyDeviceToHost, st));
-  return layer_status(L, st);
+  auto body = [&](cudaStream_t s2, uint32_t* status_dst) -> int {
+    MOE_CUDA_TRY(cudaMemcpyAsync(L->dx, x_host, T * L->d * 2, cudaMemcpyHostToDevice, s2));
+    if (fin_host) MOE_CUDA_TRY(cudaMemcpyAsync(L->dfin, fin_host, T, cudaMemcpyHostToDevice, s2));
+    TRY(layer_forward(L, L->dx, fin_host ? L->dfin : nullptr, T, k, mode, L->dout, s2));
+    MOE_CUDA_TRY(cudaMemcpyAsync(out_host, L->dout, T * L->d * 2, cudaMemcpyDeviceToHost, s2));
+    MOE_CUDA_TRY(cudaMemcpyAsync(status_dst, L->bad_row, 8, cudaMemcpyDeviceToHost, s2));
+    return MOE_OK;
+  };
+  uint32_t hs[2];
+  if (is_pinned(x_host) && is_pinned(out_host) && is_pinned(fin_host)) {
+    // pinned buffers: one captured graph (copies + kernels + status readback)
+    if (!L->hstatus) MOE_CUDA_TRY(cudaMallocHost(&L->hstatus, 8));
+    moe_layer::GraphKey key{x_host, fin_host, out_host, T, k, mode, 1, L->prof ? 1 : 0};
+    cudaGraphExec_t exec = nullptr;
+    TRY(layer_graph(L, key, [&](cudaStream_t cs) { return body(cs, L->hstatus); }, &exec));
+    MOE_CUDA_TRY(cudaGraphLaunch(exec, st));
+    MOE_CUDA_TRY(cudaStreamSynchronize(st));
+    hs[0] = L->hstatus[0];
+    hs[1] = L->hstatus[1];
+  } else {
+    TRY(body(st, hs));
+    MOE_CUDA_TRY(cudaStreamSynchronize(st));
+  }
+  if (hs[0] != 0xFFFFFFFFu) return set_error(MOE_EINVAL, "gate_top1: non-finite logit at row %u", hs[0]);
+  if (hs[1] != 0xFFFFFFFFu) return set_error(MOE_EINVAL, "build_routing_plan: expert out of range");
+  return MOE_OK;
 }
 int moe_layer_status(moe_layer* L, moe_stream_t stream) {
   if (!L) return set_error(MOE_EINVAL, "layer: null");
@@ -568,6 +729,7 @@ int moe_layer_profile(moe_layer* L, int enable) {
   }
   L->prof = enable != 0;
   L->prof_n = 0;
+  L->drop_graphs();  // event slots are baked into captured graphs
   return MOE_OK;
 }
 

@@ -70,17 +70,6 @@ __global__ void __launch_bounds__(128) layer_norm_kernel(const uint16_t* __restr
 // row pitches is bank-conflict free per quarter warp.
 constexpr int LN_R = 64, LN_KC = 64, LN_NS = 4, LN_PITCH = LN_KC + 8;
 
-__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
-               "r"(valid ? 16 : 0)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
 __global__ void __launch_bounds__(LN_R) layer_norm_rows_kernel(const uint16_t* __restrict__ x,
                                                                int64_t T, int64_t d,
                                                                const uint16_t* __restrict__ g,

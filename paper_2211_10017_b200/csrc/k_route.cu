@@ -39,23 +39,32 @@ __global__ void __launch_bounds__(kPlanBlock) plan_count_kernel(
   if (slot < S) atomicAdd(&hist[slot_key(expert, finished, slot, k, E, bad)], 1u);
   __syncthreads();
   for (int64_t i = threadIdx.x; i <= E; i += kPlanBlock)
-    blockcnt[(int64_t)blockIdx.x * (E + 1) + i] = hist[i];
+    blockcnt[i * gridDim.x + blockIdx.x] = hist[i];  // key-major [E+1][nblk]
 }
 
-// One CTA of 1024 threads; thread j owns key j (keys E+1 <= 1024*ITER).
+// One CTA of 1024 threads over the key-major histogram cnt[key][block]:
+//   pass 1: warp w sums keys w, w+32, ... over all blocks (coalesced rows);
+//   scan  : exclusive scan of the key totals -> expert_offsets, active_rows;
+//   pass 2: per key, a warp-wide running scan over blocks writes
+//           base[key][block] = offsets[key] + (count of key in earlier blocks).
 __global__ void __launch_bounds__(1024) plan_scan_kernel(
     const uint32_t* __restrict__ blockcnt, int64_t nblk, int64_t E,
     uint32_t* __restrict__ blockbase, uint32_t* __restrict__ offsets,
     uint32_t* __restrict__ problems, uint32_t* __restrict__ active) {
   __shared__ uint32_t tot[1024 + 1];
   __shared__ uint32_t warp_sum[32];
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t keys = E + 1;
-  uint32_t t = 0;
-  if (tid < keys)
-    for (int64_t b = 0; b < nblk; ++b) t += blockcnt[b * keys + tid];
-  // exclusive scan of t over tid (block-wide)
-  const int lane = tid & 31, warp = tid >> 5;
+  for (int64_t key = warp; key < keys; key += 32) {
+    const uint32_t* row = blockcnt + key * nblk;
+    uint32_t s = 0;
+    for (int64_t b = lane; b < nblk; b += 32) s += row[b];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) tot[key] = s;
+  }
+  __syncthreads();
+  const uint32_t t = tid < keys ? tot[tid] : 0u;
   uint32_t incl = t;
   for (int o = 1; o < 32; o <<= 1) {
     const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
@@ -73,16 +82,28 @@ __global__ void __launch_bounds__(1024) plan_scan_kernel(
   }
   __syncthreads();
   const uint32_t excl = incl - t + (warp > 0 ? warp_sum[warp - 1] : 0);
+  __syncthreads();  // every thread has read tot[] / warp_sum[]
   if (tid < keys) {
     tot[tid] = excl;
-    uint32_t run = excl;
-    for (int64_t b = 0; b < nblk; ++b) {
-      blockbase[b * keys + tid] = run;
-      run += blockcnt[b * keys + tid];
-    }
     offsets[tid] = excl;  // offsets[E] = start of the finished tail = active_rows
   }
   __syncthreads();
+  for (int64_t key = warp; key < keys; key += 32) {
+    const uint32_t* row = blockcnt + key * nblk;
+    uint32_t* brow = blockbase + key * nblk;
+    uint32_t carry = tot[key];
+    for (int64_t b0 = 0; b0 < nblk; b0 += 32) {
+      const int64_t b = b0 + lane;
+      const uint32_t c = b < nblk ? row[b] : 0u;
+      uint32_t in = c;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, in, o);
+        if (lane >= o) in += v;
+      }
+      if (b < nblk) brow[b] = carry + in - c;
+      carry += __shfl_sync(0xffffffffu, in, 31);
+    }
+  }
   if (tid < E && problems != nullptr) {
     problems[3 * tid] = (uint32_t)tid;
     problems[3 * tid + 1] = tot[tid];
@@ -91,29 +112,30 @@ __global__ void __launch_bounds__(1024) plan_scan_kernel(
   if (tid == 0 && active != nullptr) *active = tot[E];
 }
 
-__global__ void __launch_bounds__(kPlanBlock) plan_place_kernel(
+__global__ void __launch_bounds__(kPlanBlock) plan_place_kernel(int spb,
     const uint32_t* __restrict__ expert, const uint8_t* __restrict__ finished, int64_t S, int k,
     int64_t E, const uint32_t* __restrict__ blockbase, uint32_t* __restrict__ perm,
     uint32_t* __restrict__ inv, const uint16_t* __restrict__ src, int64_t cols,
     uint16_t* __restrict__ dst, uint32_t* bad) {
-  extern __shared__ uint32_t wcnt[];  // [8 warps][E+1], then pos/slot lists
+  // spb = slots per plan block (blockDim.x >= spb, a multiple of 32)
+  extern __shared__ uint32_t wcnt[];  // [warps][E+1], then pos/slot lists
   const int64_t keys = E + 1;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int64_t i = threadIdx.x; i < 8 * keys; i += kPlanBlock) wcnt[i] = 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
+  for (int64_t i = threadIdx.x; i < nwarp * keys; i += blockDim.x) wcnt[i] = 0;
   __syncthreads();
-  const int64_t slot = (int64_t)blockIdx.x * kPlanBlock + threadIdx.x;
-  const bool live = slot < S;
+  const int64_t slot = (int64_t)blockIdx.x * spb + threadIdx.x;
+  const bool live = (int)threadIdx.x < spb && slot < S;
   const uint32_t key = live ? slot_key(expert, finished, slot, k, E, bad) : 0xFFFFFFFFu;
   const uint32_t peers = __match_any_sync(0xffffffffu, key);
   const uint32_t lt = (1u << lane) - 1u;
   const uint32_t rank_w = __popc(peers & lt);
   if (live && (peers >> lane) == 1u) wcnt[warp * keys + key] = __popc(peers);  // highest peer
   __syncthreads();
-  uint32_t* pos_l = wcnt + 8 * keys;
+  uint32_t* pos_l = wcnt + nwarp * keys;
   if (live) {
     uint32_t before = 0;
     for (int w = 0; w < warp; ++w) before += wcnt[w * keys + key];
-    const uint32_t pos = blockbase[(int64_t)blockIdx.x * keys + key] + before + rank_w;
+    const uint32_t pos = blockbase[(int64_t)key * gridDim.x + blockIdx.x] + before + rank_w;
     perm[pos] = (uint32_t)slot;
     inv[slot] = pos;
     pos_l[threadIdx.x] = pos;
@@ -121,10 +143,10 @@ __global__ void __launch_bounds__(kPlanBlock) plan_place_kernel(
   if (dst == nullptr) return;
   __syncthreads();
   // gather: dst[pos] = src[slot / k], one warp per row, 16-byte vectors
-  const int64_t nslots = ::min((int64_t)kPlanBlock, S - (int64_t)blockIdx.x * kPlanBlock);
+  const int64_t nslots = ::min((int64_t)spb, S - (int64_t)blockIdx.x * spb);
   const bool vec = (cols % 8) == 0;
-  for (int64_t i = warp; i < nslots; i += kPlanBlock / 32) {
-    const int64_t s = (int64_t)blockIdx.x * kPlanBlock + i;
+  for (int64_t i = warp; i < nslots; i += nwarp) {
+    const int64_t s = (int64_t)blockIdx.x * spb + i;
     const uint16_t* a = src + (s / k) * cols;
     uint16_t* b = dst + (int64_t)pos_l[i] * cols;
     if (vec) {
@@ -156,9 +178,34 @@ int launch_routing_plan(const uint32_t* expert, const uint8_t* finished, int64_t
   // The row gather runs as its own wide launch (one warp per row): folding
   // it into plan_place left only S/256 CTAs to move S*cols*2 bytes.
   plan_place_kernel<<<(unsigned)nblk, kPlanBlock, smem, st>>>(
-      expert, finished, S, k, E, w.blockbase, perm, inv, nullptr, 0, nullptr, w.bad);
+      kPlanBlock, expert, finished, S, k, E, w.blockbase, perm, inv, nullptr, 0, nullptr, w.bad);
   note_launch();
   const int s1 = check_launch("routing_plan");
+  if (s1 != MOE_OK || gather_dst == nullptr) return s1;
+  return launch_permute(gather_src, cols, perm, S, k, gather_dst, st);
+}
+
+// Plan from per-block counts already produced by the fused gate kernel
+// (k_gate_fused.cu): blocks of spb = rows*k slots.  scan -> place -> gather.
+int launch_plan_from_counts(const uint32_t* expert, const uint8_t* finished, int64_t T, int k,
+                            int64_t E, int64_t spb, const PlanWork& w, uint32_t* perm,
+                            uint32_t* inv, uint32_t* offsets, uint32_t* problems,
+                            uint32_t* active, const uint16_t* gather_src, int64_t cols,
+                            uint16_t* gather_dst, cudaStream_t st) {
+  const int64_t S = T * k;
+  if (S == 0) return MOE_OK;
+  if (E + 1 > 1024) return set_error(MOE_EINVAL, "routing plan: at most 1023 experts");
+  const int64_t nblk = (S + spb - 1) / spb;
+  plan_scan_kernel<<<1, 1024, 0, st>>>(w.blockcnt, nblk, E, w.blockbase, offsets, problems,
+                                       active);
+  note_launch();
+  const int threads = (int)((spb + 31) / 32 * 32);
+  const size_t smem = ((threads / 32) * (E + 1) + threads) * 4;
+  plan_place_kernel<<<(unsigned)nblk, threads, smem, st>>>((int)spb, expert, finished, S, k, E,
+                                                           w.blockbase, perm, inv, nullptr, 0,
+                                                           nullptr, w.bad);
+  note_launch();
+  const int s1 = check_launch("plan_from_counts");
   if (s1 != MOE_OK || gather_dst == nullptr) return s1;
   return launch_permute(gather_src, cols, perm, S, k, gather_dst, st);
 }

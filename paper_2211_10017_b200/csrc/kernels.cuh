@@ -40,6 +40,30 @@ int launch_gate_logits(const uint16_t* xn, int64_t T, int64_t d, const uint16_t*
 int launch_gate_topk(const float* logits, int64_t T, int64_t E, int k, uint32_t* expert,
                      uint16_t* scale, uint32_t* bad_row, cudaStream_t st);
 
+// k_gate_fused.cu: LN + logits + top-k + per-block key histogram
+struct GateFusedArgs {
+  const uint16_t* x;
+  int64_t T, d;
+  const uint16_t *g, *b;
+  const float* gw32;  // (d, gwp) f32, zero-padded columns
+  int64_t gwp;
+  const uint16_t* gb;
+  int64_t E;
+  int k;
+  const uint8_t* finished;
+  uint16_t* xn;
+  uint32_t* expert;
+  uint16_t* scale;
+  uint32_t* blockcnt;  // ceil(T/rows) * (E+1)
+  uint32_t* bad_row;
+  int rows;            // gate_fused_rows(T)
+};
+int gate_fused_rows(int64_t T);
+bool gate_fused_supported(int64_t d, int64_t E, int k);
+int launch_gate_fused(const GateFusedArgs& a, cudaStream_t st);
+int launch_widen_gate(const uint16_t* gw, int64_t d, int64_t E, int64_t gwp, float* out,
+                      cudaStream_t st);
+
 // k_route.cu
 struct PlanWork {
   uint32_t* blockcnt;   // nblk * (E+1)
@@ -52,6 +76,11 @@ int launch_routing_plan(const uint32_t* expert, const uint8_t* finished, int64_t
                         uint32_t* problems, uint32_t* active, const PlanWork& w,
                         const uint16_t* gather_src, int64_t cols, uint16_t* gather_dst,
                         cudaStream_t st);
+int launch_plan_from_counts(const uint32_t* expert, const uint8_t* finished, int64_t T, int k,
+                            int64_t E, int64_t spb, const PlanWork& w, uint32_t* perm,
+                            uint32_t* inv, uint32_t* offsets, uint32_t* problems,
+                            uint32_t* active, const uint16_t* gather_src, int64_t cols,
+                            uint16_t* gather_dst, cudaStream_t st);
 int launch_permute(const uint16_t* x, int64_t cols, const uint32_t* perm, int64_t S, int k,
                    uint16_t* xp, cudaStream_t st);
 int launch_unpermute_scale(const uint16_t* y, int64_t T, int64_t cols, const uint32_t* perm,
@@ -80,6 +109,16 @@ struct GemmArgs {
   int64_t rows_hint;  // expected rows per problem (tile-size choice)
 };
 int launch_gemm_exact(const GemmArgs& a, cudaStream_t st);
+
+// k_gemv.cu: decode-sized FAST path (mma.sync over the same weight tiles)
+constexpr int64_t kGemvMaxRows = 256;  // routed rows (T*k) up to which the layer uses it
+struct GemvWork {
+  float* part;       // split-K partials, nsplit * rows * n
+  uint32_t* ticket;  // E * ceil(n/128), zero-initialised, self-resetting
+  int nsplit;
+};
+int gemv_splits(int64_t m, int64_t n, double active_experts);
+int launch_gemv(const GemmArgs& a, const GemvWork& w, cudaStream_t st);
 int launch_gemm_tc(const GemmArgs& a, cudaStream_t st);
 
 }  // namespace moecu

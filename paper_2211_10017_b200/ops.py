@@ -13,7 +13,7 @@ import torch
 
 from . import abi
 
-MODE_EXACT, MODE_FAST = abi.MODE_EXACT, abi.MODE_FAST
+MODE_EXACT, MODE_FAST, MODE_GEMV = abi.MODE_EXACT, abi.MODE_FAST, abi.MODE_GEMV
 
 
 def _p(t):
@@ -206,13 +206,15 @@ class MoELayer:
     def reserve(self, T, k=1):
         abi.call("moe_layer_reserve", self._h, T, k)
 
-    def forward(self, x, finished=None, k=1, mode=MODE_FAST, out=None, stream=None):
-        """Device-resident forward (no host sync, graph-capturable)."""
+    def forward(self, x, finished=None, k=1, mode=MODE_FAST, out=None, stream=None,
+                graph=False):
+        """Device-resident forward (no host sync, graph-capturable).  graph=True
+        replays a cached CUDA graph of this argument set (moe_layer_forward_graph)."""
         T = x.shape[0]
         if out is None:
             out = torch.empty_like(x)
-        abi.call("moe_layer_forward", self._h, _p(x), _p(finished), T, k, mode, _p(out),
-                 _stream(stream))
+        abi.call("moe_layer_forward_graph" if graph else "moe_layer_forward", self._h, _p(x),
+                 _p(finished), T, k, mode, _p(out), _stream(stream))
         return out
 
     def forward_host(self, x_host, finished_host=None, k=1, mode=MODE_FAST, out_host=None,

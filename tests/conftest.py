@@ -71,3 +71,18 @@ def norm_err(got, want):
     w = np.asarray(want, np.float64)
     den = max(np.abs(w).max(), 1e-30)
     return float(np.abs(g - w).max() / den)
+
+
+def layer_err(got, want, x):
+    """Normalized error of a MoE layer output, net of the final fp16 rounding:
+    max(|got - want| - ulp16(want), 0) / max|want - x|.  Both sides round
+    x + contribution to fp16 once, so a 1-ulp disagreement is rounding noise
+    that the 1e-2 budget of the contribution must not be charged with (it
+    dominates when the contribution is small, e.g. T=2)."""
+    g = np.asarray(got, np.float64)
+    w = np.asarray(want, np.float64)
+    xf = np.asarray(x, np.float64)
+    ulp = np.spacing(np.abs(np.asarray(want, np.float16))).astype(np.float64)
+    excess = np.maximum(np.abs(g - w) - ulp, 0.0)
+    den = max(np.abs(w - xf).max(), 1e-30)
+    return float(excess.max() / den)

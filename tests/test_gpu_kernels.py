@@ -287,3 +287,28 @@ def test_gemm_fast_equals_exact_semantics_large(cuda, oracle):
     a = ops.grouped_gemm(xs, probs, tiled, scales, 4, E, n, to_dev(bias), True, ops.MODE_EXACT)
     b = ops.grouped_gemm(xs, probs, tiled, scales, 4, E, n, to_dev(bias), True, ops.MODE_FAST)
     assert norm_err(to_np(b), to_np(a)) <= TOL_FAST
+
+
+@pytest.mark.parametrize("bits", [4, 8, 16])
+@pytest.mark.parametrize("shape", [(1, 1, 1024, 4096), (8, 4, 1024, 512), (64, 32, 256, 1024),
+                                   (40, 3, 4096, 256), (3, 5, 72, 136), (200, 8, 512, 2048)])
+def test_gemm_gemv_decode_within_tolerance(cuda, oracle, bits, shape):
+    """K5 decode kernel (mma.sync over the tcgen05 weight tiles, split-K with a
+    fixed-order reduction) vs the oracle: any rows per expert, ragged m/n."""
+    rows, E, m, n = shape
+    if bits == 4 and n % 8:
+        pytest.skip("int4 needs n % 8 == 0")
+    rng = np.random.default_rng(rows * 7 + E + m + n + bits)
+    ex, fin, x, w, bias = _gemm_case(rng, rows, E, m, n, bits, fin_frac=0.1)
+    got, want = _run_gemm(oracle, ex, fin, x, w, bias, bits, bits != 8, _ops().MODE_GEMV)
+    active = int((fin == 0).sum())
+    if active:
+        assert norm_err(got[:active], want[:active]) <= TOL_FAST
+
+
+def test_gemm_gemv_deterministic(cuda, oracle):
+    rng = np.random.default_rng(5)
+    ex, fin, x, w, bias = _gemm_case(rng, 16, 2, 2048, 512, 4, fin_frac=0.0)
+    a, _ = _run_gemm(oracle, ex, fin, x, w, bias, 4, False, _ops().MODE_GEMV)
+    b, _ = _run_gemm(oracle, ex, fin, x, w, bias, 4, False, _ops().MODE_GEMV)
+    assert np.array_equal(bits16(a), bits16(b))

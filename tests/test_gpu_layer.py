@@ -8,7 +8,7 @@ of the MoE contribution out - x)."""
 import numpy as np
 import pytest
 
-from conftest import bits16, norm_err, to_dev, to_np
+from conftest import bits16, layer_err, norm_err, to_dev, to_np
 
 pytestmark = pytest.mark.gpu
 
@@ -124,3 +124,46 @@ def test_c2_c3_shapes_fast_vs_exact_and_per_token_rows(cuda, oracle, T, k):
     rows = np.random.default_rng(0).choice(T, size=min(T, 16), replace=False)
     want = oracle.moe_per_token(lw, x[rows], None, k=k, bits=4, q=q)
     assert np.array_equal(bits16(ex[rows]), bits16(want))
+
+
+@pytest.mark.parametrize("T", [1, 2, 8, 64, 256])
+def test_layer_decode_shapes(cuda, oracle, T):
+    """Decode-shaped layers (C3 family, reduced d/f): fused gate + K5 GEMV
+    (T*k <= 256) -- routing bit-exact, outputs within tolerance, and the same
+    layer object reused across T (workspace growth)."""
+    lw, x, fin = _case(256, 1024, 32, T, seed=300 + T, fin_frac=0.2 if T > 1 else 0.0)
+    L = _layer(lw, 4)
+    q = tuple(to_np(t) for t in L.quant)
+    for k in (1, 2):
+        want, diag = oracle.moe_forward(lw, x, fin, k=k, bits=4, q=q, diagnostics=True)
+        got = to_np(L.forward(to_dev(x), to_dev(fin), k=k, mode=1))
+        r = L.routing(T, k)
+        for key in ("expert", "perm", "inv", "offsets", "scale"):
+            assert np.array_equal(r[key].reshape(-1), diag[key].reshape(-1)), key
+        if (want != x).any():
+            err = layer_err(got, want, x)
+            assert err <= TOL_FAST, err
+        assert np.array_equal(bits16(got)[fin == 1], bits16(x)[fin == 1])
+
+
+@pytest.mark.parametrize("E,d,T,k", [(8, 512, 4096, 2), (64, 1024, 600, 1), (128, 256, 300, 2),
+                                     (3, 40, 50, 3), (130, 64, 20, 1)])
+def test_layer_fused_gate_routing_exact(cuda, oracle, E, d, T, k):
+    """Fused LN+logits+top-k+histogram kernel (and the unfused fallback for
+    E > 128): routing identical to the oracle at BASELINE-like shapes."""
+    from oracle.oracle import random_layer
+    lw = random_layer(d, 64, E, seed=E + d + T)
+    rng = np.random.default_rng(T)
+    x = rng.standard_normal((T, d)).astype(np.float16)
+    fin = (rng.random(T) < 0.1).astype(np.uint8)
+    L = _layer(lw, 16)
+    L.forward(to_dev(x), to_dev(fin), k=k, mode=1)
+    r = L.routing(T, k)
+    xn = oracle.layer_norm(x, lw.ln_g, lw.ln_b)
+    lg = oracle.gate_logits(xn, lw.gw, lw.gb)
+    ex, sc = oracle.gate_topk(lg, k)
+    perm, inv, offs, act = oracle.routing_plan(ex, fin, E)
+    assert np.array_equal(r["expert"], ex)
+    assert np.array_equal(r["scale"], sc)
+    assert np.array_equal(r["perm"], perm) and np.array_equal(r["inv"], inv)
+    assert np.array_equal(r["offsets"], offs) and r["active"] == act
