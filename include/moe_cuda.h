@@ -164,6 +164,10 @@ typedef struct {
   const uint16_t *w1, *w2;        /* bits 16: (E,d,f), (E,f,d) */
   const uint8_t *q1, *q2;         /* bits 8/4: quantize() payloads */
   const uint16_t *s1, *s2;        /* (E,f), (E,d) scales */
+  /* expert parallelism: when e_count > 0 the expert tensors above (w/q, s,
+   * b1, b2) hold only experts [e_begin, e_begin + e_count); the gate still
+   * covers all E.  0 = every expert (single-GPU layer). */
+  int64_t e_begin, e_count;
 } moe_layer_desc;
 
 int moe_layer_create(const moe_layer_desc* desc, moe_layer** out);
@@ -191,6 +195,21 @@ int moe_layer_forward_graph(moe_layer* L, const uint16_t* x, const uint8_t* fini
 int moe_layer_forward_host(moe_layer* L, const uint16_t* x_host,
                            const uint8_t* finished_host, int64_t T, int k, int mode,
                            uint16_t* out_host, moe_stream_t stream);
+/* Expert-parallel building blocks (orchestrated over NCCL by
+ * paper_2211_10017_b200/ep.py).  route: stages LN..gather of the layer into
+ * its workspace (expert-sorted rows at *xp, plan via moe_layer_routing).
+ * experts: FFN1 (ReLU) + FFN2 of the layer's LOCAL experts over `rows`
+ * expert-sorted rows (problems: np device triples, expert ids local).
+ * combine: residual + gate-scaled un-permute of y (sorted order) using the
+ * last route's plan. */
+int moe_layer_route(moe_layer* L, const uint16_t* x, const uint8_t* finished, int64_t T, int k,
+                    moe_stream_t stream);
+int moe_layer_buffers(moe_layer* L, const uint16_t** xp, uint16_t** y);
+int moe_layer_experts(moe_layer* L, const uint16_t* xin, int64_t rows, const uint32_t* problems,
+                      int64_t np, int mode, uint16_t* out, moe_stream_t stream);
+int moe_layer_combine(moe_layer* L, const uint16_t* x, const uint16_t* y,
+                      const uint8_t* finished, int64_t T, int k, uint16_t* out,
+                      moe_stream_t stream);
 /* Synchronises and reports device-side validation (non-finite logits). */
 int moe_layer_status(moe_layer* L, moe_stream_t stream);
 /* Routing diagnostics of the last forward (device pointers owned by L):
@@ -199,10 +218,12 @@ int moe_layer_routing(moe_layer* L, const uint32_t** expert, const uint16_t** sc
                       const uint32_t** perm, const uint32_t** inv,
                       const uint32_t** offsets, const uint32_t** active);
 /* Stage timing with CUDA events recorded on the forward's own stream
- * (bench.py's roofline).  enable != 0 starts (and resets) recording for up
- * to 512 forwards; read returns the summed milliseconds of the 7 stages
- * {layer_norm, gate_logits, gate_topk, routing_plan+gather, ffn1, ffn2,
- * combine} over the recorded forwards (synchronises on the last one). */
+ * (bench.py's roofline).  enable = 1 records only the grouped-GEMM
+ * boundaries (ffn1, ffn2), enable = 2 every stage, 0 stops; enabling resets
+ * the record (up to 512 forwards; a graph replays its captured slot).  read
+ * returns the summed milliseconds of the 7 stages {gate (fused LN+logits+
+ * top-k, or layer_norm), gate_logits, gate_topk, routing_plan+gather, ffn1,
+ * ffn2, combine} (unrecorded stages read 0) over the recorded forwards. */
 int moe_layer_profile(moe_layer* L, int enable);
 int moe_layer_profile_read(moe_layer* L, double* stage_ms, int* forwards);
 /* Analytic traffic of the last forward, reference accounting

@@ -59,6 +59,10 @@ _SIGS = {
     "moe_layer_profile": (_int, [_vp, _int]),
     "moe_layer_profile_read": (_int, [_vp, _vp, _vp]),
     "moe_ep_rank_counts": (_int, [_vp, _i64, _int, _vp, _vp]),
+    "moe_layer_route": (_int, [_vp, _vp, _vp, _i64, _int, _vp]),
+    "moe_layer_buffers": (_int, [_vp, _vp, _vp]),
+    "moe_layer_experts": (_int, [_vp, _vp, _i64, _vp, _i64, _int, _vp, _vp]),
+    "moe_layer_combine": (_int, [_vp, _vp, _vp, _vp, _i64, _int, _vp, _vp]),
 }
 
 
@@ -67,7 +71,7 @@ class LayerDesc(C.Structure):
 
     _fields_ = [("d", _i64), ("f", _i64), ("E", _i64), ("bits", _int)] + [
         (nm, _vp) for nm in ("ln_g", "ln_b", "gate_w", "gate_b", "b1", "b2", "w1", "w2", "q1",
-                             "q2", "s1", "s2")]
+                             "q2", "s1", "s2")] + [("e_begin", _i64), ("e_count", _i64)]
 
 
 _lib = None

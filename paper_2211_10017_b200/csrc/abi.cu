@@ -319,6 +319,7 @@ int moe_ep_rank_counts(const uint32_t* offsets, int64_t E, int G, int64_t* count
 // ======================================================================= layer
 struct moe_layer {
   int64_t d = 0, f = 0, E = 0;
+  int64_t El = 0, e0 = 0;  // experts whose FFN weights live here: [e0, e0 + El)
   int bits = 16;
   // weights (device)
   uint16_t *ln_g = nullptr, *ln_b = nullptr, *gw = nullptr, *gb = nullptr;
@@ -334,6 +335,9 @@ struct moe_layer {
            *problems = nullptr, *active = nullptr, *bad_row = nullptr;
   uint16_t* scale = nullptr;
   uint32_t *blockcnt = nullptr, *blockbase = nullptr, *bad_expert = nullptr;
+  // EP: hidden activations of rows received from peers
+  uint16_t* ep_h = nullptr;
+  int64_t ep_cap = 0;
   // decode GEMV split-K workspace (routed rows <= kGemvMaxRows)
   float* gv_part = nullptr;
   uint32_t* gv_ticket = nullptr;
@@ -346,6 +350,7 @@ struct moe_layer {
   // stage profiling (moe_layer_profile): kStages+1 events per forward
   static constexpr int kStages = 7, kProfCap = 512;
   bool prof = false;
+  int prof_level = 0;
   int prof_n = 0;
   std::vector<cudaEvent_t> ev;
   // CUDA-graph cache (moe_layer_forward_graph / pinned-buffer host path):
@@ -362,6 +367,7 @@ struct moe_layer {
   struct Graph {
     GraphKey key;
     cudaGraphExec_t exec = nullptr;
+    uint64_t nlaunch = 0;  // kernels in the graph (moe_cuda_launch_count on replay)
   };
   std::vector<Graph> graphs;  // small LRU-less cache
   cudaStream_t cap_stream = nullptr;
@@ -415,7 +421,13 @@ static int layer_create_impl(const moe_layer_desc* D, moe_layer** out, bool devi
   L->f = D->f;
   L->E = D->E;
   L->bits = D->bits;
-  const int64_t d = D->d, f = D->f, E = D->E;
+  if (D->e_count < 0 || D->e_begin < 0 || D->e_begin + D->e_count > D->E) {
+    delete L;
+    return set_error(MOE_EINVAL, "layer: local expert range outside [0, n_experts)");
+  }
+  L->El = D->e_count > 0 ? D->e_count : D->E;
+  L->e0 = D->e_count > 0 ? D->e_begin : 0;
+  const int64_t d = D->d, f = D->f, E = D->E, El = L->El;
   const cudaMemcpyKind kind = device_src ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
   auto up = [&](uint16_t** dst, const uint16_t* src, int64_t count) -> int {
     TRY(L->alloc(dst, count * 2));
@@ -429,7 +441,7 @@ static int layer_create_impl(const moe_layer_desc* D, moe_layer** out, bool devi
   };
   if ((st = up(&L->ln_g, D->ln_g, d)) || (st = up(&L->ln_b, D->ln_b, d)) ||
       (st = up(&L->gw, D->gate_w, d * E)) || (st = up(&L->gb, D->gate_b, E)) ||
-      (st = up(&L->b1, D->b1, E * f)) || (st = up(&L->b2, D->b2, E * d)))
+      (st = up(&L->b1, D->b1, El * f)) || (st = up(&L->b2, D->b2, El * d)))
     return fail(st);
   L->gwp = (E + 3) / 4 * 4;
   if ((st = L->alloc(&L->gw32, d * L->gwp * 4)) ||
@@ -437,14 +449,14 @@ static int layer_create_impl(const moe_layer_desc* D, moe_layer** out, bool devi
     return fail(st);
   // experts: upload the reference-layout payload once, tile, drop the source
   auto tile = [&](void** dst, const void* src, int64_t m, int64_t n) -> int {
-    const int64_t src_bytes = D->bits == 16 ? E * m * n * 2 : D->bits == 8 ? E * m * n : E * m * n / 2;
+    const int64_t src_bytes = D->bits == 16 ? El * m * n * 2 : D->bits == 8 ? El * m * n : El * m * n / 2;
     void* tmp = nullptr;
     if (!device_src) {
       MOE_CUDA_TRY(cudaMalloc(&tmp, src_bytes));
       MOE_CUDA_TRY(cudaMemcpy(tmp, src, src_bytes, cudaMemcpyHostToDevice));
     }
-    TRY(L->alloc(dst, tiled_bytes(E, m, n, D->bits)));
-    const int s2 = launch_tile_weights(device_src ? src : tmp, E, m, n, D->bits, *dst, nullptr);
+    TRY(L->alloc(dst, tiled_bytes(El, m, n, D->bits)));
+    const int s2 = launch_tile_weights(device_src ? src : tmp, El, m, n, D->bits, *dst, nullptr);
     MOE_CUDA_TRY(cudaDeviceSynchronize());
     if (tmp) cudaFree(tmp);
     return s2;
@@ -456,7 +468,7 @@ static int layer_create_impl(const moe_layer_desc* D, moe_layer** out, bool devi
     if (!D->q1 || !D->q2 || !D->s1 || !D->s2)
       return fail(set_error(MOE_EINVAL, "layer: quantized experts missing"));
     if ((st = tile(&L->w1t, D->q1, d, f)) || (st = tile(&L->w2t, D->q2, f, d)) ||
-        (st = up(&L->s1, D->s1, E * f)) || (st = up(&L->s2, D->s2, E * d)))
+        (st = up(&L->s1, D->s1, El * f)) || (st = up(&L->s2, D->s2, El * d)))
       return fail(st);
   }
   *out = L;
@@ -510,29 +522,41 @@ static int layer_reserve(moe_layer* L, int64_t T, int k) {
   return MOE_OK;
 }
 
-static int layer_forward(moe_layer* L, const uint16_t* x, const uint8_t* fin, int64_t T, int k,
-                         int mode, uint16_t* out, cudaStream_t st) {
-  if (T <= 0) return set_error(MOE_EINVAL, "moe_ffn: no rows");
-  if (k < 1 || k > L->E) return set_error(MOE_EINVAL, "moe_ffn: k must be in [1, n_experts]");
-  TRY(layer_reserve(L, T, k));
-  const int64_t d = L->d, f = L->f, E = L->E, S_ = T * k;
-  L->last_T = T;
-  L->last_k = k;
-  // stage events (profiling only): ev[slot*(kStages+1) + i] before stage i
-  const bool prof = L->prof && L->prof_n < moe_layer::kProfCap;
-  cudaEvent_t* evs = prof ? &L->ev[(size_t)L->prof_n * (moe_layer::kStages + 1)] : nullptr;
-  int stage = 0;
+// Stage-event recorder of one forward (profiling only): ev[slot*(kStages+1)+i]
+// before stage i.  Inside a graph capture only an *external* record becomes a
+// real event-record node (readable after each replay).  Level 1 records only
+// the GEMM boundaries (marks 4..6): every event node costs ~2-3 us of pipeline
+// drain, so the cheap level is the one used for kernel timing.
+struct Marks {
+  moe_layer* L;
+  cudaStream_t st;
+  cudaEvent_t* evs = nullptr;
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  if (evs) MOE_CUDA_TRY(cudaStreamIsCapturing(st, &cap));
-  auto mark = [&]() -> int {
-    // inside a graph capture only an *external* record becomes a real event
-    // record node (readable after each replay)
-    if (evs)
+  int stage = 0;
+  Marks(moe_layer* l, cudaStream_t s, bool on) : L(l), st(s) {
+    if (on && L->prof && L->prof_n < moe_layer::kProfCap) {
+      evs = &L->ev[(size_t)L->prof_n * (moe_layer::kStages + 1)];
+      cudaStreamIsCapturing(st, &cap);
+    }
+  }
+  int operator()() {
+    if (evs && (L->prof_level >= 2 || (stage >= 4 && stage <= 6)))
       MOE_CUDA_TRY(cudaEventRecordWithFlags(
           evs[stage], st, cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0));
     ++stage;
     return MOE_OK;
-  };
+  }
+  void done() {
+    if (evs) ++L->prof_n;
+  }
+};
+
+// LN -> gate -> top-k -> plan -> gather into L->xp (stages 0..3)
+static int layer_route(moe_layer* L, const uint16_t* x, const uint8_t* fin, int64_t T, int k,
+                       cudaStream_t st, Marks& mark) {
+  const int64_t d = L->d, E = L->E;
+  L->last_T = T;
+  L->last_k = k;
   MOE_CUDA_TRY(cudaMemsetAsync(L->bad_row, 0xFF, 8, st));  // bad_row + bad_expert
   TRY(mark());
   PlanWork w{L->blockcnt, L->blockbase, L->bad_expert};
@@ -548,23 +572,31 @@ static int layer_forward(moe_layer* L, const uint16_t* x, const uint8_t* fin, in
                                 L->inv, L->offsets, L->problems, L->active, L->xn, d, L->xp,
                                 st));
   } else {
-  TRY(launch_layer_norm(x, T, d, L->ln_g, L->ln_b, L->xn, st));
-  TRY(mark());
-  TRY(launch_gate_logits(L->xn, T, d, L->gw, L->gb, E, L->logits, st));
-  TRY(mark());
-  TRY(launch_gate_topk(L->logits, T, E, k, L->expert, L->scale, L->bad_row, st));
-  TRY(mark());
-  TRY(launch_routing_plan(L->expert, fin, T, k, E, L->perm, L->inv, L->offsets, L->problems,
-                          L->active, w, L->xn, d, L->xp, st));
+    TRY(launch_layer_norm(x, T, d, L->ln_g, L->ln_b, L->xn, st));
+    TRY(mark());
+    TRY(launch_gate_logits(L->xn, T, d, L->gw, L->gb, E, L->logits, st));
+    TRY(mark());
+    TRY(launch_gate_topk(L->logits, T, E, k, L->expert, L->scale, L->bad_row, st));
+    TRY(mark());
+    TRY(launch_routing_plan(L->expert, fin, T, k, E, L->perm, L->inv, L->offsets, L->problems,
+                            L->active, w, L->xn, d, L->xp, st));
   }
-  TRY(mark());
+  return mark();
+}
+
+// FFN1 (ReLU) -> FFN2 over `rows` expert-sorted rows of the LOCAL experts
+// (problems: np device triples, expert ids in [0, El)); stages 4..5
+static int layer_ffn(moe_layer* L, const uint16_t* xin, int64_t rows, const uint32_t* problems,
+                     int64_t np, int mode, uint16_t* h, uint16_t* out, cudaStream_t st,
+                     Marks& mark) {
+  const int64_t d = L->d, f = L->f, El = L->El;
   const uint16_t db = debias_for(L->bits);
-  const int64_t hint = S_ / std::max<int64_t>(1, std::min<int64_t>(E, S_));
-  GemmArgs g1{L->xp, S_, d, L->problems, E, L->w1t, L->s1, L->bits, E, f, L->b1, 1, L->h, db, hint};
-  GemmArgs g2{L->h, S_, f, L->problems, E, L->w2t, L->s2, L->bits, E, d, L->b2, 0, L->y, db, hint};
-  if (mode == MOE_MODE_FAST && S_ <= kGemvMaxRows) {
+  const int64_t hint = rows / std::max<int64_t>(1, std::min<int64_t>(El, rows));
+  GemmArgs g1{xin, rows, d, problems, np, L->w1t, L->s1, L->bits, El, f, L->b1, 1, h, db, hint};
+  GemmArgs g2{h, rows, f, problems, np, L->w2t, L->s2, L->bits, El, d, L->b2, 0, out, db, hint};
+  if (mode == MOE_MODE_FAST && rows <= kGemvMaxRows) {
     // decode regime: stream the active experts' weights (K5)
-    const double act = (double)E * (1.0 - std::pow(1.0 - 1.0 / (double)E, (double)S_));
+    const double act = (double)El * (1.0 - std::pow(1.0 - 1.0 / (double)El, (double)rows));
     GemvWork w1{L->gv_part, L->gv_ticket, gemv_splits(d, f, act)};
     GemvWork w2{L->gv_part, L->gv_ticket, gemv_splits(f, d, act)};
     TRY(launch_gemv(g1, w1, st));
@@ -579,10 +611,23 @@ static int layer_forward(moe_layer* L, const uint16_t* x, const uint8_t* fin, in
     TRY(mark());
     TRY(launch_gemm_exact(g2, st));
   }
+  return mark();
+}
+
+static int layer_forward(moe_layer* L, const uint16_t* x, const uint8_t* fin, int64_t T, int k,
+                         int mode, uint16_t* out, cudaStream_t st) {
+  if (T <= 0) return set_error(MOE_EINVAL, "moe_ffn: no rows");
+  if (k < 1 || k > L->E) return set_error(MOE_EINVAL, "moe_ffn: k must be in [1, n_experts]");
+  if (L->El != L->E)
+    return set_error(MOE_EINVAL, "moe_ffn: layer holds a slice of the experts (use the EP entry points)");
+  TRY(layer_reserve(L, T, k));
+  const int64_t S_ = T * k;
+  Marks mark(L, st, true);
+  TRY(layer_route(L, x, fin, T, k, st, mark));
+  TRY(layer_ffn(L, L->xp, S_, L->problems, L->E, mode, L->h, L->y, st, mark));
+  TRY(launch_combine(x, L->y, L->inv, L->scale, fin, T, L->d, k, out, st));
   TRY(mark());
-  TRY(launch_combine(x, L->y, L->inv, L->scale, fin, T, d, k, out, st));
-  TRY(mark());
-  if (evs) ++L->prof_n;
+  mark.done();
   return MOE_OK;
 }
 
@@ -599,12 +644,14 @@ static int layer_status(moe_layer* L, cudaStream_t st) {
 // nothing executes) and instantiate it; returns the cached exec for `key`.
 template <class F>
 static int layer_graph(moe_layer* L, const moe_layer::GraphKey& key, F&& body,
-                       cudaGraphExec_t* exec) {
+                       cudaGraphExec_t* exec, uint64_t* nlaunch) {
   for (auto& g : L->graphs)
     if (g.key == key) {
       *exec = g.exec;
+      *nlaunch = g.nlaunch;
       return MOE_OK;
     }
+  const uint64_t n0 = g_launches.load();
   if (!L->cap_stream) MOE_CUDA_TRY(cudaStreamCreateWithFlags(&L->cap_stream, cudaStreamNonBlocking));
   MOE_CUDA_TRY(cudaStreamBeginCapture(L->cap_stream, cudaStreamCaptureModeThreadLocal));
   const int rc = body(L->cap_stream);
@@ -619,9 +666,13 @@ static int layer_graph(moe_layer* L, const moe_layer::GraphKey& key, F&& body,
   const cudaError_t ie = cudaGraphInstantiate(&x, g, 0);
   cudaGraphDestroy(g);
   if (ie != cudaSuccess) return set_cuda_error(ie, "graph instantiate");
+  // capture counted the kernels once; replays account for them explicitly
+  const uint64_t nl = g_launches.load() - n0;
+  g_launches.fetch_sub(nl);
   if (L->graphs.size() >= 16) L->drop_graphs();
-  L->graphs.push_back({key, x});
+  L->graphs.push_back({key, x, nl});
   *exec = x;
+  *nlaunch = nl;
   return MOE_OK;
 }
 
@@ -643,12 +694,53 @@ int moe_layer_forward_graph(moe_layer* L, const uint16_t* x, const uint8_t* fini
   if (T <= 0) return set_error(MOE_EINVAL, "moe_ffn: no rows");
   if (k < 1 || k > L->E) return set_error(MOE_EINVAL, "moe_ffn: k must be in [1, n_experts]");
   TRY(layer_reserve(L, T, k));
-  moe_layer::GraphKey key{x, finished, out, T, k, mode, 0, L->prof ? 1 : 0};
+  moe_layer::GraphKey key{x, finished, out, T, k, mode, 0, L->prof_level};
   cudaGraphExec_t exec = nullptr;
+  uint64_t nl = 0;
   TRY(layer_graph(L, key, [&](cudaStream_t cs) { return layer_forward(L, x, finished, T, k, mode, out, cs); },
-                  &exec));
+                  &exec, &nl));
   MOE_CUDA_TRY(cudaGraphLaunch(exec, S(stream)));
+  g_launches.fetch_add(nl);
   return MOE_OK;
+}
+
+int moe_layer_route(moe_layer* L, const uint16_t* x, const uint8_t* finished, int64_t T, int k,
+                    moe_stream_t stream) {
+  if (!L) return set_error(MOE_EINVAL, "layer: null");
+  if (T <= 0) return set_error(MOE_EINVAL, "moe_ffn: no rows");
+  if (k < 1 || k > L->E) return set_error(MOE_EINVAL, "moe_ffn: k must be in [1, n_experts]");
+  TRY(layer_reserve(L, T, k));
+  Marks mark(L, S(stream), false);
+  return layer_route(L, x, finished, T, k, S(stream), mark);
+}
+
+int moe_layer_buffers(moe_layer* L, const uint16_t** xp, uint16_t** y) {
+  if (!L) return set_error(MOE_EINVAL, "layer: null");
+  if (xp) *xp = L->xp;
+  if (y) *y = L->y;
+  return MOE_OK;
+}
+
+int moe_layer_experts(moe_layer* L, const uint16_t* xin, int64_t rows, const uint32_t* problems,
+                      int64_t np, int mode, uint16_t* out, moe_stream_t stream) {
+  if (!L) return set_error(MOE_EINVAL, "layer: null");
+  if (rows < 0 || np < 0 || np > L->El) return set_error(MOE_EINVAL, "moe_ffn: bad problem list");
+  if (rows == 0 || np == 0) return MOE_OK;
+  if (rows > L->ep_cap) {  // hidden-activation workspace for received rows
+    if (L->ep_h) L->release(L->ep_h);
+    L->drop_graphs();
+    TRY(L->alloc(&L->ep_h, rows * L->f * 2));
+    L->ep_cap = rows;
+  }
+  TRY(layer_reserve(L, 1, 1));  // GEMV split-K workspace
+  Marks mark(L, S(stream), false);
+  return layer_ffn(L, xin, rows, problems, np, mode, L->ep_h, out, S(stream), mark);
+}
+
+int moe_layer_combine(moe_layer* L, const uint16_t* x, const uint16_t* y, const uint8_t* finished,
+                      int64_t T, int k, uint16_t* out, moe_stream_t stream) {
+  if (!L) return set_error(MOE_EINVAL, "layer: null");
+  return launch_combine(x, y, L->inv, L->scale, finished, T, L->d, k, out, S(stream));
 }
 
 int moe_layer_create(const moe_layer_desc* desc, moe_layer** out) {
@@ -689,10 +781,12 @@ int moe_layer_forward_host(moe_layer* L, const uint16_t* x_host, const uint8_t* 
   if (is_pinned(x_host) && is_pinned(out_host) && is_pinned(fin_host)) {
     // pinned buffers: one captured graph (copies + kernels + status readback)
     if (!L->hstatus) MOE_CUDA_TRY(cudaMallocHost(&L->hstatus, 8));
-    moe_layer::GraphKey key{x_host, fin_host, out_host, T, k, mode, 1, L->prof ? 1 : 0};
+    moe_layer::GraphKey key{x_host, fin_host, out_host, T, k, mode, 1, L->prof_level};
     cudaGraphExec_t exec = nullptr;
-    TRY(layer_graph(L, key, [&](cudaStream_t cs) { return body(cs, L->hstatus); }, &exec));
+    uint64_t nl = 0;
+    TRY(layer_graph(L, key, [&](cudaStream_t cs) { return body(cs, L->hstatus); }, &exec, &nl));
     MOE_CUDA_TRY(cudaGraphLaunch(exec, st));
+    g_launches.fetch_add(nl);
     MOE_CUDA_TRY(cudaStreamSynchronize(st));
     hs[0] = L->hstatus[0];
     hs[1] = L->hstatus[1];
@@ -728,6 +822,7 @@ int moe_layer_profile(moe_layer* L, int enable) {
     for (auto& e : L->ev) MOE_CUDA_TRY(cudaEventCreate(&e));
   }
   L->prof = enable != 0;
+  L->prof_level = enable;
   L->prof_n = 0;
   L->drop_graphs();  // event slots are baked into captured graphs
   return MOE_OK;
@@ -738,8 +833,10 @@ int moe_layer_profile_read(moe_layer* L, double* stage_ms, int* forwards) {
   for (int i = 0; i < moe_layer::kStages; ++i) stage_ms[i] = 0.0;
   for (int f = 0; f < L->prof_n; ++f) {
     cudaEvent_t* e = &L->ev[(size_t)f * (moe_layer::kStages + 1)];
-    MOE_CUDA_TRY(cudaEventSynchronize(e[moe_layer::kStages]));
+    const bool all = L->prof_level >= 2;
+    MOE_CUDA_TRY(cudaEventSynchronize(e[all ? moe_layer::kStages : 6]));
     for (int i = 0; i < moe_layer::kStages; ++i) {
+      if (!all && (i < 4 || i > 5)) continue;
       float ms = 0.f;
       MOE_CUDA_TRY(cudaEventElapsedTime(&ms, e[i], e[i + 1]));
       stage_ms[i] += ms;

@@ -159,7 +159,9 @@ class MoELayer:
     """
 
     def __init__(self, ln_g, ln_b, gate_w, gate_b, w1, b1, w2, b2, bits=4, q=None,
-                 device="cuda"):
+                 device="cuda", expert_range=None):
+        """expert_range=(e_begin, e_count): w1/w2/b1/b2 (and q) hold only those
+        experts (expert parallelism); the gate always covers all E."""
         def T(a):
             if isinstance(a, torch.Tensor):
                 return a.to(device).contiguous()
@@ -171,8 +173,9 @@ class MoELayer:
 
         self.bits = bits
         d, E = gate_w.shape
-        f = w1.shape[2]
+        f = (w1.shape[2] if w1 is not None else q[1].shape[1])
         self.d, self.f, self.E = d, f, E
+        self.e_begin, self.e_count = expert_range if expert_range else (0, E)
         keep = dict(ln_g=T(ln_g), ln_b=T(ln_b), gate_w=T(gate_w), gate_b=T(gate_b), b1=T(b1),
                     b2=T(b2))
         if bits == 16:
@@ -187,7 +190,7 @@ class MoELayer:
         desc = abi.LayerDesc(d, f, E, bits, *[
             keep[nm].data_ptr() if nm in keep else None
             for nm in ("ln_g", "ln_b", "gate_w", "gate_b", "b1", "b2", "w1", "w2", "q1", "q2",
-                       "s1", "s2")])
+                       "s1", "s2")], *((self.e_begin, self.e_count) if expert_range else (0, 0)))
         h = C.c_void_p()
         torch.cuda.synchronize()
         abi.call("moe_layer_create_device", C.byref(desc), C.byref(h))
@@ -253,11 +256,47 @@ class MoELayer:
                     offsets=get(ptrs[4], E + 1, np.uint32),
                     active=int(get(ptrs[5], 1, np.uint32)[0]))
 
+    # ---- expert-parallel building blocks (moe_layer_route / _experts / _combine)
+    def route(self, x, finished=None, k=1, stream=None):
+        """LN -> gate -> top-k -> plan -> gather into the layer workspace."""
+        abi.call("moe_layer_route", self._h, _p(x), _p(finished), x.shape[0], k, _stream(stream))
+
+    def buffers(self):
+        """(xp, y) device pointers of the layer workspace (expert-sorted rows)."""
+        xp, y = C.c_void_p(), C.c_void_p()
+        abi.call("moe_layer_buffers", self._h, C.byref(xp), C.byref(y))
+        return xp.value, y.value
+
+    def experts(self, xin, problems, mode=MODE_FAST, out=None, stream=None):
+        """FFN1+FFN2 of the LOCAL experts over expert-sorted rows; problems:
+        (np, 3) int32 device tensor with local expert ids."""
+        rows = xin.shape[0]
+        if out is None:
+            out = torch.empty((rows, self.d), dtype=torch.float16, device=xin.device)
+        abi.call("moe_layer_experts", self._h, _p(xin), rows, _p(problems), problems.shape[0],
+                 mode, _p(out), _stream(stream))
+        return out
+
+    def combine(self, x, y_ptr, finished=None, k=1, out=None, stream=None):
+        """out = finished ? x : x + sum_s y[inv[r,s]] * scale[r,s] (last route's plan)."""
+        if out is None:
+            out = torch.empty_like(x)
+        abi.call("moe_layer_combine", self._h, _p(x), C.c_void_p(y_ptr), _p(finished),
+                 x.shape[0], k, _p(out), _stream(stream))
+        return out
+
+    def offsets_device(self):
+        """(E+1) int32 device view of the last plan's expert offsets."""
+        ptrs = [C.c_void_p() for _ in range(6)]
+        abi.call("moe_layer_routing", self._h, *[C.byref(p) for p in ptrs])
+        return ptrs[4].value
+
     STAGES = ("layer_norm", "gate_logits", "gate_topk", "routing_plan", "ffn1", "ffn2",
               "combine")
 
     def profile(self, enable=True):
-        """Start (reset) / stop per-stage CUDA-event timing (moe_layer_profile)."""
+        """Start (reset) / stop CUDA-event timing (moe_layer_profile): 1 / True =
+        grouped-GEMM boundaries only, 2 = every stage, 0 / False = off."""
         abi.call("moe_layer_profile", self._h, int(enable))
 
     def profile_read(self):
