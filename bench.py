@@ -225,6 +225,140 @@ def make_layers(E, d, f, T, k, R, device, seed):
     return layers, xs
 
 
+def make_ep_layers(E, d, f, T, k, R, dev, rank, G):
+    """R expert-parallel layer copies: identical full weights on every rank
+    (same seeds), each rank keeping the full gate and its E/G experts."""
+    import torch
+    from paper_2211_10017_b200.ep import CudaRank, owner_range
+    from paper_2211_10017_b200.ops import MoELayer
+    e0, el = owner_range(E, G, rank)
+    sl = slice(e0, e0 + el)
+    g = torch.Generator(device=dev)
+    ranks, xs = [], []
+    for r in range(R):
+        g.manual_seed(7000 + r)
+        n = lambda shape, s: (torch.randn(shape, generator=g, device=dev) * s).half()  # noqa
+        ln_g = (1 + 0.1 * torch.randn(d, generator=g, device=dev)).half()
+        ln_b, gw, gb = n((d,), 0.05), n((d, E), 1 / math.sqrt(d)), n((E,), 0.02)
+        w1, b1 = n((E, d, f), 1 / math.sqrt(d)), n((E, f), 0.02)
+        w2, b2 = n((E, f, d), 1 / math.sqrt(f)), n((E, d), 0.02)
+        L = MoELayer(ln_g, ln_b, gw, gb, w1[sl], b1[sl], w2[sl], b2[sl], bits=4, device=dev,
+                     expert_range=(e0, el))
+        L.quant = None
+        L.reserve(T, k)
+        ranks.append(CudaRank(L))
+        gx = torch.Generator(device=dev)
+        gx.manual_seed(9000 + 97 * rank + r)
+        xs.append(torch.randn((T, d), generator=gx, device=dev).half())
+    torch.cuda.synchronize()
+    return ranks, xs
+
+
+def run_native_ep(args, wl):
+    """N > 1: expert parallelism (ep.py) -- each rank owns E/N experts and
+    T tokens; NCCL all-to-all-v dispatch/combine every step (weak scaling)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2211_10017_b200 import abi
+    from paper_2211_10017_b200.ep import DistComm, ep_forward
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if "MASTER_ADDR" not in os.environ:  # --force-ep outside torchrun: world of 1
+        import socket
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(sk.getsockname()[1]),
+                          RANK="0", WORLD_SIZE="1")
+        sk.close()
+    dist.init_process_group("nccl", device_id=dev)
+    E, d, f, T, k, label = wl
+    if E % ws != 0:
+        raise SystemExit(f"ep: {E} experts not divisible by {ws} GPUs")
+    per_copy = E // ws * d * f + 2 * T * d * 2 + 2 * T * k * (d + f) * 2
+    R = max(2, min(32, math.ceil(2 * L2_BYTES / per_copy)))
+    ranks, xs = make_ep_layers(E, d, f, T, k, R, dev, rank, ws)
+    comm = DistComm()
+    stream = torch.cuda.current_stream()
+
+    def step(i):
+        return ep_forward([ranks[i % R]], comm, [xs[i % R]], [None], k=k, mode=1)[0]
+
+    for i in range(args.warmup + R):
+        step(i)
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n0 = abi.launch_count()
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for i in range(args.steps):
+            step(i)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = abi.launch_count() - n0
+    dist.barrier()
+    t = torch.tensor([ev0.elapsed_time(ev1)], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    value = ws * args.steps * T / (ms / 1e3)
+    # e2e: pinned host tokens in, EP forward, host result out, every step
+    xh = torch.empty((T, d), dtype=torch.float16, pin_memory=True)
+    oh = torch.empty((T, d), dtype=torch.float16, pin_memory=True)
+    xh.copy_(xs[0])
+    xd = torch.empty_like(xs[0])
+
+    def e2e_step(i):
+        xd.copy_(xh, non_blocking=True)
+        out = ep_forward([ranks[i % R]], comm, [xd], [None], k=k, mode=1)[0]
+        oh.copy_(out, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+
+    for i in range(args.warmup):
+        e2e_step(i)
+    dist.barrier()
+    e0_, e1_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0_.record(stream)
+    for i in range(args.steps):
+        e2e_step(i)
+    e1_.record(stream)
+    torch.cuda.synchronize()
+    t = torch.tensor([e0_.elapsed_time(e1_)], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_value = ws * args.steps * T / (float(t.item()) / 1e3)
+    hbm, tc_burst, tc_sus, peak_src = load_peaks()
+    S = T * k
+    flops = 4.0 * S * d * f  # per rank per step (balanced routing)
+    achieved = flops / (ms / args.steps * 1e-3) / 1e12
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f16 (int4 weight-only experts, f32 accumulate)",
+        "data": "synthetic (random_model init distributions, seeded, generated on device)",
+        "config": {"workload": label, "E": E, "d_model": d, "d_ff": f, "tokens_per_gpu": T,
+                   "top_k": k, "bits": 4, "mode": "fast", "parallelism": f"ep{ws}",
+                   "experts_per_gpu": E // ws,
+                   "transport": "NCCL all_to_all_single (counts, dispatch, combine)",
+                   "l2": f"inputs larger than L2: {R} distinct layer copies rotated"},
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": tc_burst,
+                     "unit": "TFLOP/s", "frac": achieved / tc_burst, "traffic": None,
+                     "kernel": "whole EP layer step (layer-level: 4*T*k*d*f per rank / step time)",
+                     "peak_source": peak_src},
+        "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": T * d * 2,
+                "d2h_bytes_per_step": T * d * 2, "path": "EPMoELayer-equivalent ep_forward"},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def run_native(args, wl):
     import numpy as np
     import torch
@@ -233,10 +367,10 @@ def run_native(args, wl):
     from paper_2211_10017_b200 import abi
 
     ws, rank, local = dist_env()
+    if ws > 1 or args.force_ep:
+        return run_native_ep(args, wl)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if ws > 1:
-        dist.init_process_group("nccl", device_id=dev)
     E, d, f, T, k, label = wl
     per_copy = E * d * f + 2 * T * d * 2 + T * k * (d + f) * 2  # weights + x/out + xp/h
     R = max(2, min(64, math.ceil(2 * L2_BYTES / per_copy)))
@@ -412,6 +546,7 @@ def main():
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--force-ep", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     wl = WORKLOADS[args.workload]

@@ -485,7 +485,7 @@ static int layer_reserve(moe_layer* L, int64_t T, int k) {
                   (void*)L->blockcnt, (void*)L->dx, (void*)L->dout, (void*)L->dfin})
     if (p) L->release(p);
   const int64_t d = L->d, f = L->f, E = L->E;
-  const int64_t nblk = std::max(plan_blocks(cS), (cT + 7) / 8);  // plan or fused-gate blocks
+  const int64_t nblk = std::max(plan_blocks(cS), cT);  // plan or gate blocks (>= 1 row each)
   TRY(L->alloc(&L->xn, cT * d * 2));
   TRY(L->alloc(&L->xp, cS * d * 2));
   TRY(L->alloc(&L->h, cS * f * 2));
@@ -563,7 +563,7 @@ static int layer_route(moe_layer* L, const uint16_t* x, const uint8_t* fin, int6
   if (gate_fused_supported(d, E, k) && (reinterpret_cast<uintptr_t>(x) & 15) == 0) {
     // one kernel: LN + logits + top-k + key histogram; then scan/place/gather
     GateFusedArgs ga{x, T, d, L->ln_g, L->ln_b, L->gw32, L->gwp, L->gb, E, k, fin, L->xn,
-                     L->expert, L->scale, L->blockcnt, L->bad_row, gate_fused_rows(T)};
+                     L->expert, L->scale, L->blockcnt, L->bad_row, gate_fused_rows(T, E, k)};
     TRY(launch_gate_fused(ga, st));
     TRY(mark());
     TRY(mark());

@@ -1,229 +1,257 @@
-// k_gate_fused.cu -- K2 fused gating for the layer hot path:
+// k_gate_fused.cu -- K2 gating for the layer hot path, bit-exact with
 //   LayerNorm (proj/src/model.cpp:175-205) -> f32 gate logits (:273-297) ->
 //   top-k softmax gate (proj/src/routing.cpp:11-41, top-k extension) ->
-//   per-block routing-key histogram (routing.cpp:55-62, first pass of the
-//   counting sort) in ONE kernel, bit-exact with the reference.
+//   per-block routing-key histogram (routing.cpp:55-62, first counting-sort
+//   pass), as two kernels:
 //
-// A CTA owns ROWS token rows (staged once in shared memory by cp.async) and
-// runs every serial chain the reference defines on them:
-//   * LN: one thread per row does the left-to-right f32 sum and the centred
-//     sum of squares (the only true serial chains); all 256 threads then
-//     normalise and write xn (shared + global, 16-byte stores).
-//   * logits: every (row, expert) pair is an independent serial chain over
-//     k; lane -> row, (warp, lane / ROWS) -> a group of EPG experts held in
-//     registers.  fp16 x fp16 products are exact in f32, so fmaf == the
-//     reference's mul-then-add; only the k order matters and is kept.  Gate
-//     weights are pre-widened to f32 once per layer and streamed through a
-//     3-stage cp.async ring of KC-row chunks (warp-broadcast reads).
-//   * top-k: argmax by warp shuffle (value desc, index asc == the
-//     reference's first maximum with strict '>'), expf of every logit in
-//     parallel (device port of glibc expf), then one thread per row sums
-//     them in expert order.
-//   * histogram: key = finished ? E : expert per slot r*k+s, counted in
-//     shared memory; blockcnt[block][E+1] feeds plan_scan (k_route.cu),
-//     whose blocks are exactly this kernel's ROWS*k slots.
+// ln_rows_kernel -- 16 token rows per CTA arrive by bulk copy (TMA engine);
+//   one lane per row runs the reference's two serial f32 chains (sum, then
+//   centred sum of squares, every op RN32, no contraction); all threads then
+//   normalise and write xn.  The chains are the latency floor of the whole
+//   layer at decode sizes (2*d dependent FADDs per row).
+//
+// gate_topk_kernel -- every (row, expert) logit is its own serial k-chain;
+//   products of two fp16 values are exact in f32, so fmaf == the reference's
+//   mul-then-add and only the k order matters.  A thread owns RPT rows x EPG
+//   experts of chains in registers (FMA-bound, ~1.25 issue slots per FMA);
+//   xn and the pre-widened f32 gate weights stream through a 3-stage cp.async
+//   ring of KC-input chunks (weights read as warp broadcasts, rows
+//   conflict-free).  Then: warp-shuffle argmax (value desc, index asc == the
+//   reference's first maximum under strict '>'), expf of every logit in
+//   parallel (device port of glibc expf), one thread per row sums them in
+//   expert order, gate scales, and a shared-memory histogram of routing keys
+//   (finished ? E : expert) written key-major as blockcnt[key][block] for
+//   plan_scan (k_route.cu), whose blocks are this kernel's RB*k slots.
 #include "kernels.cuh"
 
 namespace moecu {
 
-namespace gf {
-constexpr int kThreads = 256;
-constexpr int kMaxRing = 16;            // mbarriers in the gate-weight ring
-constexpr size_t kBudget = 100 * 1024;  // target smem per CTA (2 CTAs / SM)
+// =================================================================== LN rows
+namespace lnr {
+constexpr int ROWS = 16;
+constexpr int kThreads = 128;
+}  // namespace lnr
 
-struct Smem {
-  int xp;      // row pitch (halves)
-  int lp;      // logits row pitch (floats)
-  int kc;      // gate-weight rows per chunk
-  int ring;    // chunks resident at once
-  size_t off_w, off_l, off_st, off_h, off_bar, total;
-};
-
-// gwp = pitch (floats) of the widened gate weights in global and shared memory
-__host__ __device__ inline Smem layout(int rows, int d, int E, int gwp) {
-  Smem s;
-  s.xp = d + 8;
-  s.lp = E + 1;
-  size_t off = (size_t)rows * s.xp * 2;
-  off = (off + 15) & ~size_t(15);
-  s.off_w = off;
-  const size_t fixed = off + (size_t)2 * rows * s.lp * 4 + (size_t)rows * 10 * 4 +
-                       (size_t)(E + 1) * 4 + kMaxRing * 8 + 256;
-  // chunk: a multiple of 8 rows, ~8-16 KB; ring: as deep as the budget allows
-  int kc = (int)(16384 / ((size_t)gwp * 4)) / 8 * 8;
-  kc = kc < 8 ? 8 : (kc > 128 ? 128 : kc);
-  if (kc > d) kc = (d + 7) / 8 * 8;
-  const int nch = (d + kc - 1) / kc;
-  const size_t cb = (size_t)kc * gwp * 4;
-  int ring = fixed + cb * 2 < kBudget ? (int)((kBudget - fixed) / cb) : 2;
-  ring = ring < 2 ? 2 : (ring > kMaxRing ? kMaxRing : ring);
-  if (ring > nch) ring = nch;
-  s.kc = kc;
-  s.ring = ring;
-  off += cb * ring + 64;  // + over-read slack of the last expert group
-  off = (off + 15) & ~size_t(15);
-  s.off_l = off;
-  off += (size_t)2 * rows * s.lp * 4;  // logits, then expf values
-  s.off_st = off;
-  off += (size_t)rows * 2 * 4 + (size_t)rows * 8 * 4;  // mean, inv, sel[8]
-  s.off_h = off;
-  off += (size_t)(E + 1) * 4;
-  off = (off + 7) & ~size_t(7);
-  s.off_bar = off;
-  off += (kMaxRing + 1) * 8;
-  s.total = (off + 15) & ~size_t(15);
-  return s;
-}
-}  // namespace gf
-
-template <int ROWS, int EPG>
-__global__ void __launch_bounds__(gf::kThreads) gate_fused_kernel(
+__global__ void __launch_bounds__(lnr::kThreads) ln_rows_kernel(
     const uint16_t* __restrict__ x, int64_t T, int d, const uint16_t* __restrict__ g,
-    const uint16_t* __restrict__ b, const float* __restrict__ gw32, int gwp,
-    const uint16_t* __restrict__ gb, int E, int k, const uint8_t* __restrict__ finished,
-    uint16_t* __restrict__ xn_out, uint32_t* __restrict__ expert, uint16_t* __restrict__ scale,
-    uint32_t* __restrict__ blockcnt, uint32_t* bad_row) {
-  constexpr int RPW = 32 / ROWS;       // row groups per warp
+    const uint16_t* __restrict__ b, uint16_t* __restrict__ xn) {
   extern __shared__ __align__(16) uint8_t sm[];
-  const gf::Smem L = gf::layout(ROWS, d, E, gwp);
+  const int xp = d + 8;
   uint16_t* xs = reinterpret_cast<uint16_t*>(sm);
-  float* ws = reinterpret_cast<float*>(sm + L.off_w);
-  float* lg = reinterpret_cast<float*>(sm + L.off_l);
-  float* st_mean = reinterpret_cast<float*>(sm + L.off_st);
-  float* st_inv = st_mean + ROWS;
-  uint32_t* sel = reinterpret_cast<uint32_t*>(st_inv + ROWS);  // [ROWS][8]
-  uint32_t* hist = reinterpret_cast<uint32_t*>(sm + L.off_h);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L.off_bar);  // [ring] chunks, [kMaxRing] rows
-
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t r0 = (int64_t)blockIdx.x * ROWS;
-  const int nrow = (int)::min((int64_t)ROWS, T - r0);
+  float* st = reinterpret_cast<float*>(sm + (size_t)lnr::ROWS * xp * 2);  // mean, inv
+  uint64_t* bar = reinterpret_cast<uint64_t*>(st + 2 * lnr::ROWS);
+  const int tid = threadIdx.x;
+  const int64_t r0 = (int64_t)blockIdx.x * lnr::ROWS;
+  const int nrow = (int)::min((int64_t)lnr::ROWS, T - r0);
   const int d8 = d / 8;
-  const int KC = L.kc, NSL = L.ring;
-  const int nch = (d + KC - 1) / KC;
-
-  for (int i = tid; i <= E; i += gf::kThreads) hist[i] = 0;
-
-  // ---- bulk-copy the rows and the first NSL gate-weight chunks (TMA engine)
-  auto issue = [&](int c) {  // thread 0 only
-    const int stg = c % NSL;
-    const int kc = ::min(KC, d - c * KC);
-    const uint32_t bytes = (uint32_t)kc * gwp * 4;
-    mbar_arrive_expect_tx(&bars[stg], bytes);
-    bulk_load(ws + (size_t)stg * KC * gwp, gw32 + (size_t)c * KC * gwp, bytes, &bars[stg]);
-  };
   if (tid == 0) {
-    for (int i = 0; i <= gf::kMaxRing; ++i) mbar_init(&bars[i], 1);
+    mbar_init(bar, 1);
     fence_barrier_init();
-    uint64_t* bx = &bars[gf::kMaxRing];
-    mbar_arrive_expect_tx(bx, (uint32_t)nrow * d * 2);
-    for (int r = 0; r < nrow; ++r) bulk_load(xs + r * L.xp, x + (r0 + r) * d, (uint32_t)d * 2, bx);
-    for (int c = 0; c < ::min(NSL, nch); ++c) issue(c);
+    mbar_arrive_expect_tx(bar, (uint32_t)nrow * d * 2);
+    for (int r = 0; r < nrow; ++r) bulk_load(xs + r * xp, x + (r0 + r) * d, (uint32_t)d * 2, bar);
   }
   __syncthreads();
-  mbar_wait(&bars[gf::kMaxRing], 0);  // rows landed
-
-  // ---- LN statistics: one serial chain per row (model.cpp:178-192)
-  if (tid < nrow) {
-    const uint16_t* row = xs + tid * L.xp;
+  mbar_wait(bar, 0);
+  if (tid < nrow) {  // model.cpp:178-192, serial
+    // the next 16 bytes are loaded while the current 8 adds run (the shared
+    // load latency would otherwise sit on the dependent chain)
+    const uint4* row = reinterpret_cast<const uint4*>(xs + tid * xp);
     float s = 0.f;
+    uint4 cur = row[0];
     for (int c = 0; c < d8; ++c) {
-      const uint4 v = *reinterpret_cast<const uint4*>(row + c * 8);
-      const uint16_t* h = reinterpret_cast<const uint16_t*>(&v);
+      const uint4 nxt = row[c + 1 < d8 ? c + 1 : c];
+      const uint16_t* h = reinterpret_cast<const uint16_t*>(&cur);
 #pragma unroll
       for (int i = 0; i < 8; ++i) s = __fadd_rn(s, h2f(h[i]));
+      cur = nxt;
     }
     const float mean = __fdiv_rn(s, (float)d);
     float v2 = 0.f;
+    cur = row[0];
     for (int c = 0; c < d8; ++c) {
-      const uint4 v = *reinterpret_cast<const uint4*>(row + c * 8);
-      const uint16_t* h = reinterpret_cast<const uint16_t*>(&v);
+      const uint4 nxt = row[c + 1 < d8 ? c + 1 : c];
+      const uint16_t* h = reinterpret_cast<const uint16_t*>(&cur);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const float dx = __fsub_rn(h2f(h[i]), mean);
         v2 = __fadd_rn(v2, __fmul_rn(dx, dx));
       }
+      cur = nxt;
     }
-    const float var = __fdiv_rn(v2, (float)d);
-    st_mean[tid] = mean;
-    st_inv[tid] = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(var, 1e-5f)));
+    st[tid] = mean;
+    st[lnr::ROWS + tid] = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(v2, (float)d), 1e-5f)));
   }
   __syncthreads();
-
-  // ---- normalise (model.cpp:193-194): xs <- xn, and xn -> global
-  for (int i = tid; i < nrow * d8; i += gf::kThreads) {
+  for (int i = tid; i < nrow * d8; i += lnr::kThreads) {  // model.cpp:193-194
     const int r = i / d8, c = i % d8;
-    uint4 v = *reinterpret_cast<const uint4*>(xs + r * L.xp + c * 8);
+    uint4 v = *reinterpret_cast<const uint4*>(xs + r * xp + c * 8);
     const uint4 gv = __ldg(reinterpret_cast<const uint4*>(g) + c);
     const uint4 bv = __ldg(reinterpret_cast<const uint4*>(b) + c);
     uint16_t* h = reinterpret_cast<uint16_t*>(&v);
     const uint16_t* gh = reinterpret_cast<const uint16_t*>(&gv);
     const uint16_t* bh = reinterpret_cast<const uint16_t*>(&bv);
-    const float mean = st_mean[r], inv = st_inv[r];
+    const float mean = st[r], inv = st[lnr::ROWS + r];
 #pragma unroll
     for (int j = 0; j < 8; ++j)
       h[j] = f2h(__fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(h2f(h[j]), mean), inv), h2f(gh[j])),
                            h2f(bh[j])));
-    *reinterpret_cast<uint4*>(xs + r * L.xp + c * 8) = v;
-    *reinterpret_cast<uint4*>(xn_out + (r0 + r) * d + c * 8) = v;
+    *reinterpret_cast<uint4*>(xn + (r0 + r) * d + c * 8) = v;
   }
+}
 
-  // ---- logits: serial k chains (model.cpp:284-288)
-  const int rr = lane % ROWS;
-  const int grp = warp * RPW + lane / ROWS;
-  const int e0 = grp * EPG;
-  float acc[EPG];
+// ========================================================== logits + top-k
+namespace gk {
+constexpr int kThreads = 256;
+constexpr int NS = 3;
+
+struct Cfg {
+  int ng;       // expert groups (power of two)
+  int rt;       // row-threads = kThreads / ng
+  int rb;       // rows per CTA = rt * rpt
+  int kc;       // inputs per pipeline chunk
+  int xpitch;   // xn chunk row pitch (halves)
+  size_t xbytes, wbytes, stage, body, total;
+};
+
+__host__ __device__ inline int pow2_at_least(int v) {
+  int p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+__host__ __device__ inline Cfg cfg(int E, int gwp, int epg, int rpt) {
+  Cfg c;
+  c.ng = pow2_at_least((E + epg - 1) / epg);
+  if (c.ng > kThreads) c.ng = kThreads;
+  c.rt = kThreads / c.ng;
+  c.rb = c.rt * rpt;
+  int kc = (int)(16384 / ((size_t)gwp * 4)) / 8 * 8;
+  c.kc = kc < 16 ? 16 : (kc > 64 ? 64 : kc);
+  c.xpitch = c.kc + 8;
+  c.xbytes = (size_t)c.rb * c.xpitch * 2;
+  c.wbytes = (size_t)c.kc * gwp * 4 + 64;  // + over-read slack of the last expert group
+  c.stage = (c.xbytes + c.wbytes + 15) & ~size_t(15);
+  const size_t pipe = NS * c.stage;
+  const size_t lg = (size_t)2 * c.rb * (E + 1) * 4;  // logits + expf values (reuse the ring)
+  c.body = ((pipe > lg ? pipe : lg) + 15) & ~size_t(15);
+  c.total = c.body + (size_t)c.rb * 8 * 4 + (size_t)(E + 1) * 4 + 16;  // + sel[8], hist
+  return c;
+}
+}  // namespace gk
+
+template <int EPG, int RPT>
+__global__ void __launch_bounds__(gk::kThreads) gate_topk_kernel(
+    const uint16_t* __restrict__ xn, int64_t T, int d, const float* __restrict__ gw32, int gwp,
+    const uint16_t* __restrict__ gb, int E, int k, const uint8_t* __restrict__ finished,
+    uint32_t* __restrict__ expert, uint16_t* __restrict__ scale, uint32_t* __restrict__ blockcnt,
+    uint32_t* bad_row) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const gk::Cfg C = gk::cfg(E, gwp, EPG, RPT);
+  uint32_t* sel = reinterpret_cast<uint32_t*>(sm + C.body);  // [rb][8]
+  uint32_t* hist = sel + C.rb * 8;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int rt = tid % C.rt, eg = tid / C.rt;  // row-thread fastest: a warp shares eg
+  const int e0 = eg * EPG;
+  const int64_t r0 = (int64_t)blockIdx.x * C.rb;
+  const int nrow = (int)::min((int64_t)C.rb, T - r0);
+  const int KC = C.kc, nch = (d + KC - 1) / KC;
+  const int wq = (E + 3) / 4;  // 16-byte pieces per gate-weight row
+
+  for (int i = tid; i <= E; i += gk::kThreads) hist[i] = 0;
+
+  auto issue = [&](int c) {
+    if (c < nch) {
+      uint8_t* stg = sm + (size_t)(c % gk::NS) * C.stage;
+      uint16_t* xs = reinterpret_cast<uint16_t*>(stg);
+      float* ws = reinterpret_cast<float*>(stg + C.xbytes);
+      const int k0 = c * KC, kc = ::min(KC, d - k0), kq = kc / 8;
+      for (int i = tid; i < C.rb * kq; i += gk::kThreads) {
+        const int r = i / kq, q = i % kq;
+        const bool ok = r < nrow;
+        cp_async16(xs + r * C.xpitch + q * 8, ok ? xn + (r0 + r) * d + k0 + q * 8 : xn, ok);
+      }
+      for (int i = tid; i < kc * wq; i += gk::kThreads) {
+        const int kk = i / wq, q = i % wq;
+        cp_async16(ws + kk * gwp + q * 4, gw32 + (size_t)(k0 + kk) * gwp + q * 4, true);
+      }
+    }
+    cp_async_commit();
+  };
+  for (int c = 0; c < gk::NS - 1; ++c) issue(c);
+
+  float acc[RPT][EPG];
 #pragma unroll
-  for (int j = 0; j < EPG; ++j) acc[j] = 0.f;
-  const uint16_t* xrow = xs + rr * L.xp;
-  __syncthreads();  // xn complete in shared memory
+  for (int i = 0; i < RPT; ++i)
+#pragma unroll
+    for (int j = 0; j < EPG; ++j) acc[i][j] = 0.f;
+
   for (int c = 0; c < nch; ++c) {
-    const int stg = c % NSL;
-    mbar_wait(&bars[stg], (uint32_t)(c / NSL) & 1u);
-    const float* wc = ws + (size_t)stg * KC * gwp + e0;
-    const int k0 = c * KC, kc = ::min(KC, d - k0);
+    cp_async_wait<gk::NS - 2>();
+    __syncthreads();
+    issue(c + gk::NS - 1);
+    const uint8_t* stg = sm + (size_t)(c % gk::NS) * C.stage;
+    const uint16_t* xs = reinterpret_cast<const uint16_t*>(stg);
+    const float* ws = reinterpret_cast<const float*>(stg + C.xbytes) + e0;
+    const int kc = ::min(KC, d - c * KC);
     if (e0 < E) {
       for (int kk = 0; kk < kc; kk += 8) {
-        const uint4 v = *reinterpret_cast<const uint4*>(xrow + k0 + kk);
-        const uint16_t* h = reinterpret_cast<const uint16_t*>(&v);
+        uint4 xv[RPT];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const float xv = h2f(h[i]);
-          const float* wr = wc + (kk + i) * gwp;
+        for (int i = 0; i < RPT; ++i)
+          xv[i] = *reinterpret_cast<const uint4*>(xs + (rt + i * C.rt) * C.xpitch + kk);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float* wr = ws + (kk + q) * gwp;
+          float w[EPG];
           if constexpr (EPG >= 4) {
 #pragma unroll
             for (int j = 0; j < EPG; j += 4) {
               const float4 w4 = *reinterpret_cast<const float4*>(wr + j);
-              acc[j] = fmaf(xv, w4.x, acc[j]);
-              acc[j + 1] = fmaf(xv, w4.y, acc[j + 1]);
-              acc[j + 2] = fmaf(xv, w4.z, acc[j + 2]);
-              acc[j + 3] = fmaf(xv, w4.w, acc[j + 3]);
+              w[j] = w4.x;
+              w[j + 1] = w4.y;
+              w[j + 2] = w4.z;
+              w[j + 3] = w4.w;
             }
           } else {
 #pragma unroll
-            for (int j = 0; j < EPG; ++j) acc[j] = fmaf(xv, wr[j], acc[j]);
+            for (int j = 0; j < EPG; ++j) w[j] = wr[j];
+          }
+#pragma unroll
+          for (int i = 0; i < RPT; ++i) {
+            const float xf = h2f(reinterpret_cast<const uint16_t*>(&xv[i])[q]);
+#pragma unroll
+            for (int j = 0; j < EPG; ++j) acc[i][j] = fmaf(xf, w[j], acc[i][j]);  // exact product
           }
         }
       }
     }
-    __syncthreads();  // stage consumed by every thread
-    if (tid == 0 && c + NSL < nch) issue(c + NSL);
   }
+  cp_async_wait<0>();
+  __syncthreads();  // ring free: reuse as logits / expf buffers
+
+  float* lg = reinterpret_cast<float*>(sm);
+  const int lp = E + 1;
+  float* ex = lg + (size_t)C.rb * lp;
 #pragma unroll
-  for (int j = 0; j < EPG; ++j)
-    if (e0 + j < E && rr < nrow) lg[rr * L.lp + e0 + j] = __fadd_rn(acc[j], h2f(gb[e0 + j]));
+  for (int i = 0; i < RPT; ++i) {
+    const int r = rt + i * C.rt;
+#pragma unroll
+    for (int j = 0; j < EPG; ++j)
+      if (e0 + j < E && r < nrow) lg[r * lp + e0 + j] = __fadd_rn(acc[i][j], h2f(gb[e0 + j]));
+  }
   __syncthreads();
 
   // ---- top-k selection (routing.cpp:15-31): one warp per row, shuffles
-  for (int r = warp; r < nrow; r += 8) {
-    const float* l = lg + r * L.lp;
-    bool fin_ok = true;
-    for (int j = lane; j < E; j += 32) fin_ok &= isfinite(l[j]);
-    fin_ok = __all_sync(0xffffffffu, fin_ok);
-    if (!fin_ok) {
+  for (int r = warp; r < nrow; r += gk::kThreads / 32) {
+    const float* l = lg + r * lp;
+    bool ok = true;
+    for (int j = lane; j < E; j += 32) ok &= isfinite(l[j]);
+    ok = __all_sync(0xffffffffu, ok);
+    if (!ok) {
       if (lane == 0) {
         atomicMin(bad_row, (uint32_t)(r0 + r));
-        for (int s = 0; s < k; ++s) sel[r * 8 + s] = 0xFFFFFFFFu;
+        sel[r * 8] = 0xFFFFFFFFu;
       }
       continue;
     }
@@ -234,7 +262,7 @@ __global__ void __launch_bounds__(gf::kThreads) gate_fused_kernel(
         bool taken = false;
         for (int q = 0; q < s; ++q) taken |= sel[r * 8 + q] == (uint32_t)j;
         const float v = l[j];
-        if (!taken && (v > bv || bj == 0x7FFFFFFF)) {  // lane-local: first max (j ascends)
+        if (!taken && (v > bv || bj == 0x7FFFFFFF)) {  // lane-local first maximum
           bv = v;
           bj = j;
         }
@@ -254,16 +282,15 @@ __global__ void __launch_bounds__(gf::kThreads) gate_fused_kernel(
   }
   __syncthreads();
   // expf(l_j - mx) for every (row, expert) in parallel (routing.cpp:34)
-  float* ex = lg + ROWS * L.lp;
-  for (int i = tid; i < nrow * E; i += gf::kThreads) {
+  for (int i = tid; i < nrow * E; i += gk::kThreads) {
     const int r = i / E, j = i % E;
     const uint32_t s0 = sel[r * 8];
     if (s0 == 0xFFFFFFFFu) continue;
-    const float* l = lg + r * L.lp;
-    ex[r * L.lp + j] = moe_glibc_expf(__fsub_rn(l[j], l[s0]));
+    const float* l = lg + r * lp;
+    ex[r * lp + j] = moe_glibc_expf(__fsub_rn(l[j], l[s0]));
   }
   __syncthreads();
-  // serial Σ and scales, one thread per row (routing.cpp:33-38)
+  // serial sum in expert order, scales, routing keys (routing.cpp:33-38, 55-62)
   if (tid < nrow) {
     const int r = tid;
     const int64_t row = r0 + r;
@@ -275,9 +302,9 @@ __global__ void __launch_bounds__(gf::kThreads) gate_fused_kernel(
         atomicAdd(&hist[fin ? E : 0], 1u);
       }
     } else {
-      const float* exr = ex + r * L.lp;
+      const float* exr = ex + r * lp;
       float sum = 0.f;
-      for (int j = 0; j < E; ++j) sum = __fadd_rn(sum, exr[j]);  // expert order
+      for (int j = 0; j < E; ++j) sum = __fadd_rn(sum, exr[j]);
       for (int s = 0; s < k; ++s) {
         const uint32_t e = sel[r * 8 + s];
         const float num = s == 0 ? 1.0f : exr[e];
@@ -288,9 +315,10 @@ __global__ void __launch_bounds__(gf::kThreads) gate_fused_kernel(
     }
   }
   __syncthreads();
-  for (int i = tid; i <= E; i += gf::kThreads) blockcnt[(int64_t)i * gridDim.x + blockIdx.x] = hist[i];
+  for (int i = tid; i <= E; i += gk::kThreads) blockcnt[(int64_t)i * gridDim.x + blockIdx.x] = hist[i];
 }
 
+// ================================================================= launchers
 __global__ void widen_gate_kernel(const uint16_t* __restrict__ gw, int64_t d, int64_t E,
                                   int64_t gwp, float* __restrict__ out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -307,59 +335,79 @@ int launch_widen_gate(const uint16_t* gw, int64_t d, int64_t E, int64_t gwp, flo
   return check_launch("widen_gate");
 }
 
-int gate_fused_rows(int64_t T) {
-  if (T >= 32 * 148) return 32;
-  if (T >= 16 * 148) return 16;
-  return 8;
-}
+int64_t gate_fused_pitch(int64_t E) { return (E + 3) / 4 * 4; }
 
-template <int ROWS, int EPG>
-static int launch_gf(const GateFusedArgs& a, cudaStream_t st) {
-  const gf::Smem L = gf::layout(ROWS, (int)a.d, (int)a.E, (int)a.gwp);
-  static size_t attr = 0;
-  if (L.total > 48 * 1024 && L.total > attr) {
-    MOE_CUDA_TRY(cudaFuncSetAttribute(gate_fused_kernel<ROWS, EPG>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
-    attr = L.total;
+// (EPG, RPT): most chains per thread that still gives >= 2 CTAs per SM
+static void pick(int64_t T, int64_t E, int k, int* epg, int* rpt) {
+  static const int kEpg[] = {8, 8, 4, 2, 1};
+  static const int kRpt[] = {2, 1, 1, 1, 1};
+  for (int i = 0; i < 5; ++i) {
+    const gk::Cfg c = gk::cfg((int)E, (int)gate_fused_pitch(E), kEpg[i], kRpt[i]);
+    const bool slots_ok = (int64_t)c.rb * k <= 256;  // plan_place block limit
+    if (slots_ok && ((T + c.rb - 1) / c.rb >= 2 * 148 || i == 4)) {
+      *epg = kEpg[i];
+      *rpt = kRpt[i];
+      return;
+    }
   }
-  const unsigned grid = (unsigned)((a.T + ROWS - 1) / ROWS);
-  gate_fused_kernel<ROWS, EPG><<<grid, gf::kThreads, L.total, st>>>(
-      a.x, a.T, (int)a.d, a.g, a.b, a.gw32, (int)a.gwp, a.gb, (int)a.E, a.k, a.finished, a.xn,
-      a.expert, a.scale, a.blockcnt, a.bad_row);
-  note_launch();
-  return check_launch("gate_fused");
+  *epg = 1;
+  *rpt = 1;
 }
 
-template <int ROWS>
-static int launch_gf_rows(const GateFusedArgs& a, cudaStream_t st) {
-  constexpr int NG = 8 * (32 / ROWS);
-  const int64_t need = (a.E + NG - 1) / NG;
-  if (need <= 1) return launch_gf<ROWS, 1>(a, st);
-  if (need <= 2) return launch_gf<ROWS, 2>(a, st);
-  if (need <= 4) return launch_gf<ROWS, 4>(a, st);
-  if (need <= 8) return launch_gf<ROWS, 8>(a, st);
-  return launch_gf<ROWS, 16>(a, st);
-}
-
-int64_t gate_fused_pitch(int64_t E) {
-  // covers every expert group's float4 reads at every ROWS (see layout)
-  return (E + 3) / 4 * 4;
+int gate_fused_rows(int64_t T, int64_t E, int k) {
+  int epg, rpt;
+  pick(T, E, k, &epg, &rpt);
+  return gk::cfg((int)E, (int)gate_fused_pitch(E), epg, rpt).rb;
 }
 
 bool gate_fused_supported(int64_t d, int64_t E, int k) {
-  if (d % 8 != 0 || k < 1 || k > 8 || E < 1) return false;
-  if (E > 128) return false;  // EPG <= 16 at ROWS = 32 (8 expert groups)
-  const gf::Smem L = gf::layout(32, (int)d, (int)E, (int)gate_fused_pitch(E));
-  return L.total <= 220 * 1024;
+  if (d % 8 != 0 || k < 1 || k > 8 || E < 1 || E > 256) return false;
+  if ((size_t)lnr::ROWS * (d + 8) * 2 + 256 > 200 * 1024) return false;
+  // slots of one gate block must fit a plan_place block (<= 256)
+  const gk::Cfg c = gk::cfg((int)E, (int)gate_fused_pitch(E), 1, 1);
+  return (int64_t)c.rb * k <= 256 && c.total <= 200 * 1024;
+}
+
+template <int EPG, int RPT>
+static int launch_gk(const GateFusedArgs& a, cudaStream_t st) {
+  const gk::Cfg C = gk::cfg((int)a.E, (int)a.gwp, EPG, RPT);
+  static size_t attr = 0;
+  if (C.total > 48 * 1024 && C.total > attr) {
+    MOE_CUDA_TRY(cudaFuncSetAttribute(gate_topk_kernel<EPG, RPT>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C.total));
+    attr = C.total;
+  }
+  const unsigned grid = (unsigned)((a.T + C.rb - 1) / C.rb);
+  gate_topk_kernel<EPG, RPT><<<grid, gk::kThreads, C.total, st>>>(
+      a.xn, a.T, (int)a.d, a.gw32, (int)a.gwp, a.gb, (int)a.E, a.k, a.finished, a.expert,
+      a.scale, a.blockcnt, a.bad_row);
+  note_launch();
+  return check_launch("gate_topk");
 }
 
 int launch_gate_fused(const GateFusedArgs& a, cudaStream_t st) {
   if (a.T == 0) return MOE_OK;
-  switch (a.rows) {
-    case 32: return launch_gf_rows<32>(a, st);
-    case 16: return launch_gf_rows<16>(a, st);
-    default: return launch_gf_rows<8>(a, st);
+  // 1. LayerNorm rows
+  const size_t smem = (size_t)lnr::ROWS * (a.d + 8) * 2 + 2 * lnr::ROWS * 4 + 16;
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    MOE_CUDA_TRY(cudaFuncSetAttribute(ln_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+    attr = smem;
   }
+  ln_rows_kernel<<<(unsigned)((a.T + lnr::ROWS - 1) / lnr::ROWS), lnr::kThreads, smem, st>>>(
+      a.x, a.T, (int)a.d, a.g, a.b, a.xn);
+  note_launch();
+  const int s1 = check_launch("ln_rows");
+  if (s1 != MOE_OK) return s1;
+  // 2. logits + top-k + key histogram
+  int epg, rpt;
+  pick(a.T, a.E, a.k, &epg, &rpt);
+  if (epg == 8 && rpt == 2) return launch_gk<8, 2>(a, st);
+  if (epg == 8) return launch_gk<8, 1>(a, st);
+  if (epg == 4) return launch_gk<4, 1>(a, st);
+  if (epg == 2) return launch_gk<2, 1>(a, st);
+  return launch_gk<1, 1>(a, st);
 }
 
 }  // namespace moecu

@@ -5,16 +5,19 @@
 //
 //   D[feature, token] = sum_k  Wq[k, feature] * X[token, k]
 //
-// * MMA M = 128 output features of one expert, N = BN tokens (up to 256),
+// * MMA M = 128 output features of one expert, N = BN tokens (up to 224),
 //   K = 16 per instruction, kind::f16 with f32 accumulation in TMEM
-//   (double-buffered: 2 x BN columns), both operands in shared memory
-//   (128-byte swizzle, K-major): A = the dequantised weight tile, B = the
-//   activation tile (TMA).
-// * Dequant warps (one per 32-feature slice, two groups alternating
-//   k-blocks) turn each feature's 64 codes -- bulk-copied into shared memory
-//   packed -- into fp16 with the magic I2F trick
+//   (double-buffered: 2 x BN columns).  A = the dequantised weight tile lives
+//   in TENSOR MEMORY (2 stages x 32 columns; "TS" MMA), B = the activation
+//   tile in shared memory (TMA, 128-byte swizzle, K-major).  Keeping A out of
+//   shared memory removes the A-tile stores and the MMA's A reads from the
+//   shared-memory pipe, which ncu showed ~80% busy in the SS form.
+// * Dequant warps (one per 32-feature TMEM lane quarter, two groups
+//   alternating k-blocks) turn each feature's 64 codes -- bulk-copied into
+//   shared memory packed -- into fp16 with the magic I2F trick
 //   (proj/include/moeinfer/dequant.hpp:39-63; 9 ops per 8 int4 codes) and
-//   store them swizzled as the A tile.  The per-channel scale is applied to
+//   write them to TMEM with one tcgen05.st.32x32b.x32 per thread.  The
+//   per-channel scale is applied to
 //   the f32 accumulator in the epilogue instead of to each weight (the
 //   reference rounds q*s to fp16 first; both stay inside the tolerance,
 //   DESIGN.md §4).
@@ -53,26 +56,23 @@ template <int BITS, int BN>
 struct Cfg {
   static constexpr int WBYTES = wblock_bytes(BITS);
   static constexpr int BBYTES = BN * 128;   // BN rows x 64 fp16
-  static constexpr int ABYTES = 128 * 128;  // 128 features x 64 fp16
   static constexpr int STAGE = BBYTES + WBYTES;
   static constexpr int EPI_WBUF = 32 * 32 * 2;                   // per warp: [32][32] fp16
   static constexpr int EPI = kEpiGroups * 4 * EPI_WBUF;
-  static constexpr int BUDGET = 220 * 1024 - EPI;                // stages + A ring
-  static constexpr int NA = 2;                                   // A stages
-  static constexpr int NS0 = (BUDGET - NA * ABYTES) / STAGE;
+  static constexpr int BUDGET = 220 * 1024 - EPI;                // TMA stages
+  static constexpr int NA = 2;                                   // A stages (TMEM, 32 cols each)
+  static constexpr int NS0 = BUDGET / STAGE;
   static constexpr int NS = NS0 > 8 ? 8 : NS0;                   // TMA stages
-  // [TMA stages][B | W] | [A stages] | epilogue staging | barriers | table
-  static constexpr int OFF_A = NS * STAGE;
-  static constexpr int OFF_EPI = OFF_A + NA * ABYTES;
+  // [TMA stages][B | W] | epilogue staging | barriers | table
+  static constexpr int OFF_EPI = NS * STAGE;
   static constexpr int OFF_BAR = OFF_EPI + EPI;
   static constexpr int NBAR = 2 * NS + 2 * NA + 4;
   static constexpr int OFF_TMEMPTR = OFF_BAR + NBAR * 8;
   static constexpr int OFF_TABLE = OFF_TMEMPTR + 16;
   static constexpr int SMEM = OFF_TABLE + (kMaxProblems + 1) * 4 + 1024;  // + align slack
-  static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128
-                                 : 2 * BN <= 256 ? 256 : 512;
+  static constexpr int A_COL = 2 * BN;                           // TMEM: acc0 | acc1 | A ring
   static_assert(NS >= 2, "pipeline too shallow");
-  static_assert(2 * BN <= 512, "TMEM overflow");
+  static_assert(2 * BN + NA * 32 <= 512, "TMEM overflow");
   static_assert(BBYTES % 1024 == 0 && WBYTES % 1024 == 0, "stage alignment");
   static_assert(SMEM <= 227 * 1024, "shared memory");
 };
@@ -229,10 +229,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_after();
           TC_TRACE(2, it);
           const uint64_t bdesc = umma_desc_sw128(smem_base + s * C::STAGE);
-          const uint64_t adesc = umma_desc_sw128(smem_base + C::OFF_A + a * C::ABYTES);
+          const uint32_t a_tmem = tmem + C::A_COL + a * 32;
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk)  // K advance of 16 fp16 = 32 bytes = 2 descriptor units
-            tc_mma_ss(d_tmem, adesc + (uint64_t)(kk * 2), bdesc + (uint64_t)(kk * 2), idesc,
+          for (int kk = 0; kk < 4; ++kk)  // K advance of 16: B 32 bytes (2 desc units), A 8 TMEM columns
+            tc_mma_ts(d_tmem, a_tmem + kk * 8, bdesc + (uint64_t)(kk * 2), idesc,
                       (kb | kk) != 0 ? 1u : 0u);
           tc_commit(&empty[s]);
           tc_commit(&aempty[a]);
@@ -285,17 +285,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             v[c8 * 4 + 3] = c.w;
           }
         }
-        // A tile row `feat`: 128 bytes, 16-byte chunk c (k = 8c..8c+7) stored at
-        // chunk position c ^ (feat & 7) -- the 128B-swizzle K-major atom layout
-        // (conflict-free: a quarter warp covers 8 rows x distinct chunk slots).
-        if (!(P.dbg & 2)) {
-          uint8_t* arow = smem + C::OFF_A + a * C::ABYTES + feat * 128;
-#pragma unroll
-          for (int c = 0; c < 8; ++c)
-            *reinterpret_cast<uint4*>(arow + ((c ^ (feat & 7)) << 4)) =
-                make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
-        }
-        fence_proxy_async_smem();  // generic-proxy stores -> visible to tcgen05.mma
+        // A row `feat` = TMEM lane feat: 64 fp16 = 32 columns (k pairs), one
+        // 32x32b.x32 store per thread into this warp's lane quarter
+        if (!(P.dbg & 2))
+          tmem_st_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + C::A_COL + a * 32, v);
+        tc_wait_st();
+        tc_fence_before();  // TMEM stores -> ordered before the mbarrier arrive
         __syncwarp();
         if (lane == 0) mbar_arrive(&afull[a]);
         if (lane == 0 && q == 0) TC_TRACE(5, it);
@@ -477,7 +472,7 @@ template <int BITS>
 static int run_tc_bits(const GemmArgs& a, cudaStream_t st) {
   // token-tile width from the expected rows per problem (wider MMAs amortise
   // the per-instruction issue cost; narrower ones waste less on small experts)
-  if (a.rows_hint >= 160) return run_tc<BITS, 256>(a, st);
+  if (a.rows_hint >= 160) return run_tc<BITS, 224>(a, st);
   if (a.rows_hint >= 96) return run_tc<BITS, 128>(a, st);
   if (a.rows_hint >= 40) return run_tc<BITS, 64>(a, st);
   return run_tc<BITS, 32>(a, st);

@@ -109,7 +109,7 @@ struct Params {
 };
 
 template <int BITS>
-__global__ void __launch_bounds__(kThreads) gemv_kernel(const Params P) {
+__global__ void __launch_bounds__(kThreads, 2) gemv_kernel(const Params P) {
   using F = Frag<BITS>;
   constexpr int WBYTES = wblock_bytes(BITS);
   extern __shared__ __align__(16) uint16_t xs[];  // [NT][kp]
@@ -140,10 +140,19 @@ __global__ void __launch_bounds__(kThreads) gemv_kernel(const Params P) {
     }
   }
 
+  using W = uint32_t[F::U][F::NW];
+  auto load_group = [&](int kb, W& w) {
+#pragma unroll
+    for (int u = 0; u < F::U; ++u)
+      if (kb + u < kb1) load_frag<BITS>(wbase + (int64_t)(kb + u) * WBYTES, fg, t, w[u]);
+  };
   for (int64_t rb = r0; rb < r1; rb += NT) {
     const int nrow = (int)(r1 - rb < (int64_t)NT ? r1 - rb : (int64_t)NT);
+    uint32_t wa[F::U][F::NW], wb[F::U][F::NW];
+    __syncthreads();  // previous pass done with xs
+    // first weight group in flight before waiting for the activations
+    load_group(kb0, wa);
     // stage x[rb .. rb+nrow)[k range] (zero-filled past m / past nrow)
-    __syncthreads();
     const int kq = kspan / 8;
     for (int i = threadIdx.x; i < NT * kq; i += kThreads) {
       const int r = i / kq, c = i % kq;
@@ -155,19 +164,17 @@ __global__ void __launch_bounds__(kThreads) gemv_kernel(const Params P) {
     cp_async_wait<0>();
     __syncthreads();
 
-    float acc[2][4];
+    // two independent accumulator chains per n-tile (even / odd MMA of a
+    // k-block) halve the dependent mma.sync latency chain
+    float acc[2][2][4];
 #pragma unroll
     for (int j = 0; j < 2; ++j)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) acc[j][q] = 0.f;
-
-    uint32_t wa[F::U][F::NW], wb[F::U][F::NW];
-    auto load_group = [&](int kb, uint32_t(&w)[F::U][F::NW]) {
+      for (int c = 0; c < 2; ++c)
 #pragma unroll
-      for (int u = 0; u < F::U; ++u)
-        if (kb + u < kb1) load_frag<BITS>(wbase + (int64_t)(kb + u) * WBYTES, fg, t, w[u]);
-    };
-    auto compute_group = [&](int kb, const uint32_t(&w)[F::U][F::NW]) {
+        for (int q = 0; q < 4; ++q) acc[j][c][q] = 0.f;
+
+    auto compute_group = [&](int kb, const W& w) {
 #pragma unroll
       for (int u = 0; u < F::U; ++u) {
         if (kb + u >= kb1) break;
@@ -183,12 +190,11 @@ __global__ void __launch_bounds__(kThreads) gemv_kernel(const Params P) {
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const uint32_t a[4] = {lo[2 * i], hi[2 * i], lo[2 * i + 1], hi[2 * i + 1]};
-            mma_16816(acc[j], a, xv[2 * i], xv[2 * i + 1]);
+            mma_16816(acc[j][i & 1], a, xv[2 * i], xv[2 * i + 1]);
           }
         }
       }
     };
-    load_group(kb0, wa);
     for (int kb = kb0; kb < kb1; kb += 2 * F::U) {
       load_group(kb + F::U, wb);
       compute_group(kb, wa);
@@ -196,6 +202,10 @@ __global__ void __launch_bounds__(kThreads) gemv_kernel(const Params P) {
       load_group(kb + 2 * F::U, wa);
       compute_group(kb + F::U, wb);
     }
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[j][0][q] += acc[j][1][q];
 
     // D fragment: acc[j][0..1] -> feature g, tokens 8j+2t, +1; [2..3] -> feature g+8
     if (P.nsplit == 1) {
@@ -206,7 +216,7 @@ __global__ void __launch_bounds__(kThreads) gemv_kernel(const Params P) {
           const int tok = j * 8 + 2 * t + (q & 1), h = q >> 1;
           const int64_t f = feat0 + g + 8 * h;
           if (tok < nrow && f < P.n) {
-            float v = fmaf(acc[j][q], sc[h], bi[h]);
+            float v = fmaf(acc[j][0][q], sc[h], bi[h]);
             if (P.relu) v = v > 0.f ? v : 0.f;
             P.out[(rb + tok) * P.n + f] = f2h(v);
           }
@@ -218,7 +228,7 @@ __global__ void __launch_bounds__(kThreads) gemv_kernel(const Params P) {
         for (int q = 0; q < 4; ++q) {
           const int tok = j * 8 + 2 * t + (q & 1), h = q >> 1;
           const int64_t f = feat0 + g + 8 * h;
-          if (tok < nrow && f < P.n) P.part[((int64_t)split * P.rows + rb + tok) * P.n + f] = acc[j][q];
+          if (tok < nrow && f < P.n) P.part[((int64_t)split * P.rows + rb + tok) * P.n + f] = acc[j][0][q];
         }
     }
   }

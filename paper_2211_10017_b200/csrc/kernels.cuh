@@ -56,9 +56,9 @@ struct GateFusedArgs {
   uint16_t* scale;
   uint32_t* blockcnt;  // ceil(T/rows) * (E+1)
   uint32_t* bad_row;
-  int rows;            // gate_fused_rows(T)
+  int rows;            // gate_fused_rows(T, E, k)
 };
-int gate_fused_rows(int64_t T);
+int gate_fused_rows(int64_t T, int64_t E, int k);  // rows per gate block (plan block = rows*k slots)
 bool gate_fused_supported(int64_t d, int64_t E, int k);
 int launch_gate_fused(const GateFusedArgs& a, cudaStream_t st);
 int launch_widen_gate(const uint16_t* gw, int64_t d, int64_t E, int64_t gwp, float* out,

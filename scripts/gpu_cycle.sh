@@ -1,0 +1,6 @@
+# tests + bench at every workload + launch lists
+set -x
+timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -8
+python bench.py --steps 200 --warmup 10 2>&1 | tail -1
+for w in c1i4 c3_1 c3_8 c3_64 c4; do python bench.py --workload $w --steps 100 --warmup 5 --no-cpu-baseline 2>&1 | tail -1; done
+for w in c2 c3_64 c4; do timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$w.csv python bench.py --workload $w --steps 3 --warmup 3 --no-cpu-baseline > /dev/null 2>&1; done

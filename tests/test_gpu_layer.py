@@ -147,7 +147,7 @@ def test_layer_decode_shapes(cuda, oracle, T):
 
 
 @pytest.mark.parametrize("E,d,T,k", [(8, 512, 4096, 2), (64, 1024, 600, 1), (128, 256, 300, 2),
-                                     (3, 40, 50, 3), (130, 64, 20, 1)])
+                                     (3, 40, 50, 3), (130, 64, 20, 1), (300, 32, 40, 2)])
 def test_layer_fused_gate_routing_exact(cuda, oracle, E, d, T, k):
     """Fused LN+logits+top-k+histogram kernel (and the unfused fallback for
     E > 128): routing identical to the oracle at BASELINE-like shapes."""
