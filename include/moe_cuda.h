@@ -205,6 +205,9 @@ int moe_layer_forward_host(moe_layer* L, const uint16_t* x_host,
 int moe_layer_route(moe_layer* L, const uint16_t* x, const uint8_t* finished, int64_t T, int k,
                     moe_stream_t stream);
 int moe_layer_buffers(moe_layer* L, const uint16_t** xp, uint16_t** y);
+/* Re-run only FFN1 + FFN2 over the last forward's routed rows (kernel timing:
+ * bench.py captures back-to-back calls in a graph between two events). */
+int moe_layer_ffn(moe_layer* L, int mode, moe_stream_t stream);
 int moe_layer_experts(moe_layer* L, const uint16_t* xin, int64_t rows, const uint32_t* problems,
                       int64_t np, int mode, uint16_t* out, moe_stream_t stream);
 int moe_layer_combine(moe_layer* L, const uint16_t* x, const uint16_t* y,

@@ -61,6 +61,7 @@ _SIGS = {
     "moe_ep_rank_counts": (_int, [_vp, _i64, _int, _vp, _vp]),
     "moe_layer_route": (_int, [_vp, _vp, _vp, _i64, _int, _vp]),
     "moe_layer_buffers": (_int, [_vp, _vp, _vp]),
+    "moe_layer_ffn": (_int, [_vp, _int, _vp]),
     "moe_layer_experts": (_int, [_vp, _vp, _i64, _vp, _i64, _int, _vp, _vp]),
     "moe_layer_combine": (_int, [_vp, _vp, _vp, _vp, _i64, _int, _vp, _vp]),
 }

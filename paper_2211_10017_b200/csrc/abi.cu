@@ -714,6 +714,15 @@ int moe_layer_route(moe_layer* L, const uint16_t* x, const uint8_t* finished, in
   return layer_route(L, x, finished, T, k, S(stream), mark);
 }
 
+int moe_layer_ffn(moe_layer* L, int mode, moe_stream_t stream) {
+  if (!L) return set_error(MOE_EINVAL, "layer: null");
+  if (L->last_T <= 0) return set_error(MOE_EINVAL, "moe_ffn: no routed forward yet");
+  if (L->El != L->E) return set_error(MOE_EINVAL, "moe_ffn: expert slice (use moe_layer_experts)");
+  Marks mark(L, S(stream), false);
+  return layer_ffn(L, L->xp, L->last_T * L->last_k, L->problems, L->E, mode, L->h, L->y,
+                   S(stream), mark);
+}
+
 int moe_layer_buffers(moe_layer* L, const uint16_t** xp, uint16_t** y) {
   if (!L) return set_error(MOE_EINVAL, "layer: null");
   if (xp) *xp = L->xp;

@@ -4,7 +4,7 @@
 //   per-block routing-key histogram (routing.cpp:55-62, first counting-sort
 //   pass), as two kernels:
 //
-// ln_rows_kernel -- 16 token rows per CTA arrive by bulk copy (TMA engine);
+// ln_rows_kernel -- 32 token rows per CTA arrive by bulk copy (TMA engine);
 //   one lane per row runs the reference's two serial f32 chains (sum, then
 //   centred sum of squares, every op RN32, no contraction); all threads then
 //   normalise and write xn.  The chains are the latency floor of the whole
@@ -28,7 +28,7 @@ namespace moecu {
 
 // =================================================================== LN rows
 namespace lnr {
-constexpr int ROWS = 16;
+constexpr int ROWS = 32;  // one full warp of row chains
 constexpr int kThreads = 128;
 }  // namespace lnr
 
@@ -109,8 +109,9 @@ struct Cfg {
   int rt;       // row-threads = kThreads / ng
   int rb;       // rows per CTA = rt * rpt
   int kc;       // inputs per pipeline chunk
-  int xpitch;   // xn chunk row pitch (halves)
-  size_t xbytes, wbytes, stage, body, total;
+  int xpitch;   // fp16 xn chunk row pitch (halves)
+  int fpitch;   // f32 xn chunk row pitch (floats)
+  size_t xbytes, wbytes, stage, off_xf, body, total;
 };
 
 __host__ __device__ inline int pow2_at_least(int v) {
@@ -128,14 +129,26 @@ __host__ __device__ inline Cfg cfg(int E, int gwp, int epg, int rpt) {
   int kc = (int)(16384 / ((size_t)gwp * 4)) / 8 * 8;
   c.kc = kc < 16 ? 16 : (kc > 64 ? 64 : kc);
   c.xpitch = c.kc + 8;
+  c.fpitch = c.kc + 4;  // 16-byte rows, consecutive row-threads on distinct banks
   c.xbytes = (size_t)c.rb * c.xpitch * 2;
   c.wbytes = (size_t)c.kc * gwp * 4 + 64;  // + over-read slack of the last expert group
   c.stage = (c.xbytes + c.wbytes + 15) & ~size_t(15);
-  const size_t pipe = NS * c.stage;
+  c.off_xf = NS * c.stage;  // f32 copy of the current xn chunk
+  const size_t pipe = c.off_xf + (size_t)c.rb * c.fpitch * 4;
   const size_t lg = (size_t)2 * c.rb * (E + 1) * 4;  // logits + expf values (reuse the ring)
   c.body = ((pipe > lg ? pipe : lg) + 15) & ~size_t(15);
   c.total = c.body + (size_t)c.rb * 8 * 4 + (size_t)(E + 1) * 4 + 16;  // + sel[8], hist
   return c;
+}
+
+// two independent f32 FMAs in one instruction (FFMA2, sm_100): c += a * b, each lane RN
+__device__ __forceinline__ float2 ffma2(float a, float2 b, float2 c) {
+  uint64_t r;
+  const uint64_t bb = (uint64_t)__float_as_uint(b.x) | ((uint64_t)__float_as_uint(b.y) << 32);
+  const uint64_t cc = (uint64_t)__float_as_uint(c.x) | ((uint64_t)__float_as_uint(c.y) << 32);
+  const uint64_t aa = (uint64_t)__float_as_uint(a) | ((uint64_t)__float_as_uint(a) << 32);
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(aa), "l"(bb), "l"(cc));
+  return make_float2(__uint_as_float((uint32_t)r), __uint_as_float((uint32_t)(r >> 32)));
 }
 }  // namespace gk
 
@@ -180,48 +193,68 @@ __global__ void __launch_bounds__(gk::kThreads) gate_topk_kernel(
   };
   for (int c = 0; c < gk::NS - 1; ++c) issue(c);
 
-  float acc[RPT][EPG];
+  // chains: RPT rows x EPG experts; EPG >= 2 as float2 pairs (FFMA2)
+  constexpr int NP = EPG >= 2 ? EPG / 2 : 1;
+  float2 acc[RPT][NP];
 #pragma unroll
   for (int i = 0; i < RPT; ++i)
 #pragma unroll
-    for (int j = 0; j < EPG; ++j) acc[i][j] = 0.f;
+    for (int j = 0; j < NP; ++j) acc[i][j] = make_float2(0.f, 0.f);
+  float* xf = reinterpret_cast<float*>(sm + C.off_xf);
 
   for (int c = 0; c < nch; ++c) {
     cp_async_wait<gk::NS - 2>();
-    __syncthreads();
-    issue(c + gk::NS - 1);
+    __syncthreads();  // chunk c landed; previous chunk's f32 copy fully consumed
     const uint8_t* stg = sm + (size_t)(c % gk::NS) * C.stage;
     const uint16_t* xs = reinterpret_cast<const uint16_t*>(stg);
-    const float* ws = reinterpret_cast<const float*>(stg + C.xbytes) + e0;
-    const int kc = ::min(KC, d - c * KC);
+    const int kc = ::min(KC, d - c * KC), kq = kc / 8;
+    // widen the chunk once (fp16 -> f32 exactly), instead of per expert group
+    for (int i = tid; i < C.rb * kq; i += gk::kThreads) {
+      const int r = i / kq, q = i % kq;
+      const uint4 v = *reinterpret_cast<const uint4*>(xs + r * C.xpitch + q * 8);
+      const uint16_t* h = reinterpret_cast<const uint16_t*>(&v);
+      float4* dst = reinterpret_cast<float4*>(xf + r * C.fpitch + q * 8);
+      dst[0] = make_float4(h2f(h[0]), h2f(h[1]), h2f(h[2]), h2f(h[3]));
+      dst[1] = make_float4(h2f(h[4]), h2f(h[5]), h2f(h[6]), h2f(h[7]));
+    }
+    issue(c + gk::NS - 1);
+    __syncthreads();
+    const float* wp = reinterpret_cast<const float*>(stg + C.xbytes) + e0;
     if (e0 < E) {
-      for (int kk = 0; kk < kc; kk += 8) {
-        uint4 xv[RPT];
+      const float* xr = xf + rt * C.fpitch;
+      for (int kk = 0; kk < kc; kk += 4) {
+        float4 xv[RPT];
 #pragma unroll
         for (int i = 0; i < RPT; ++i)
-          xv[i] = *reinterpret_cast<const uint4*>(xs + (rt + i * C.rt) * C.xpitch + kk);
+          xv[i] = *reinterpret_cast<const float4*>(xr + i * C.rt * C.fpitch + kk);
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const float* wr = ws + (kk + q) * gwp;
-          float w[EPG];
-          if constexpr (EPG >= 4) {
+        for (int q = 0; q < 4; ++q) {
+          const float* wr = wp + (kk + q) * gwp;
+          if constexpr (EPG >= 2) {
+            float2 w[NP];
+            if constexpr (EPG >= 4) {
 #pragma unroll
-            for (int j = 0; j < EPG; j += 4) {
-              const float4 w4 = *reinterpret_cast<const float4*>(wr + j);
-              w[j] = w4.x;
-              w[j + 1] = w4.y;
-              w[j + 2] = w4.z;
-              w[j + 3] = w4.w;
+              for (int j = 0; j < NP; j += 2) {
+                const float4 w4 = *reinterpret_cast<const float4*>(wr + 2 * j);
+                w[j] = make_float2(w4.x, w4.y);
+                w[j + 1] = make_float2(w4.z, w4.w);
+              }
+            } else {
+              w[0] = *reinterpret_cast<const float2*>(wr);
+            }
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) {
+              const float xq = q == 0 ? xv[i].x : q == 1 ? xv[i].y : q == 2 ? xv[i].z : xv[i].w;
+#pragma unroll
+              for (int j = 0; j < NP; ++j) acc[i][j] = gk::ffma2(xq, w[j], acc[i][j]);  // exact products
             }
           } else {
+            const float w0 = wr[0];
 #pragma unroll
-            for (int j = 0; j < EPG; ++j) w[j] = wr[j];
-          }
-#pragma unroll
-          for (int i = 0; i < RPT; ++i) {
-            const float xf = h2f(reinterpret_cast<const uint16_t*>(&xv[i])[q]);
-#pragma unroll
-            for (int j = 0; j < EPG; ++j) acc[i][j] = fmaf(xf, w[j], acc[i][j]);  // exact product
+            for (int i = 0; i < RPT; ++i) {
+              const float xq = q == 0 ? xv[i].x : q == 1 ? xv[i].y : q == 2 ? xv[i].z : xv[i].w;
+              acc[i][0].x = fmaf(xq, w0, acc[i][0].x);
+            }
           }
         }
       }
@@ -237,8 +270,10 @@ __global__ void __launch_bounds__(gk::kThreads) gate_topk_kernel(
   for (int i = 0; i < RPT; ++i) {
     const int r = rt + i * C.rt;
 #pragma unroll
-    for (int j = 0; j < EPG; ++j)
-      if (e0 + j < E && r < nrow) lg[r * lp + e0 + j] = __fadd_rn(acc[i][j], h2f(gb[e0 + j]));
+    for (int j = 0; j < EPG; ++j) {
+      const float a = (j & 1) ? acc[i][j / 2].y : acc[i][j / 2].x;
+      if (e0 + j < E && r < nrow) lg[r * lp + e0 + j] = __fadd_rn(a, h2f(gb[e0 + j]));
+    }
   }
   __syncthreads();
 
@@ -337,16 +372,23 @@ int launch_widen_gate(const uint16_t* gw, int64_t d, int64_t E, int64_t gwp, flo
 
 int64_t gate_fused_pitch(int64_t E) { return (E + 3) / 4 * 4; }
 
-// (EPG, RPT): most chains per thread that still gives >= 2 CTAs per SM
+// (EPG, RPT): the most chains per thread (FFMA2 pairs, shared weight loads)
+// that still fills the machine; below that the gate is latency-bound and
+// 8 expert chains per thread beat many one-chain CTAs.
 static void pick(int64_t T, int64_t E, int k, int* epg, int* rpt) {
-  static const int kEpg[] = {8, 8, 4, 2, 1};
-  static const int kRpt[] = {2, 1, 1, 1, 1};
-  for (int i = 0; i < 5; ++i) {
-    const gk::Cfg c = gk::cfg((int)E, (int)gate_fused_pitch(E), kEpg[i], kRpt[i]);
-    const bool slots_ok = (int64_t)c.rb * k <= 256;  // plan_place block limit
-    if (slots_ok && ((T + c.rb - 1) / c.rb >= 2 * 148 || i == 4)) {
+  const int64_t gwp = gate_fused_pitch(E);
+  const gk::Cfg c82 = gk::cfg((int)E, (int)gwp, 8, 2);
+  if ((int64_t)c82.rb * k <= 1024 && (T + c82.rb - 1) / c82.rb >= 148) {
+    *epg = 8;
+    *rpt = 2;
+    return;
+  }
+  static const int kEpg[] = {8, 4, 2, 1};
+  for (int i = 0; i < 4; ++i) {
+    const gk::Cfg c = gk::cfg((int)E, (int)gwp, kEpg[i], 1);
+    if ((int64_t)c.rb * k <= 1024) {
       *epg = kEpg[i];
-      *rpt = kRpt[i];
+      *rpt = 1;
       return;
     }
   }
@@ -363,9 +405,9 @@ int gate_fused_rows(int64_t T, int64_t E, int k) {
 bool gate_fused_supported(int64_t d, int64_t E, int k) {
   if (d % 8 != 0 || k < 1 || k > 8 || E < 1 || E > 256) return false;
   if ((size_t)lnr::ROWS * (d + 8) * 2 + 256 > 200 * 1024) return false;
-  // slots of one gate block must fit a plan_place block (<= 256)
+  // slots of one gate block must fit a plan_place block (<= 1024 threads)
   const gk::Cfg c = gk::cfg((int)E, (int)gate_fused_pitch(E), 1, 1);
-  return (int64_t)c.rb * k <= 256 && c.total <= 200 * 1024;
+  return (int64_t)c.rb * k <= 1024 && c.total <= 200 * 1024;
 }
 
 template <int EPG, int RPT>

@@ -52,27 +52,32 @@ constexpr int kEpiGroups = 2;                           // epilogue warp groups
 constexpr int kThreads = 32 * (4 + 4 * kDqGroups + 4 * kEpiGroups);
 constexpr int kMaxProblems = 1024;
 
-template <int BITS, int BN>
+// TS = true: A (dequantised weights) in TMEM, 2 x BN accumulator columns
+// (BN <= 224).  TS = false: A in shared memory (SS MMA), which frees TMEM for
+// two 256-column accumulators -- chosen when 256-token tiles fit one wave.
+template <int BITS, int BN, bool TS>
 struct Cfg {
   static constexpr int WBYTES = wblock_bytes(BITS);
   static constexpr int BBYTES = BN * 128;   // BN rows x 64 fp16
+  static constexpr int ABYTES = TS ? 0 : 128 * 128;  // SS: 128 features x 64 fp16 per A stage
   static constexpr int STAGE = BBYTES + WBYTES;
   static constexpr int EPI_WBUF = 32 * 32 * 2;                   // per warp: [32][32] fp16
   static constexpr int EPI = kEpiGroups * 4 * EPI_WBUF;
-  static constexpr int BUDGET = 220 * 1024 - EPI;                // TMA stages
-  static constexpr int NA = 2;                                   // A stages (TMEM, 32 cols each)
+  static constexpr int NA = 2;                                   // A stages
+  static constexpr int BUDGET = 220 * 1024 - EPI - NA * ABYTES;  // TMA stages
   static constexpr int NS0 = BUDGET / STAGE;
   static constexpr int NS = NS0 > 8 ? 8 : NS0;                   // TMA stages
-  // [TMA stages][B | W] | epilogue staging | barriers | table
-  static constexpr int OFF_EPI = NS * STAGE;
+  // [TMA stages][B | W] | [SS: A stages] | epilogue staging | barriers | table
+  static constexpr int OFF_A = NS * STAGE;
+  static constexpr int OFF_EPI = OFF_A + NA * ABYTES;
   static constexpr int OFF_BAR = OFF_EPI + EPI;
   static constexpr int NBAR = 2 * NS + 2 * NA + 4;
   static constexpr int OFF_TMEMPTR = OFF_BAR + NBAR * 8;
   static constexpr int OFF_TABLE = OFF_TMEMPTR + 16;
   static constexpr int SMEM = OFF_TABLE + (kMaxProblems + 1) * 4 + 1024;  // + align slack
-  static constexpr int A_COL = 2 * BN;                           // TMEM: acc0 | acc1 | A ring
+  static constexpr int A_COL = 2 * BN;                           // TMEM: acc0 | acc1 | [TS: A ring]
   static_assert(NS >= 2, "pipeline too shallow");
-  static_assert(2 * BN + NA * 32 <= 512, "TMEM overflow");
+  static_assert(2 * BN + (TS ? NA * 32 : 0) <= 512, "TMEM overflow");
   static_assert(BBYTES % 1024 == 0 && WBYTES % 1024 == 0, "stage alignment");
   static_assert(SMEM <= 227 * 1024, "shared memory");
 };
@@ -126,11 +131,11 @@ constexpr int kTraceN = 1024;  // events per role slot
       P.trace[(slot) * kTraceN + (idx)] = clock64();                             \
   } while (0)
 
-template <int BITS, int BN>
+template <int BITS, int BN, bool TS>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ OutMaps O,
                    const Params P) {
-  using C = Cfg<BITS, BN>;
+  using C = Cfg<BITS, BN, TS>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte alignment for the 128B-swizzle atoms, by pointer arithmetic on
   // the shared array so the compiler keeps shared-space (LDS/STS) accesses.
@@ -213,11 +218,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---------------------------------------------------------- MMA issuer
     // The whole loop (waits included) runs on one thread: see header.
     if (lane == 0) {
-      constexpr uint32_t idesc = umma_idesc_f16(128, BN);
       const uint32_t smem_base = smem_u32(smem);
       uint32_t it = 0, local = 0;
       for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
         const int acc = local & 1;
+        // a problem's last token tile is usually partial: the MMA N follows
+        // the live rows (multiple of 16) so padding costs no tensor time
+        const Tile Tt = decode(table, np, P.problems, t, P.nft, BN);
+        const int64_t live = Tt.r1 - Tt.row0;
+        const int nmma = live >= BN ? BN : (int)((live + 15) / 16 * 16);
+        const uint32_t idesc = umma_idesc_f16(128, nmma);
         mbar_wait(&tempty[acc], ((local >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem + acc * BN;
@@ -229,11 +239,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_after();
           TC_TRACE(2, it);
           const uint64_t bdesc = umma_desc_sw128(smem_base + s * C::STAGE);
-          const uint32_t a_tmem = tmem + C::A_COL + a * 32;
+          if constexpr (TS) {
+            const uint32_t a_tmem = tmem + C::A_COL + a * 32;
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk)  // K advance of 16: B 32 bytes (2 desc units), A 8 TMEM columns
-            tc_mma_ts(d_tmem, a_tmem + kk * 8, bdesc + (uint64_t)(kk * 2), idesc,
-                      (kb | kk) != 0 ? 1u : 0u);
+            for (int kk = 0; kk < 4; ++kk)  // K advance of 16: B 32 bytes (2 desc units), A 8 TMEM cols
+              tc_mma_ts(d_tmem, a_tmem + kk * 8, bdesc + (uint64_t)(kk * 2), idesc,
+                        (kb | kk) != 0 ? 1u : 0u);
+          } else {
+            const uint64_t adesc = umma_desc_sw128(smem_base + C::OFF_A + a * C::ABYTES);
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)  // K advance of 16 fp16 = 32 bytes = 2 desc units
+              tc_mma_ss(d_tmem, adesc + (uint64_t)(kk * 2), bdesc + (uint64_t)(kk * 2), idesc,
+                        (kb | kk) != 0 ? 1u : 0u);
+          }
           tc_commit(&empty[s]);
           tc_commit(&aempty[a]);
           TC_TRACE(3, it);
@@ -285,12 +303,25 @@ __global__ void __launch_bounds__(kThreads, 1)
             v[c8 * 4 + 3] = c.w;
           }
         }
-        // A row `feat` = TMEM lane feat: 64 fp16 = 32 columns (k pairs), one
-        // 32x32b.x32 store per thread into this warp's lane quarter
-        if (!(P.dbg & 2))
-          tmem_st_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + C::A_COL + a * 32, v);
-        tc_wait_st();
-        tc_fence_before();  // TMEM stores -> ordered before the mbarrier arrive
+        if constexpr (TS) {
+          // A row `feat` = TMEM lane feat: 64 fp16 = 32 columns (k pairs), one
+          // 32x32b.x32 store per thread into this warp's lane quarter
+          if (!(P.dbg & 2))
+            tmem_st_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + C::A_COL + a * 32, v);
+          tc_wait_st();
+          tc_fence_before();  // TMEM stores -> ordered before the mbarrier arrive
+        } else {
+          // A tile row `feat`: 128 bytes, 16-byte chunk c (k = 8c..8c+7) stored at
+          // chunk position c ^ (feat & 7) -- the 128B-swizzle K-major atom layout
+          if (!(P.dbg & 2)) {
+            uint8_t* arow = smem + C::OFF_A + a * C::ABYTES + feat * 128;
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+              *reinterpret_cast<uint4*>(arow + ((c ^ (feat & 7)) << 4)) =
+                  make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+          }
+          fence_proxy_async_smem();  // generic-proxy stores -> visible to tcgen05.mma
+        }
         __syncwarp();
         if (lane == 0) mbar_arrive(&afull[a]);
         if (lane == 0 && q == 0) TC_TRACE(5, it);
@@ -394,9 +425,9 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-template <int BITS, int BN>
+template <int BITS, int BN, bool TS>
 static int run_tc(const GemmArgs& a, cudaStream_t st) {
-  using C = tc::Cfg<BITS, BN>;
+  using C = tc::Cfg<BITS, BN, TS>;
   auto encode = get_encode();
   if (!encode) return set_error(MOE_ECUDA, "cuTensorMapEncodeTiled unavailable");
   CUtensorMap tmap;
@@ -441,7 +472,7 @@ static int run_tc(const GemmArgs& a, cudaStream_t st) {
   }
   static bool attr_set = false;
   if (!attr_set) {
-    MOE_CUDA_TRY(cudaFuncSetAttribute(tc::gemm_tc_kernel<BITS, BN>,
+    MOE_CUDA_TRY(cudaFuncSetAttribute(tc::gemm_tc_kernel<BITS, BN, TS>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr_set = true;
   }
@@ -450,7 +481,7 @@ static int run_tc(const GemmArgs& a, cudaStream_t st) {
   P.dbg = std::getenv("MOE_TC_DBG") ? std::atoi(std::getenv("MOE_TC_DBG")) : 0;
   if (trace_path) MOE_CUDA_TRY(cudaMalloc(&P.trace, 12 * tc::kTraceN * 8));
   if (P.trace) MOE_CUDA_TRY(cudaMemset(P.trace, 0, 12 * tc::kTraceN * 8));
-  tc::gemm_tc_kernel<BITS, BN><<<sm_count(), tc::kThreads, C::SMEM, st>>>(tmap, O, P);
+  tc::gemm_tc_kernel<BITS, BN, TS><<<sm_count(), tc::kThreads, C::SMEM, st>>>(tmap, O, P);
   note_launch();
   const int rc = check_launch("gemm_tc");
   if (P.trace) {
@@ -471,11 +502,19 @@ static int run_tc(const GemmArgs& a, cudaStream_t st) {
 template <int BITS>
 static int run_tc_bits(const GemmArgs& a, cudaStream_t st) {
   // token-tile width from the expected rows per problem (wider MMAs amortise
-  // the per-instruction issue cost; narrower ones waste less on small experts)
-  if (a.rows_hint >= 160) return run_tc<BITS, 224>(a, st);
-  if (a.rows_hint >= 96) return run_tc<BITS, 128>(a, st);
-  if (a.rows_hint >= 40) return run_tc<BITS, 64>(a, st);
-  return run_tc<BITS, 32>(a, st);
+  // the per-instruction issue cost; narrower ones waste less on small
+  // experts).  256-token tiles (A in shared memory, double-buffered 256-col
+  // accumulators) when they fit one wave -- e.g. an FFN2 with few feature
+  // tiles -- else 224-token tiles with A in TMEM.
+  const int64_t nft = (a.n + 127) / 128;
+  if (a.rows_hint >= 160) {
+    const int64_t tiles256 = a.np * ((a.rows_hint + 255) / 256) * nft;
+    if (tiles256 <= sm_count()) return run_tc<BITS, 256, false>(a, st);
+    return run_tc<BITS, 224, true>(a, st);
+  }
+  if (a.rows_hint >= 96) return run_tc<BITS, 128, true>(a, st);
+  if (a.rows_hint >= 40) return run_tc<BITS, 64, true>(a, st);
+  return run_tc<BITS, 32, true>(a, st);
 }
 
 int launch_gemm_tc(const GemmArgs& a, cudaStream_t st) {

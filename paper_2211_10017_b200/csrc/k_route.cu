@@ -55,10 +55,20 @@ __global__ void __launch_bounds__(1024) plan_scan_kernel(
   __shared__ uint32_t warp_sum[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t keys = E + 1;
+  // loads are issued 8 per lane before any use (latency, not bandwidth, bound)
   for (int64_t key = warp; key < keys; key += 32) {
     const uint32_t* row = blockcnt + key * nblk;
     uint32_t s = 0;
-    for (int64_t b = lane; b < nblk; b += 32) s += row[b];
+    for (int64_t b0 = 0; b0 < nblk; b0 += 256) {
+      uint32_t v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int64_t b = b0 + j * 32 + lane;
+        v[j] = b < nblk ? row[b] : 0u;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) s += v[j];
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (lane == 0) tot[key] = s;
@@ -92,15 +102,29 @@ __global__ void __launch_bounds__(1024) plan_scan_kernel(
     const uint32_t* row = blockcnt + key * nblk;
     uint32_t* brow = blockbase + key * nblk;
     uint32_t carry = tot[key];
-    for (int64_t b0 = 0; b0 < nblk; b0 += 32) {
-      const int64_t b = b0 + lane;
-      const uint32_t c = b < nblk ? row[b] : 0u;
-      uint32_t in = c;
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t v = __shfl_up_sync(0xffffffffu, in, o);
-        if (lane >= o) in += v;
+    for (int64_t b0 = 0; b0 < nblk; b0 += 256) {  // lane owns 8 consecutive blocks
+      uint32_t v[8], pre[8], run = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int64_t b = b0 + lane * 8 + j;
+        v[j] = b < nblk ? row[b] : 0u;
       }
-      if (b < nblk) brow[b] = carry + in - c;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        pre[j] = run;
+        run += v[j];
+      }
+      uint32_t in = run;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, in, o);
+        if (lane >= o) in += u;
+      }
+      const uint32_t base = carry + in - run;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int64_t b = b0 + lane * 8 + j;
+        if (b < nblk) brow[b] = base + pre[j];
+      }
       carry += __shfl_sync(0xffffffffu, in, 31);
     }
   }
@@ -112,7 +136,7 @@ __global__ void __launch_bounds__(1024) plan_scan_kernel(
   if (tid == 0 && active != nullptr) *active = tot[E];
 }
 
-__global__ void __launch_bounds__(kPlanBlock) plan_place_kernel(int spb,
+__global__ void __launch_bounds__(1024) plan_place_kernel(int spb,
     const uint32_t* __restrict__ expert, const uint8_t* __restrict__ finished, int64_t S, int k,
     int64_t E, const uint32_t* __restrict__ blockbase, uint32_t* __restrict__ perm,
     uint32_t* __restrict__ inv, const uint16_t* __restrict__ src, int64_t cols,

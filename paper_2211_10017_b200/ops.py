@@ -285,6 +285,10 @@ class MoELayer:
                  x.shape[0], k, _p(out), _stream(stream))
         return out
 
+    def ffn(self, mode=MODE_FAST, stream=None):
+        """Re-run FFN1 + FFN2 on the last forward's routed rows (moe_layer_ffn)."""
+        abi.call("moe_layer_ffn", self._h, mode, _stream(stream))
+
     def offsets_device(self):
         """(E+1) int32 device view of the last plan's expert offsets."""
         ptrs = [C.c_void_p() for _ in range(6)]
