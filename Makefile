@@ -13,7 +13,7 @@ PY       ?= python
 PKG      := paper_2211_10017_b200
 CSRC     := $(PKG)/csrc
 ARCH     := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS  := -std=c++17 -O3 $(ARCH) -lineinfo -Xcompiler -fPIC -Xcompiler -ffp-contract=off \
+NVFLAGS  := -std=c++17 -O3 $(ARCH) -lineinfo --fmad=false -Xcompiler -fPIC -Xcompiler -ffp-contract=off \
             -I$(CSRC) -Iinclude --expt-relaxed-constexpr
 CUDA_INC := /usr/local/cuda/include
 PYINC    := $(shell $(PY) -c "import sysconfig;print(sysconfig.get_paths()['include'])")

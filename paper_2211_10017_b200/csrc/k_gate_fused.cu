@@ -22,28 +22,40 @@
 //   expert order, gate scales, and a shared-memory histogram of routing keys
 //   (finished ? E : expert) written key-major as blockcnt[key][block] for
 //   plan_scan (k_route.cu), whose blocks are this kernel's RB*k slots.
+#include <cstdio>
+#include <cstdlib>
+
 #include "kernels.cuh"
 
 namespace moecu {
 
 // =================================================================== LN rows
+// The two serial chains run one lane per row over an f32 copy of the rows
+// that all 128 threads widen first (the chain lane then issues one FADD per
+// element in pass 1 and FADD2/FMUL2 pairs + one chained FADD per element in
+// pass 2 -- latency-bound, not issue-bound); every op is the reference's
+// RN32 step in the same order.
 namespace lnr {
-constexpr int ROWS = 32;  // one full warp of row chains
+constexpr int ROWS = 16;
 constexpr int kThreads = 128;
+__host__ __device__ inline size_t smem(int d) {
+  return (size_t)ROWS * (d + 8) * 2 + (size_t)ROWS * (d + 4) * 4 + 2 * ROWS * 4 + 16;
+}
 }  // namespace lnr
 
 __global__ void __launch_bounds__(lnr::kThreads) ln_rows_kernel(
     const uint16_t* __restrict__ x, int64_t T, int d, const uint16_t* __restrict__ g,
     const uint16_t* __restrict__ b, uint16_t* __restrict__ xn) {
   extern __shared__ __align__(16) uint8_t sm[];
-  const int xp = d + 8;
+  const int xp = d + 8, fp = d + 4;
   uint16_t* xs = reinterpret_cast<uint16_t*>(sm);
-  float* st = reinterpret_cast<float*>(sm + (size_t)lnr::ROWS * xp * 2);  // mean, inv
+  float* xf = reinterpret_cast<float*>(sm + (size_t)lnr::ROWS * xp * 2);
+  float* st = xf + (size_t)lnr::ROWS * fp;  // mean, inv
   uint64_t* bar = reinterpret_cast<uint64_t*>(st + 2 * lnr::ROWS);
   const int tid = threadIdx.x;
   const int64_t r0 = (int64_t)blockIdx.x * lnr::ROWS;
   const int nrow = (int)::min((int64_t)lnr::ROWS, T - r0);
-  const int d8 = d / 8;
+  const int d8 = d / 8, d4 = d / 4;
   if (tid == 0) {
     mbar_init(bar, 1);
     fence_barrier_init();
@@ -52,31 +64,37 @@ __global__ void __launch_bounds__(lnr::kThreads) ln_rows_kernel(
   }
   __syncthreads();
   mbar_wait(bar, 0);
+  for (int i = tid; i < nrow * d8; i += lnr::kThreads) {  // widen (exact)
+    const int r = i / d8, c = i % d8;
+    const uint4 v = *reinterpret_cast<const uint4*>(xs + r * xp + c * 8);
+    const uint16_t* h = reinterpret_cast<const uint16_t*>(&v);
+    float4* dst = reinterpret_cast<float4*>(xf + r * fp + c * 8);
+    dst[0] = make_float4(h2f(h[0]), h2f(h[1]), h2f(h[2]), h2f(h[3]));
+    dst[1] = make_float4(h2f(h[4]), h2f(h[5]), h2f(h[6]), h2f(h[7]));
+  }
+  __syncthreads();
   if (tid < nrow) {  // model.cpp:178-192, serial
-    // the next 16 bytes are loaded while the current 8 adds run (the shared
-    // load latency would otherwise sit on the dependent chain)
-    const uint4* row = reinterpret_cast<const uint4*>(xs + tid * xp);
+    const float4* row = reinterpret_cast<const float4*>(xf + tid * fp);
     float s = 0.f;
-    uint4 cur = row[0];
-    for (int c = 0; c < d8; ++c) {
-      const uint4 nxt = row[c + 1 < d8 ? c + 1 : c];
-      const uint16_t* h = reinterpret_cast<const uint16_t*>(&cur);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) s = __fadd_rn(s, h2f(h[i]));
-      cur = nxt;
+    for (int c = 0; c < d4; ++c) {
+      const float4 v = row[c];
+      s = __fadd_rn(s, v.x);
+      s = __fadd_rn(s, v.y);
+      s = __fadd_rn(s, v.z);
+      s = __fadd_rn(s, v.w);
     }
     const float mean = __fdiv_rn(s, (float)d);
+    const float2 m2 = make_float2(mean, mean);
     float v2 = 0.f;
-    cur = row[0];
-    for (int c = 0; c < d8; ++c) {
-      const uint4 nxt = row[c + 1 < d8 ? c + 1 : c];
-      const uint16_t* h = reinterpret_cast<const uint16_t*>(&cur);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float dx = __fsub_rn(h2f(h[i]), mean);
-        v2 = __fadd_rn(v2, __fmul_rn(dx, dx));
-      }
-      cur = nxt;
+    for (int c = 0; c < d4; ++c) {
+      const float4 v = row[c];
+      const float2 d01 = f2_sub(make_float2(v.x, v.y), m2);
+      const float2 d23 = f2_sub(make_float2(v.z, v.w), m2);
+      const float2 q01 = f2_mul(d01, d01), q23 = f2_mul(d23, d23);
+      v2 = __fadd_rn(v2, q01.x);
+      v2 = __fadd_rn(v2, q01.y);
+      v2 = __fadd_rn(v2, q23.x);
+      v2 = __fadd_rn(v2, q23.y);
     }
     st[tid] = mean;
     st[lnr::ROWS + tid] = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(v2, (float)d), 1e-5f)));
@@ -84,18 +102,29 @@ __global__ void __launch_bounds__(lnr::kThreads) ln_rows_kernel(
   __syncthreads();
   for (int i = tid; i < nrow * d8; i += lnr::kThreads) {  // model.cpp:193-194
     const int r = i / d8, c = i % d8;
-    uint4 v = *reinterpret_cast<const uint4*>(xs + r * xp + c * 8);
+    const float4* src = reinterpret_cast<const float4*>(xf + r * fp + c * 8);
     const uint4 gv = __ldg(reinterpret_cast<const uint4*>(g) + c);
     const uint4 bv = __ldg(reinterpret_cast<const uint4*>(b) + c);
-    uint16_t* h = reinterpret_cast<uint16_t*>(&v);
     const uint16_t* gh = reinterpret_cast<const uint16_t*>(&gv);
     const uint16_t* bh = reinterpret_cast<const uint16_t*>(&bv);
     const float mean = st[r], inv = st[lnr::ROWS + r];
+    uint4 o;
+    uint32_t* ow = reinterpret_cast<uint32_t*>(&o);
+    // scalar RN ops: ptxas contracts a packed f32x2 mul followed by a packed
+    // add into FFMA2 even under --fmad=false, which would change the bits
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
-      h[j] = f2h(__fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(h2f(h[j]), mean), inv), h2f(gh[j])),
-                           h2f(bh[j])));
-    *reinterpret_cast<uint4*>(xn + (r0 + r) * d + c * 8) = v;
+    for (int h = 0; h < 2; ++h) {
+      const float4 v = src[h];
+      const float xv[4] = {v.x, v.y, v.z, v.w};
+      float y[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        y[q] = __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(xv[q], mean), inv), h2f(gh[h * 4 + q])),
+                         h2f(bh[h * 4 + q]));
+      ow[2 * h] = (uint32_t)f2h(y[0]) | ((uint32_t)f2h(y[1]) << 16);
+      ow[2 * h + 1] = (uint32_t)f2h(y[2]) | ((uint32_t)f2h(y[3]) << 16);
+    }
+    *reinterpret_cast<uint4*>(xn + (r0 + r) * d + c * 8) = o;
   }
 }
 
@@ -103,6 +132,7 @@ __global__ void __launch_bounds__(lnr::kThreads) ln_rows_kernel(
 namespace gk {
 constexpr int kThreads = 256;
 constexpr int NS = 3;
+constexpr int kMaxCopies = 8;  // cp.async per thread per chunk, for x and for w each
 
 struct Cfg {
   int ng;       // expert groups (power of two)
@@ -131,10 +161,12 @@ __host__ __device__ inline Cfg cfg(int E, int gwp, int epg, int rpt) {
   c.xpitch = c.kc + 8;
   c.fpitch = c.kc + 4;  // 16-byte rows, consecutive row-threads on distinct banks
   c.xbytes = (size_t)c.rb * c.xpitch * 2;
-  c.wbytes = (size_t)c.kc * gwp * 4 + 64;  // + over-read slack of the last expert group
+  // gate weights staged transposed, [group][k][EPG]: a thread's EPG weights
+  // for consecutive k are contiguous (compile-time offsets, 16-byte loads)
+  c.wbytes = (size_t)c.ng * epg * c.kc * 4;
   c.stage = (c.xbytes + c.wbytes + 15) & ~size_t(15);
-  c.off_xf = NS * c.stage;  // f32 copy of the current xn chunk
-  const size_t pipe = c.off_xf + (size_t)c.rb * c.fpitch * 4;
+  c.off_xf = NS * c.stage;
+  const size_t pipe = c.off_xf;
   const size_t lg = (size_t)2 * c.rb * (E + 1) * 4;  // logits + expf values (reuse the ring)
   c.body = ((pipe > lg ? pipe : lg) + 15) & ~size_t(15);
   c.total = c.body + (size_t)c.rb * 8 * 4 + (size_t)(E + 1) * 4 + 16;  // + sel[8], hist
@@ -157,9 +189,10 @@ __global__ void __launch_bounds__(gk::kThreads) gate_topk_kernel(
     const uint16_t* __restrict__ xn, int64_t T, int d, const float* __restrict__ gw32, int gwp,
     const uint16_t* __restrict__ gb, int E, int k, const uint8_t* __restrict__ finished,
     uint32_t* __restrict__ expert, uint16_t* __restrict__ scale, uint32_t* __restrict__ blockcnt,
-    uint32_t* bad_row) {
+    uint32_t* bad_row, long long* trace) {
   extern __shared__ __align__(16) uint8_t sm[];
   const gk::Cfg C = gk::cfg(E, gwp, EPG, RPT);
+  long long tw = 0, tc = 0, t_0 = clock64();  // dev-only phase trace (MOE_GATE_TRACE)
   uint32_t* sel = reinterpret_cast<uint32_t*>(sm + C.body);  // [rb][8]
   uint32_t* hist = sel + C.rb * 8;
 
@@ -169,24 +202,48 @@ __global__ void __launch_bounds__(gk::kThreads) gate_topk_kernel(
   const int64_t r0 = (int64_t)blockIdx.x * C.rb;
   const int nrow = (int)::min((int64_t)C.rb, T - r0);
   const int KC = C.kc, nch = (d + KC - 1) / KC;
-  const int wq = (E + 3) / 4;  // 16-byte pieces per gate-weight row
 
   for (int i = tid; i <= E; i += gk::kThreads) hist[i] = 0;
 
+  // Every chunk copies the same (row, piece) / (k, expert-chunk) pattern, only
+  // shifted by k0: each thread's copy descriptors are computed once.
+  constexpr int CW = EPG >= 4 ? 4 : EPG;  // experts per weight copy (16 / 8 / 4 bytes)
+  constexpr int MAXC = gk::kMaxCopies;     // copies per thread per chunk (host-checked)
+  const int wc = (E + CW - 1) / CW;
+  const int nx = C.rb * (KC / 8), nw = KC * wc;
+  int xsrc[MAXC], xdst[MAXC], wsrc[MAXC], wdst[MAXC];
+#pragma unroll
+  for (int j = 0; j < MAXC; ++j) {  // fully unrolled: descriptors stay in registers
+    const int i = tid + j * gk::kThreads;
+    const int r = i / (KC / 8), q = i % (KC / 8);
+    xsrc[j] = (i < nx && r < nrow) ? (int)(r * d + q * 8) : -1;  // elements from row r0
+    xdst[j] = r * C.xpitch + q * 8;
+    const int kk = i / wc, e = (i % wc) * CW;
+    wsrc[j] = i < nw ? kk * gwp + e : -1;
+    wdst[j] = ((e / EPG) * KC + kk) * EPG + (e % EPG);
+  }
+  const uint16_t* xbase = xn + r0 * d;
   auto issue = [&](int c) {
     if (c < nch) {
       uint8_t* stg = sm + (size_t)(c % gk::NS) * C.stage;
       uint16_t* xs = reinterpret_cast<uint16_t*>(stg);
       float* ws = reinterpret_cast<float*>(stg + C.xbytes);
-      const int k0 = c * KC, kc = ::min(KC, d - k0), kq = kc / 8;
-      for (int i = tid; i < C.rb * kq; i += gk::kThreads) {
-        const int r = i / kq, q = i % kq;
-        const bool ok = r < nrow;
-        cp_async16(xs + r * C.xpitch + q * 8, ok ? xn + (r0 + r) * d + k0 + q * 8 : xn, ok);
+      const int k0 = c * KC;
+      const bool full = k0 + KC <= d;
+#pragma unroll
+      for (int j = 0; j < MAXC; ++j) {
+        if (tid + j * gk::kThreads >= nx) break;
+        const bool ok = xsrc[j] >= 0 && (full || (xsrc[j] % d) + k0 < d);
+        cp_async16(xs + xdst[j], ok ? xbase + xsrc[j] + k0 : xn, ok);
       }
-      for (int i = tid; i < kc * wq; i += gk::kThreads) {
-        const int kk = i / wq, q = i % wq;
-        cp_async16(ws + kk * gwp + q * 4, gw32 + (size_t)(k0 + kk) * gwp + q * 4, true);
+      const float* wk = gw32 + (size_t)k0 * gwp;
+#pragma unroll
+      for (int j = 0; j < MAXC; ++j) {
+        if (wsrc[j] < 0) break;
+        if (!full && wsrc[j] / gwp + k0 >= d) continue;
+        if constexpr (CW == 4) cp_async16(ws + wdst[j], wk + wsrc[j], true);
+        else if constexpr (CW == 2) cp_async8(ws + wdst[j], wk + wsrc[j]);
+        else cp_async4(ws + wdst[j], wk + wsrc[j]);
       }
     }
     cp_async_commit();
@@ -200,66 +257,62 @@ __global__ void __launch_bounds__(gk::kThreads) gate_topk_kernel(
   for (int i = 0; i < RPT; ++i)
 #pragma unroll
     for (int j = 0; j < NP; ++j) acc[i][j] = make_float2(0.f, 0.f);
-  float* xf = reinterpret_cast<float*>(sm + C.off_xf);
 
+  const long long t_1 = clock64();
   for (int c = 0; c < nch; ++c) {
+    const long long ta = clock64();
     cp_async_wait<gk::NS - 2>();
-    __syncthreads();  // chunk c landed; previous chunk's f32 copy fully consumed
-    const uint8_t* stg = sm + (size_t)(c % gk::NS) * C.stage;
-    const uint16_t* xs = reinterpret_cast<const uint16_t*>(stg);
-    const int kc = ::min(KC, d - c * KC), kq = kc / 8;
-    // widen the chunk once (fp16 -> f32 exactly), instead of per expert group
-    for (int i = tid; i < C.rb * kq; i += gk::kThreads) {
-      const int r = i / kq, q = i % kq;
-      const uint4 v = *reinterpret_cast<const uint4*>(xs + r * C.xpitch + q * 8);
-      const uint16_t* h = reinterpret_cast<const uint16_t*>(&v);
-      float4* dst = reinterpret_cast<float4*>(xf + r * C.fpitch + q * 8);
-      dst[0] = make_float4(h2f(h[0]), h2f(h[1]), h2f(h[2]), h2f(h[3]));
-      dst[1] = make_float4(h2f(h[4]), h2f(h[5]), h2f(h[6]), h2f(h[7]));
-    }
+    __syncthreads();  // chunk c landed for every thread; chunk c-1 fully consumed
+    tw += clock64() - ta;
     issue(c + gk::NS - 1);
-    __syncthreads();
-    const float* wp = reinterpret_cast<const float*>(stg + C.xbytes) + e0;
+    const long long tb = clock64();
+    const uint8_t* stg = sm + (size_t)(c % gk::NS) * C.stage;
+    const uint16_t* xr = reinterpret_cast<const uint16_t*>(stg) + rt * C.xpitch;
+    const float* wg = reinterpret_cast<const float*>(stg + C.xbytes) + (size_t)eg * KC * EPG;
+    const int kc = ::min(KC, d - c * KC);
     if (e0 < E) {
-      const float* xr = xf + rt * C.fpitch;
-      for (int kk = 0; kk < kc; kk += 4) {
-        float4 xv[RPT];
+      for (int kk = 0; kk < kc; kk += 8) {
+        // every operand of 8 k-steps first (latency), then the FMAs
+        uint4 xh[RPT];
 #pragma unroll
         for (int i = 0; i < RPT; ++i)
-          xv[i] = *reinterpret_cast<const float4*>(xr + i * C.rt * C.fpitch + kk);
+          xh[i] = *reinterpret_cast<const uint4*>(xr + i * C.rt * C.xpitch + kk);
+        float wv[8][EPG];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float* wr = wp + (kk + q) * gwp;
-          if constexpr (EPG >= 2) {
-            float2 w[NP];
-            if constexpr (EPG >= 4) {
+        for (int q = 0; q < 8; ++q) {
+          if constexpr (EPG >= 4) {
 #pragma unroll
-              for (int j = 0; j < NP; j += 2) {
-                const float4 w4 = *reinterpret_cast<const float4*>(wr + 2 * j);
-                w[j] = make_float2(w4.x, w4.y);
-                w[j + 1] = make_float2(w4.z, w4.w);
-              }
-            } else {
-              w[0] = *reinterpret_cast<const float2*>(wr);
-            }
-#pragma unroll
-            for (int i = 0; i < RPT; ++i) {
-              const float xq = q == 0 ? xv[i].x : q == 1 ? xv[i].y : q == 2 ? xv[i].z : xv[i].w;
-#pragma unroll
-              for (int j = 0; j < NP; ++j) acc[i][j] = gk::ffma2(xq, w[j], acc[i][j]);  // exact products
+            for (int j = 0; j < EPG; j += 4) {
+              const float4 w4 = *reinterpret_cast<const float4*>(wg + (kk + q) * EPG + j);
+              wv[q][j] = w4.x;
+              wv[q][j + 1] = w4.y;
+              wv[q][j + 2] = w4.z;
+              wv[q][j + 3] = w4.w;
             }
           } else {
-            const float w0 = wr[0];
 #pragma unroll
-            for (int i = 0; i < RPT; ++i) {
-              const float xq = q == 0 ? xv[i].x : q == 1 ? xv[i].y : q == 2 ? xv[i].z : xv[i].w;
-              acc[i][0].x = fmaf(xq, w0, acc[i][0].x);
+            for (int j = 0; j < EPG; ++j) wv[q][j] = wg[(kk + q) * EPG + j];
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+#pragma unroll
+          for (int i = 0; i < RPT; ++i) {
+            const float xq = h2f(reinterpret_cast<const uint16_t*>(&xh[i])[q]);
+            if constexpr (EPG >= 2) {
+#pragma unroll
+              for (int j = 0; j < NP; ++j)  // exact products, k order kept per chain
+                acc[i][j] = gk::ffma2(xq, make_float2(wv[q][2 * j], wv[q][2 * j + 1]), acc[i][j]);
+            } else {
+              acc[i][0].x = fmaf(xq, wv[q][0], acc[i][0].x);
             }
           }
         }
       }
     }
+    tc += clock64() - tb;
   }
+  const long long t_2 = clock64();
   cp_async_wait<0>();
   __syncthreads();  // ring free: reuse as logits / expf buffers
 
@@ -351,6 +404,14 @@ __global__ void __launch_bounds__(gk::kThreads) gate_topk_kernel(
   }
   __syncthreads();
   for (int i = tid; i <= E; i += gk::kThreads) blockcnt[(int64_t)i * gridDim.x + blockIdx.x] = hist[i];
+  if (trace != nullptr && blockIdx.x == 0 && tid == 0) {
+    trace[0] = t_1 - t_0;  // prologue (first issues)
+    trace[1] = tw;         // chunk waits + barriers
+    trace[2] = tc;         // chunk compute
+    trace[3] = t_2 - t_1;  // whole chunk loop
+    trace[4] = clock64() - t_2;  // top-k, expf, scales, histogram
+    trace[5] = nch;
+  }
 }
 
 // ================================================================= launchers
@@ -372,27 +433,46 @@ int launch_widen_gate(const uint16_t* gw, int64_t d, int64_t E, int64_t gwp, flo
 
 int64_t gate_fused_pitch(int64_t E) { return (E + 3) / 4 * 4; }
 
+// copy descriptors of a config fit the per-thread register arrays
+static bool copies_fit(int64_t E, int epg, const gk::Cfg& c) {
+  const int cw = epg >= 4 ? 4 : epg;
+  const int64_t nx = (int64_t)c.rb * (c.kc / 8), nw = (int64_t)c.kc * ((E + cw - 1) / cw);
+  return nx <= (int64_t)gk::kThreads * gk::kMaxCopies && nw <= (int64_t)gk::kThreads * gk::kMaxCopies;
+}
+
 // (EPG, RPT): the most chains per thread (FFMA2 pairs, shared weight loads)
 // that still fills the machine; below that the gate is latency-bound and
 // 8 expert chains per thread beat many one-chain CTAs.
 static void pick(int64_t T, int64_t E, int k, int* epg, int* rpt) {
   const int64_t gwp = gate_fused_pitch(E);
-  const gk::Cfg c82 = gk::cfg((int)E, (int)gwp, 8, 2);
-  if ((int64_t)c82.rb * k <= 1024 && (T + c82.rb - 1) / c82.rb >= 148) {
-    *epg = 8;
-    *rpt = 2;
-    return;
-  }
-  static const int kEpg[] = {8, 4, 2, 1};
-  for (int i = 0; i < 4; ++i) {
-    const gk::Cfg c = gk::cfg((int)E, (int)gwp, kEpg[i], 1);
-    if ((int64_t)c.rb * k <= 1024) {
-      *epg = kEpg[i];
-      *rpt = 1;
+  if (const char* ov = std::getenv("MOE_GATE_CFG")) {  // dev experiments: "EPG,RPT"
+    int a = 0, b = 0;
+    if (std::sscanf(ov, "%d,%d", &a, &b) == 2 && (a == 1 || a == 2 || a == 4 || a == 8) &&
+        (b == 1 || (b == 2 && a == 8))) {
+      *epg = a;
+      *rpt = b;
       return;
     }
   }
-  *epg = 1;
+  // Measured on B200 (scripts/route_probe.py): the machine must be filled
+  // first (C2: 1 chain/thread over 128 CTAs beats 8 chains/thread over 16),
+  // then more chains per thread win (C4: 8x2 over 256 CTAs); below one CTA
+  // per SM, 4 chains per thread balance latency and parallelism (C3 decode).
+  static const int kE[] = {8, 8, 4, 2, 1};
+  static const int kR[] = {2, 1, 1, 1, 1};
+  for (int i = 0; i < 5; ++i) {
+    const gk::Cfg c = gk::cfg((int)E, (int)gwp, kE[i], kR[i]);
+    if ((int64_t)c.rb * k <= 1024 && copies_fit(E, kE[i], c) && (T + c.rb - 1) / c.rb >= 148) {
+      *epg = kE[i];
+      *rpt = kR[i];
+      return;
+    }
+  }
+  // otherwise: the most CTAs if that still covers half the SMs, else 4 chains
+  const gk::Cfg c1 = gk::cfg((int)E, (int)gwp, 1, 1);
+  const gk::Cfg c4 = gk::cfg((int)E, (int)gwp, 4, 1);
+  const bool ok1 = copies_fit(E, 1, c1), ok4 = copies_fit(E, 4, c4) && (int64_t)c4.rb * k <= 1024;
+  *epg = (ok1 && ((T + c1.rb - 1) / c1.rb >= 74 || !ok4)) ? 1 : 4;
   *rpt = 1;
 }
 
@@ -404,10 +484,11 @@ int gate_fused_rows(int64_t T, int64_t E, int k) {
 
 bool gate_fused_supported(int64_t d, int64_t E, int k) {
   if (d % 8 != 0 || k < 1 || k > 8 || E < 1 || E > 256) return false;
-  if ((size_t)lnr::ROWS * (d + 8) * 2 + 256 > 200 * 1024) return false;
-  // slots of one gate block must fit a plan_place block (<= 1024 threads)
-  const gk::Cfg c = gk::cfg((int)E, (int)gate_fused_pitch(E), 1, 1);
-  return (int64_t)c.rb * k <= 1024 && c.total <= 200 * 1024;
+  if (lnr::smem((int)d) > 200 * 1024) return false;
+  // slots of one gate block must fit a plan_place block (<= 1024 threads),
+  // and the EPG=4 fallback must fit the copy descriptors
+  const gk::Cfg c = gk::cfg((int)E, (int)gate_fused_pitch(E), 4, 1);
+  return (int64_t)c.rb * k <= 1024 && copies_fit(E, 4, c) && c.total <= 200 * 1024;
 }
 
 template <int EPG, int RPT>
@@ -420,17 +501,25 @@ static int launch_gk(const GateFusedArgs& a, cudaStream_t st) {
     attr = C.total;
   }
   const unsigned grid = (unsigned)((a.T + C.rb - 1) / C.rb);
+  static long long* trace = nullptr;
+  const bool tr = std::getenv("MOE_GATE_TRACE") != nullptr;
+  if (tr && !trace) MOE_CUDA_TRY(cudaMallocManaged(&trace, 8 * 8));
   gate_topk_kernel<EPG, RPT><<<grid, gk::kThreads, C.total, st>>>(
       a.xn, a.T, (int)a.d, a.gw32, (int)a.gwp, a.gb, (int)a.E, a.k, a.finished, a.expert,
-      a.scale, a.blockcnt, a.bad_row);
+      a.scale, a.blockcnt, a.bad_row, tr ? trace : nullptr);
   note_launch();
+  if (tr) {
+    cudaStreamSynchronize(st);
+    std::fprintf(stderr, "gate_trace EPG=%d RPT=%d grid=%u rb=%d kc=%d: pro=%lld wait=%lld comp=%lld loop=%lld tail=%lld nch=%lld\n",
+                 EPG, RPT, grid, C.rb, C.kc, trace[0], trace[1], trace[2], trace[3], trace[4], trace[5]);
+  }
   return check_launch("gate_topk");
 }
 
 int launch_gate_fused(const GateFusedArgs& a, cudaStream_t st) {
   if (a.T == 0) return MOE_OK;
   // 1. LayerNorm rows
-  const size_t smem = (size_t)lnr::ROWS * (a.d + 8) * 2 + 2 * lnr::ROWS * 4 + 16;
+  const size_t smem = lnr::smem((int)a.d);
   static size_t attr = 0;
   if (smem > 48 * 1024 && smem > attr) {
     MOE_CUDA_TRY(cudaFuncSetAttribute(ln_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -17,13 +17,15 @@
 // Loads run U k-blocks ahead (double-buffered registers) so every warp keeps
 // 2-4 KB in flight.  Split-K partials (f32) are reduced in a fixed order by
 // the last CTA of each (problem, feature tile) -- deterministic.
+#include <type_traits>
+
 #include "kernels.cuh"
 
 namespace moecu {
 
 namespace gv {
-constexpr int kWarps = 8;
-constexpr int kThreads = 32 * kWarps;
+constexpr int kWarps = 8;                 // compute warps, 16 features each
+constexpr int kThreads = 32 * (kWarps + 1);  // + one producer warp
 constexpr int NT = 16;  // token rows per pass (2 MMA n-tiles)
 
 template <int BITS>
@@ -106,155 +108,266 @@ struct Params {
   int64_t m, n, rows, nft, nkb;
   int np, nsplit, kbs_per_split, relu;
   uint32_t db2;           // debias constant in both halves
+  uint32_t hb2;           // -(64 + debias - 1024) in both halves (i2f_u4_fast)
+  int nitems;             // np * nft * nsplit work items, strided over persistent CTAs
+};
+
+// Weight blocks stream through a ring of NST stages (TMA bulk copies issued
+// by a producer warp, mbarrier full/empty handshake); the 8 compute warps read
+// their fragment words from shared memory.  Registers stay free for
+// occupancy, and every CTA keeps NST x WBYTES of weights in flight.
+template <int BITS>
+struct Ring {
+  static constexpr int WB = wblock_bytes(BITS);
+  static constexpr int NST = BITS == 4 ? 8 : BITS == 8 ? 6 : 4;
 };
 
 template <int BITS>
-__global__ void __launch_bounds__(kThreads, 2) gemv_kernel(const Params P) {
-  using F = Frag<BITS>;
-  constexpr int WBYTES = wblock_bytes(BITS);
-  extern __shared__ __align__(16) uint16_t xs[];  // [NT][kp]
-  __shared__ uint32_t s_last;
-  const int split = blockIdx.x % P.nsplit;
-  const int ft = (blockIdx.x / P.nsplit) % P.nft;
-  const int p = blockIdx.x / (P.nsplit * (int)P.nft);
-  if (p >= P.np) return;
-  const int64_t e = P.problems[3 * p];
-  const int64_t r0 = P.problems[3 * p + 1], r1 = P.problems[3 * p + 2];
-  if (r1 <= r0) return;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  const int kb0 = split * P.kbs_per_split;
-  const int kb1 = (int)(P.nkb < (int64_t)(kb0 + P.kbs_per_split) ? P.nkb : (int64_t)(kb0 + P.kbs_per_split));
-  if (kb0 >= kb1) return;
-  const int kspan = (kb1 - kb0) * 64;
-  const int kp = kspan + 8;  // conflict-free fragment reads (see header)
-  const int fg = warp * 16 + g;
-  const uint8_t* wbase = P.tiled + ((e * P.nft + ft) * P.nkb) * (int64_t)WBYTES;
-  const int64_t feat0 = (int64_t)ft * 128 + warp * 16;
-  float sc[2] = {1.f, 1.f}, bi[2] = {0.f, 0.f};
+__device__ __forceinline__ void frag_from_smem(const uint8_t* blk, int fg, int t,
+                                               uint32_t (&w)[Frag<BITS>::NW]) {
+  if constexpr (BITS == 4) {
+    const uint8_t* p = blk + (t >> 1) * 2048 + (t & 1) * 8;
+    const uint2 a = *reinterpret_cast<const uint2*>(p + fg * 16);
+    const uint2 b = *reinterpret_cast<const uint2*>(p + (fg + 8) * 16);
+    w[0] = a.x; w[1] = a.y; w[2] = b.x; w[3] = b.y;
+  } else if constexpr (BITS == 8) {
+    const uint8_t* p = blk + t * 2048;
+    const uint4 a = *reinterpret_cast<const uint4*>(p + fg * 16);
+    const uint4 b = *reinterpret_cast<const uint4*>(p + (fg + 8) * 16);
+    w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+    w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
+  } else {
+    const uint8_t* p = blk + 2 * t * 2048;
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int64_t f = feat0 + g + 8 * h;
-    if (f < P.n) {
-      if (P.scales) sc[h] = h2f(P.scales[e * P.n + f]);
-      bi[h] = h2f(P.bias[e * P.n + f]);
+    for (int c = 0; c < 2; ++c) {
+      const uint4 a = *reinterpret_cast<const uint4*>(p + c * 2048 + fg * 16);
+      const uint4 b = *reinterpret_cast<const uint4*>(p + c * 2048 + (fg + 8) * 16);
+      w[4 * c + 0] = a.x; w[4 * c + 1] = a.y; w[4 * c + 2] = a.z; w[4 * c + 3] = a.w;
+      w[8 + 4 * c + 0] = b.x; w[8 + 4 * c + 1] = b.y; w[8 + 4 * c + 2] = b.z; w[8 + 4 * c + 3] = b.w;
     }
   }
+}
 
-  using W = uint32_t[F::U][F::NW];
-  auto load_group = [&](int kb, W& w) {
-#pragma unroll
-    for (int u = 0; u < F::U; ++u)
-      if (kb + u < kb1) load_frag<BITS>(wbase + (int64_t)(kb + u) * WBYTES, fg, t, w[u]);
-  };
-  for (int64_t rb = r0; rb < r1; rb += NT) {
-    const int nrow = (int)(r1 - rb < (int64_t)NT ? r1 - rb : (int64_t)NT);
-    uint32_t wa[F::U][F::NW], wb[F::U][F::NW];
-    __syncthreads();  // previous pass done with xs
-    // first weight group in flight before waiting for the activations
-    load_group(kb0, wa);
-    // stage x[rb .. rb+nrow)[k range] (zero-filled past m / past nrow)
-    const int kq = kspan / 8;
-    for (int i = threadIdx.x; i < NT * kq; i += kThreads) {
-      const int r = i / kq, c = i % kq;
-      const int64_t k = (int64_t)kb0 * 64 + c * 8;
-      const bool ok = r < nrow && k < P.m;
-      cp_async16(xs + r * kp + c * 8, ok ? P.x + (rb + r) * P.m + k : P.x, ok);
+constexpr int kCompute = 32 * kWarps;  // compute threads; warp kWarps is the producer
+
+template <int BITS>
+__device__ __forceinline__ void dequant_fast(const uint32_t (&w)[Frag<BITS>::NW], uint32_t db2,
+                                             uint32_t hb2, uint32_t (&lo)[8], uint32_t (&hi)[8]) {
+  if constexpr (BITS == 4) {
+    i2f_u4_fast(w[0], db2, hb2, &lo[0]);
+    i2f_u4_fast(w[1], db2, hb2, &lo[4]);
+    i2f_u4_fast(w[2], db2, hb2, &hi[0]);
+    i2f_u4_fast(w[3], db2, hb2, &hi[4]);
+  } else {
+    dequant_frag<BITS>(w, db2, lo, hi);
+  }
+}
+
+struct Item {
+  int64_t e, r0, r1;
+  int ft, split, kb0, kb1;
+};
+
+// item order: feature tile fastest, then k-split, then problem -- a CTA's
+// consecutive items share the expert rows it has staged
+__device__ __forceinline__ Item item_at(const Params& P, int i) {
+  Item it;
+  it.ft = i % (int)P.nft;
+  it.split = (i / (int)P.nft) % P.nsplit;
+  const int p = i / (P.nsplit * (int)P.nft);
+  it.e = P.problems[3 * p];
+  it.r0 = P.problems[3 * p + 1];
+  it.r1 = P.problems[3 * p + 2];
+  it.kb0 = it.split * P.kbs_per_split;
+  const int64_t hi = (int64_t)it.kb0 + P.kbs_per_split;
+  it.kb1 = (int)(P.nkb < hi ? P.nkb : hi);
+  return it;
+}
+
+// Persistent: CTA b handles work items b, b + grid, ...  The producer warp
+// streams the weight blocks of all of them back to back through the ring
+// (it never drains between items); the compute warps stage only the live
+// rows of each item (the MMA's unused B rows only feed discarded columns).
+template <int BITS>
+__global__ void __launch_bounds__(kThreads, 3) gemv_kernel(const Params P) {
+  using F = Frag<BITS>;
+  using RG = Ring<BITS>;
+  extern __shared__ __align__(1024) uint8_t gsm[];
+  uint8_t* ring = gsm;                                            // [NST][WB]
+  uint64_t* full = reinterpret_cast<uint64_t*>(gsm + RG::NST * RG::WB);
+  uint64_t* empty = full + RG::NST;
+  uint16_t* xs = reinterpret_cast<uint16_t*>(empty + RG::NST);  // [NT][kp]
+  __shared__ uint32_t s_last;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int kp = P.kbs_per_split * 64 + 8;  // row pitch of xs (conflict-free fragments)
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < RG::NST; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kWarps);
     }
-    cp_async_commit();
-    cp_async_wait<0>();
-    __syncthreads();
+    fence_barrier_init();
+  }
+  __syncthreads();
 
-    // two independent accumulator chains per n-tile (even / odd MMA of a
-    // k-block) halve the dependent mma.sync latency chain
-    float acc[2][2][4];
-#pragma unroll
-    for (int j = 0; j < 2; ++j)
-#pragma unroll
-      for (int c = 0; c < 2; ++c)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) acc[j][c][q] = 0.f;
-
-    auto compute_group = [&](int kb, const W& w) {
-#pragma unroll
-      for (int u = 0; u < F::U; ++u) {
-        if (kb + u >= kb1) break;
-        uint32_t lo[8], hi[8];
-        dequant_frag<BITS>(w[u], P.db2, lo, hi);
-        const uint16_t* xk = xs + (kb + u - kb0) * 64 + 16 * t;
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          if (j * 8 >= nrow) break;
-          const uint4 xa = *reinterpret_cast<const uint4*>(xk + (j * 8 + g) * kp);
-          const uint4 xb = *reinterpret_cast<const uint4*>(xk + (j * 8 + g) * kp + 8);
-          const uint32_t xv[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const uint32_t a[4] = {lo[2 * i], hi[2 * i], lo[2 * i + 1], hi[2 * i + 1]};
-            mma_16816(acc[j][i & 1], a, xv[2 * i], xv[2 * i + 1]);
+  if (warp == kWarps) {
+    // ------------------------------------------------------------- producer
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      int n = 0;
+      const int ipc = (P.nitems + gridDim.x - 1) / gridDim.x;
+      const int i0 = blockIdx.x * ipc, i1 = min(P.nitems, i0 + ipc);
+      for (int i = i0; i < i1; ++i) {
+        const Item it = item_at(P, i);
+        if (it.r1 <= it.r0) continue;
+        const uint8_t* wb = P.tiled + ((it.e * P.nft + it.ft) * P.nkb) * (int64_t)RG::WB;
+        const int npass = (int)((it.r1 - it.r0 + NT - 1) / NT);
+        for (int pass = 0; pass < npass; ++pass)
+          for (int kb = it.kb0; kb < it.kb1; ++kb, ++n) {
+            if (n >= RG::NST) mbar_wait(&empty[s], ph ^ 1u);
+            mbar_arrive_expect_tx(&full[s], RG::WB);
+            bulk_load(ring + s * RG::WB, wb + (int64_t)kb * RG::WB, RG::WB, &full[s]);
+            if (++s == RG::NST) {
+              s = 0;
+              ph ^= 1u;
+            }
           }
+      }
+    }
+  } else {
+    // -------------------------------------------------------------- compute
+    int s = 0;
+    uint32_t ph = 0;
+    const int fg = warp * 16 + g;
+    const int ipc = (P.nitems + gridDim.x - 1) / gridDim.x;
+    const int i0 = blockIdx.x * ipc, i1 = min(P.nitems, i0 + ipc);
+    int64_t staged_r = -1;  // first row staged in xs (-1: none)
+    int staged_kb = -1;
+    for (int i = i0; i < i1; ++i) {
+      const Item it = item_at(P, i);
+      if (it.r1 <= it.r0) continue;
+      const int64_t feat0 = (int64_t)it.ft * 128 + warp * 16;
+      float sc[2] = {1.f, 1.f}, bi[2] = {0.f, 0.f};
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t f = feat0 + g + 8 * h;
+        if (f < P.n) {
+          if (P.scales) sc[h] = h2f(P.scales[it.e * P.n + f]);
+          bi[h] = h2f(P.bias[it.e * P.n + f]);
         }
       }
-    };
-    for (int kb = kb0; kb < kb1; kb += 2 * F::U) {
-      load_group(kb + F::U, wb);
-      compute_group(kb, wa);
-      if (kb + F::U >= kb1) break;
-      load_group(kb + 2 * F::U, wa);
-      compute_group(kb + F::U, wb);
-    }
-#pragma unroll
-    for (int j = 0; j < 2; ++j)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) acc[j][0][q] += acc[j][1][q];
-
-    // D fragment: acc[j][0..1] -> feature g, tokens 8j+2t, +1; [2..3] -> feature g+8
-    if (P.nsplit == 1) {
-#pragma unroll
-      for (int j = 0; j < 2; ++j)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int tok = j * 8 + 2 * t + (q & 1), h = q >> 1;
-          const int64_t f = feat0 + g + 8 * h;
-          if (tok < nrow && f < P.n) {
-            float v = fmaf(acc[j][0][q], sc[h], bi[h]);
-            if (P.relu) v = v > 0.f ? v : 0.f;
-            P.out[(rb + tok) * P.n + f] = f2h(v);
+      const int nkbl = it.kb1 - it.kb0;
+      const int kq = nkbl * 8;  // 16-byte pieces per staged row
+      for (int64_t rb = it.r0; rb < it.r1; rb += NT) {
+        const int nrow = (int)(it.r1 - rb < (int64_t)NT ? it.r1 - rb : (int64_t)NT);
+        if (rb != staged_r || it.kb0 != staged_kb) {  // same rows as the last item: reuse
+          named_bar_sync(1, kCompute);  // everyone done with xs
+          for (int q = threadIdx.x; q < nrow * kq; q += kCompute) {
+            const int r = q / kq, c = q % kq;
+            const int64_t k = (int64_t)it.kb0 * 64 + c * 8;
+            const bool ok = k < P.m;
+            cp_async16(xs + r * kp + c * 8, ok ? P.x + (rb + r) * P.m + k : P.x, ok);
           }
+          cp_async_commit();
+          cp_async_wait<0>();
+          named_bar_sync(1, kCompute);
+          staged_r = rb;
+          staged_kb = it.kb0;
         }
-    } else {
+
+        float acc[2][2][4];
 #pragma unroll
-      for (int j = 0; j < 2; ++j)
+        for (int j = 0; j < 2; ++j)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int tok = j * 8 + 2 * t + (q & 1), h = q >> 1;
-          const int64_t f = feat0 + g + 8 * h;
-          if (tok < nrow && f < P.n) P.part[((int64_t)split * P.rows + rb + tok) * P.n + f] = acc[j][0][q];
+          for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[j][c][q] = 0.f;
+        const uint16_t* xk0 = xs + 16 * t + g * kp;
+        auto kloop = [&](auto ntile_c) {
+          constexpr int NTL = decltype(ntile_c)::value;
+          const uint16_t* xk = xk0;
+          for (int kbl = 0; kbl < nkbl; ++kbl, xk += 64) {
+            mbar_wait(&full[s], ph);
+            uint32_t w[F::NW];
+            frag_from_smem<BITS>(ring + s * RG::WB, fg, t, w);
+            uint32_t lo[8], hi[8];
+            dequant_fast<BITS>(w, P.db2, P.hb2, lo, hi);
+#pragma unroll
+            for (int j = 0; j < NTL; ++j) {
+              const uint4 xa = *reinterpret_cast<const uint4*>(xk + j * 8 * kp);
+              const uint4 xb = *reinterpret_cast<const uint4*>(xk + j * 8 * kp + 8);
+              const uint32_t xv[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const uint32_t a[4] = {lo[2 * q], hi[2 * q], lo[2 * q + 1], hi[2 * q + 1]};
+                mma_16816(acc[j][q & 1], a, xv[2 * q], xv[2 * q + 1]);
+              }
+            }
+            // the MMAs consumed every word loaded from the stage (in every
+            // lane): only now may the producer refill it
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+            if (++s == RG::NST) {
+              s = 0;
+              ph ^= 1u;
+            }
+          }
+        };
+        if (nrow > 8)
+          kloop(std::integral_constant<int, 2>{});
+        else
+          kloop(std::integral_constant<int, 1>{});
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[j][0][q] += acc[j][1][q];
+        // D fragment: acc[j][0][0..1] -> feature g, tokens 8j+2t, +1; [2..3] -> g+8
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int tok = j * 8 + 2 * t + (q & 1), h = q >> 1;
+            const int64_t f = feat0 + g + 8 * h;
+            if (tok < nrow && f < P.n) {
+              if (P.nsplit == 1) {
+                float v = fmaf(acc[j][0][q], sc[h], bi[h]);
+                if (P.relu) v = v > 0.f ? v : 0.f;
+                P.out[(rb + tok) * P.n + f] = f2h(v);
+              } else {
+                P.part[((int64_t)it.split * P.rows + rb + tok) * P.n + f] = acc[j][0][q];
+              }
+            }
+          }
+      }
+      if (P.nsplit > 1) {
+        // last CTA of this (expert, feature tile) reduces the splits in order
+        __threadfence();
+        named_bar_sync(1, kCompute);
+        if (threadIdx.x == 0) {
+          const uint32_t prev = atomicAdd(&P.ticket[it.e * P.nft + it.ft], 1u);
+          s_last = prev == (uint32_t)P.nsplit - 1;
         }
+        named_bar_sync(1, kCompute);
+        if (s_last) {
+          __threadfence();
+          const int64_t nrows = it.r1 - it.r0;
+          const int64_t fbase = (int64_t)it.ft * 128;
+          for (int64_t q = threadIdx.x; q < nrows * 128; q += kCompute) {
+            const int64_t r = it.r0 + q / 128, f = fbase + q % 128;
+            if (f >= P.n) continue;
+            float a = 0.f;
+            for (int s2 = 0; s2 < P.nsplit; ++s2)
+              a += __ldcg(&P.part[((int64_t)s2 * P.rows + r) * P.n + f]);
+            float v = fmaf(a, P.scales ? h2f(P.scales[it.e * P.n + f]) : 1.f,
+                           h2f(P.bias[it.e * P.n + f]));
+            if (P.relu) v = v > 0.f ? v : 0.f;
+            P.out[r * P.n + f] = f2h(v);
+          }
+          if (threadIdx.x == 0) P.ticket[it.e * P.nft + it.ft] = 0;
+        }
+      }
     }
   }
-  if (P.nsplit == 1) return;
-  // last CTA of this (problem, feature tile) reduces the splits in order
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const uint32_t prev = atomicAdd(&P.ticket[e * P.nft + ft], 1u);
-    s_last = prev == (uint32_t)P.nsplit - 1;
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  const int64_t nrows = r1 - r0;
-  const int64_t fbase = (int64_t)ft * 128;
-  for (int64_t i = threadIdx.x; i < nrows * 128; i += kThreads) {
-    const int64_t r = r0 + i / 128, f = fbase + i % 128;
-    if (f >= P.n) continue;
-    float a = 0.f;
-    for (int s = 0; s < P.nsplit; ++s) a += __ldcg(&P.part[((int64_t)s * P.rows + r) * P.n + f]);
-    float v = fmaf(a, P.scales ? h2f(P.scales[e * P.n + f]) : 1.f, h2f(P.bias[e * P.n + f]));
-    if (P.relu) v = v > 0.f ? v : 0.f;
-    P.out[r * P.n + f] = f2h(v);
-  }
-  if (threadIdx.x == 0) P.ticket[e * P.nft + ft] = 0;
 }
 }  // namespace gv
 
@@ -262,13 +375,19 @@ int gemv_splits(int64_t m, int64_t n, double active_experts) {
   const int64_t nft = (n + 127) / 128, nkb = (m + 63) / 64;
   int s = 1;
   while (s < 16 && nkb / (2 * s) >= 4 && active_experts * nft * s < 2.0 * 148) s *= 2;
+  while (s < 64 && (nkb + s - 1) / s > 16) s *= 2;  // <= 1024 inputs staged per CTA
   return s;
 }
 
-size_t gemv_smem(int64_t m, int nsplit) {
+static size_t ring_bytes(int bits) {
+  const int nst = bits == 4 ? gv::Ring<4>::NST : bits == 8 ? gv::Ring<8>::NST : gv::Ring<16>::NST;
+  return (size_t)nst * wblock_bytes(bits) + 2 * nst * 8;
+}
+
+size_t gemv_smem(int64_t m, int nsplit, int bits) {
   const int64_t nkb = (m + 63) / 64;
   const int64_t kbs = (nkb + nsplit - 1) / nsplit;
-  return (size_t)gv::NT * (kbs * 64 + 8) * 2;
+  return ring_bytes(bits) + (size_t)gv::NT * (kbs * 64 + 8) * 2;
 }
 
 template <int BITS>
@@ -292,14 +411,22 @@ static int run_gemv(const GemmArgs& a, const GemvWork& w, cudaStream_t st) {
   P.nsplit = (int)((P.nkb + P.kbs_per_split - 1) / P.kbs_per_split);  // no empty splits
   P.relu = a.relu;
   P.db2 = (uint32_t)a.debias | ((uint32_t)a.debias << 16);
-  const size_t smem = gemv_smem(a.m, w.nsplit);
+  {
+    const int off = (int)(a.debias & 0x3FF);  // debias - 1024 (8; 9 under MOE_FAULT_INJECT)
+    const uint16_t hb = (uint16_t)(0x8000 | (21 << 10) | (off << 4));  // -(64 + off)
+    P.hb2 = (uint32_t)hb | ((uint32_t)hb << 16);
+  }
+  P.nitems = (int)(a.np * P.nft * P.nsplit);
+  const size_t smem = gemv_smem(a.m, w.nsplit, BITS);
   static size_t attr = 0;
   if (smem > 48 * 1024 && smem > attr) {
     MOE_CUDA_TRY(cudaFuncSetAttribute(gv::gemv_kernel<BITS>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = smem;
   }
-  const int64_t grid = a.np * P.nft * P.nsplit;
+  // persistent: enough CTAs for the live items (empty problems are skipped
+  // inside), at most 3 per SM
+  const int64_t grid = std::min<int64_t>((int64_t)P.nitems, 3 * (int64_t)sm_count());
   gv::gemv_kernel<BITS><<<(unsigned)grid, gv::kThreads, smem, st>>>(P);
   note_launch();
   return check_launch("gemv");
@@ -310,7 +437,7 @@ int launch_gemv(const GemmArgs& a, const GemvWork& w, cudaStream_t st) {
   if (a.m % 8 != 0) return set_error(MOE_EINVAL, "gemv: m must be a multiple of 8");
   if (w.nsplit > 1 && (w.part == nullptr || w.ticket == nullptr))
     return set_error(MOE_EINVAL, "gemv: split-K workspace missing");
-  if (gemv_smem(a.m, w.nsplit) > 200 * 1024)
+  if (gemv_smem(a.m, w.nsplit, a.bits) > 200 * 1024)
     return set_error(MOE_EINVAL, "gemv: k range too long for one CTA (raise nsplit)");
   switch (a.bits) {
     case 4: return run_gemv<4>(a, w, st);

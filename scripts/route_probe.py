@@ -1,0 +1,18 @@
+"""Dev probe: device time of moe_layer_route (LN + gate + plan + gather) per config."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from oracle.oracle import random_layer
+from paper_2211_10017_b200.ops import MoELayer
+d, f, E, T, k = [int(v) for v in sys.argv[1:6]]
+lw = random_layer(d, 64, E, seed=1)
+L = MoELayer(lw.ln_g, lw.ln_b, lw.gw, lw.gb, lw.w1, lw.b1, lw.w2, lw.b2, bits=16)
+x = torch.randn(T, d, device="cuda").half()
+L.reserve(T, k)
+for _ in range(3): L.route(x, None, k)
+torch.cuda.synchronize()
+s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+s.record()
+for _ in range(20): L.route(x, None, k)
+e.record(); torch.cuda.synchronize()
+print(f"route d={d} E={E} T={T} k={k} cfg={os.environ.get('MOE_GATE_CFG','auto')}: {s.elapsed_time(e)/20*1e3:.1f} us")
