@@ -128,6 +128,74 @@ __global__ void __launch_bounds__(lnr::kThreads) ln_rows_kernel(
   }
 }
 
+// Large-T form: 32 rows per CTA, conversions inline (higher occupancy; the
+// kernel is issue-bound there, not latency-bound).
+__global__ void __launch_bounds__(128) ln_rows_wide_kernel(
+    const uint16_t* __restrict__ x, int64_t T, int d, const uint16_t* __restrict__ g,
+    const uint16_t* __restrict__ b, uint16_t* __restrict__ xn) {
+  constexpr int ROWS = 32;
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int xp = d + 8;
+  uint16_t* xs = reinterpret_cast<uint16_t*>(sm);
+  float* st = reinterpret_cast<float*>(sm + (size_t)ROWS * xp * 2);  // mean, inv
+  uint64_t* bar = reinterpret_cast<uint64_t*>(st + 2 * ROWS);
+  const int tid = threadIdx.x;
+  const int64_t r0 = (int64_t)blockIdx.x * ROWS;
+  const int nrow = (int)::min((int64_t)ROWS, T - r0);
+  const int d8 = d / 8;
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_barrier_init();
+    mbar_arrive_expect_tx(bar, (uint32_t)nrow * d * 2);
+    for (int r = 0; r < nrow; ++r) bulk_load(xs + r * xp, x + (r0 + r) * d, (uint32_t)d * 2, bar);
+  }
+  __syncthreads();
+  mbar_wait(bar, 0);
+  if (tid < nrow) {  // model.cpp:178-192, serial
+    const uint4* row = reinterpret_cast<const uint4*>(xs + tid * xp);
+    float s = 0.f;
+    uint4 cur = row[0];
+    for (int c = 0; c < d8; ++c) {
+      const uint4 nxt = row[c + 1 < d8 ? c + 1 : c];
+      const uint16_t* h = reinterpret_cast<const uint16_t*>(&cur);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) s = __fadd_rn(s, h2f(h[i]));
+      cur = nxt;
+    }
+    const float mean = __fdiv_rn(s, (float)d);
+    float v2 = 0.f;
+    cur = row[0];
+    for (int c = 0; c < d8; ++c) {
+      const uint4 nxt = row[c + 1 < d8 ? c + 1 : c];
+      const uint16_t* h = reinterpret_cast<const uint16_t*>(&cur);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float dx = __fsub_rn(h2f(h[i]), mean);
+        v2 = __fadd_rn(v2, __fmul_rn(dx, dx));
+      }
+      cur = nxt;
+    }
+    st[tid] = mean;
+    st[ROWS + tid] = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(v2, (float)d), 1e-5f)));
+  }
+  __syncthreads();
+  for (int i = tid; i < nrow * d8; i += 128) {  // model.cpp:193-194
+    const int r = i / d8, c = i % d8;
+    uint4 v = *reinterpret_cast<const uint4*>(xs + r * xp + c * 8);
+    const uint4 gv = __ldg(reinterpret_cast<const uint4*>(g) + c);
+    const uint4 bv = __ldg(reinterpret_cast<const uint4*>(b) + c);
+    uint16_t* h = reinterpret_cast<uint16_t*>(&v);
+    const uint16_t* gh = reinterpret_cast<const uint16_t*>(&gv);
+    const uint16_t* bh = reinterpret_cast<const uint16_t*>(&bv);
+    const float mean = st[r], inv = st[ROWS + r];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      h[j] = f2h(__fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(h2f(h[j]), mean), inv), h2f(gh[j])),
+                           h2f(bh[j])));
+    *reinterpret_cast<uint4*>(xn + (r0 + r) * d + c * 8) = v;
+  }
+}
+
 // ========================================================== logits + top-k
 namespace gk {
 constexpr int kThreads = 256;
@@ -518,16 +586,29 @@ static int launch_gk(const GateFusedArgs& a, cudaStream_t st) {
 
 int launch_gate_fused(const GateFusedArgs& a, cudaStream_t st) {
   if (a.T == 0) return MOE_OK;
-  // 1. LayerNorm rows
-  const size_t smem = lnr::smem((int)a.d);
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
-    MOE_CUDA_TRY(cudaFuncSetAttribute(ln_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
-    attr = smem;
+  // 1. LayerNorm rows: latency-bound below ~1 row per SM thread group (f32
+  //    widening + packed ops), issue-bound above (inline conversions, more CTAs)
+  if (a.T <= 2048) {
+    const size_t smem = lnr::smem((int)a.d);
+    static size_t attr = 0;
+    if (smem > 48 * 1024 && smem > attr) {
+      MOE_CUDA_TRY(cudaFuncSetAttribute(ln_rows_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr = smem;
+    }
+    ln_rows_kernel<<<(unsigned)((a.T + lnr::ROWS - 1) / lnr::ROWS), lnr::kThreads, smem, st>>>(
+        a.x, a.T, (int)a.d, a.g, a.b, a.xn);
+  } else {
+    const size_t smem = (size_t)32 * (a.d + 8) * 2 + 64 * 4 + 16;
+    static size_t attr = 0;
+    if (smem > 48 * 1024 && smem > attr) {
+      MOE_CUDA_TRY(cudaFuncSetAttribute(ln_rows_wide_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr = smem;
+    }
+    ln_rows_wide_kernel<<<(unsigned)((a.T + 31) / 32), 128, smem, st>>>(a.x, a.T, (int)a.d, a.g,
+                                                                       a.b, a.xn);
   }
-  ln_rows_kernel<<<(unsigned)((a.T + lnr::ROWS - 1) / lnr::ROWS), lnr::kThreads, smem, st>>>(
-      a.x, a.T, (int)a.d, a.g, a.b, a.xn);
   note_launch();
   const int s1 = check_launch("ln_rows");
   if (s1 != MOE_OK) return s1;

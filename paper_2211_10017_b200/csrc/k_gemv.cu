@@ -24,6 +24,7 @@
 namespace moecu {
 
 namespace gv {
+constexpr int kMaxGemvProblems = 1024;
 constexpr int kWarps = 8;                 // compute warps, 16 features each
 constexpr int kThreads = 32 * (kWarps + 1);  // + one producer warp
 constexpr int NT = 16;  // token rows per pass (2 MMA n-tiles)
@@ -170,11 +171,11 @@ struct Item {
 
 // item order: feature tile fastest, then k-split, then problem -- a CTA's
 // consecutive items share the expert rows it has staged
-__device__ __forceinline__ Item item_at(const Params& P, int i) {
+__device__ __forceinline__ Item item_at(const Params& P, const int* live, int i) {
   Item it;
   it.ft = i % (int)P.nft;
   it.split = (i / (int)P.nft) % P.nsplit;
-  const int p = i / (P.nsplit * (int)P.nft);
+  const int p = live[i / (P.nsplit * (int)P.nft)];
   it.e = P.problems[3 * p];
   it.r0 = P.problems[3 * p + 1];
   it.r1 = P.problems[3 * p + 2];
@@ -198,6 +199,8 @@ __global__ void __launch_bounds__(kThreads, 3) gemv_kernel(const Params P) {
   uint64_t* empty = full + RG::NST;
   uint16_t* xs = reinterpret_cast<uint16_t*>(empty + RG::NST);  // [NT][kp]
   __shared__ uint32_t s_last;
+  __shared__ int s_live[kMaxGemvProblems];  // non-empty problems, in order
+  __shared__ int s_nlive;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int kp = P.kbs_per_split * 64 + 8;  // row pitch of xs (conflict-free fragments)
   if (threadIdx.x == 0) {
@@ -207,7 +210,19 @@ __global__ void __launch_bounds__(kThreads, 3) gemv_kernel(const Params P) {
     }
     fence_barrier_init();
   }
+  if (warp == 0) {  // compact the live problems: work items cover only those
+    int base = 0;
+    for (int p0 = 0; p0 < P.np; p0 += 32) {
+      const int p = p0 + lane;
+      const bool live = p < P.np && P.problems[3 * p + 2] > P.problems[3 * p + 1];
+      const uint32_t m = __ballot_sync(0xffffffffu, live);
+      if (live) s_live[base + __popc(m & ((1u << lane) - 1u))] = p;
+      base += __popc(m);
+    }
+    if (lane == 0) s_nlive = base;
+  }
   __syncthreads();
+  const int nitems = s_nlive * P.nsplit * (int)P.nft;
 
   if (warp == kWarps) {
     // ------------------------------------------------------------- producer
@@ -215,10 +230,10 @@ __global__ void __launch_bounds__(kThreads, 3) gemv_kernel(const Params P) {
       int s = 0;
       uint32_t ph = 0;
       int n = 0;
-      const int ipc = (P.nitems + gridDim.x - 1) / gridDim.x;
-      const int i0 = blockIdx.x * ipc, i1 = min(P.nitems, i0 + ipc);
+      const int i0 = (int)((int64_t)blockIdx.x * nitems / gridDim.x);  // balanced blocks
+      const int i1 = (int)((int64_t)(blockIdx.x + 1) * nitems / gridDim.x);
       for (int i = i0; i < i1; ++i) {
-        const Item it = item_at(P, i);
+        const Item it = item_at(P, s_live, i);
         if (it.r1 <= it.r0) continue;
         const uint8_t* wb = P.tiled + ((it.e * P.nft + it.ft) * P.nkb) * (int64_t)RG::WB;
         const int npass = (int)((it.r1 - it.r0 + NT - 1) / NT);
@@ -239,12 +254,12 @@ __global__ void __launch_bounds__(kThreads, 3) gemv_kernel(const Params P) {
     int s = 0;
     uint32_t ph = 0;
     const int fg = warp * 16 + g;
-    const int ipc = (P.nitems + gridDim.x - 1) / gridDim.x;
-    const int i0 = blockIdx.x * ipc, i1 = min(P.nitems, i0 + ipc);
+    const int i0 = (int)((int64_t)blockIdx.x * nitems / gridDim.x);
+    const int i1 = (int)((int64_t)(blockIdx.x + 1) * nitems / gridDim.x);
     int64_t staged_r = -1;  // first row staged in xs (-1: none)
     int staged_kb = -1;
     for (int i = i0; i < i1; ++i) {
-      const Item it = item_at(P, i);
+      const Item it = item_at(P, s_live, i);
       if (it.r1 <= it.r0) continue;
       const int64_t feat0 = (int64_t)it.ft * 128 + warp * 16;
       float sc[2] = {1.f, 1.f}, bi[2] = {0.f, 0.f};
@@ -434,6 +449,7 @@ static int run_gemv(const GemmArgs& a, const GemvWork& w, cudaStream_t st) {
 
 int launch_gemv(const GemmArgs& a, const GemvWork& w, cudaStream_t st) {
   if (a.np == 0 || a.rows == 0) return MOE_OK;
+  if (a.np > gv::kMaxGemvProblems) return set_error(MOE_EINVAL, "gemv: at most 1024 problems");
   if (a.m % 8 != 0) return set_error(MOE_EINVAL, "gemv: m must be a multiple of 8");
   if (w.nsplit > 1 && (w.part == nullptr || w.ticket == nullptr))
     return set_error(MOE_EINVAL, "gemv: split-K workspace missing");
