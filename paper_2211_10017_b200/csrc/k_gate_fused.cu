@@ -74,10 +74,15 @@ __global__ void __launch_bounds__(lnr::kThreads) ln_rows_kernel(
   }
   __syncthreads();
   if (tid < nrow) {  // model.cpp:178-192, serial
+    // shared loads run two pieces ahead of the dependent adds (LDS latency
+    // would otherwise sit on the chain)
     const float4* row = reinterpret_cast<const float4*>(xf + tid * fp);
     float s = 0.f;
+    float4 c0 = row[0], c1 = row[d4 > 1 ? 1 : 0];
     for (int c = 0; c < d4; ++c) {
-      const float4 v = row[c];
+      const float4 v = c0;
+      c0 = c1;
+      c1 = row[c + 2 < d4 ? c + 2 : c];
       s = __fadd_rn(s, v.x);
       s = __fadd_rn(s, v.y);
       s = __fadd_rn(s, v.z);
@@ -86,8 +91,12 @@ __global__ void __launch_bounds__(lnr::kThreads) ln_rows_kernel(
     const float mean = __fdiv_rn(s, (float)d);
     const float2 m2 = make_float2(mean, mean);
     float v2 = 0.f;
+    c0 = row[0];
+    c1 = row[d4 > 1 ? 1 : 0];
     for (int c = 0; c < d4; ++c) {
-      const float4 v = row[c];
+      const float4 v = c0;
+      c0 = c1;
+      c1 = row[c + 2 < d4 ? c + 2 : c];
       const float2 d01 = f2_sub(make_float2(v.x, v.y), m2);
       const float2 d23 = f2_sub(make_float2(v.z, v.w), m2);
       const float2 q01 = f2_mul(d01, d01), q23 = f2_mul(d23, d23);
@@ -253,7 +262,7 @@ __device__ __forceinline__ float2 ffma2(float a, float2 b, float2 c) {
 }  // namespace gk
 
 template <int EPG, int RPT>
-__global__ void __launch_bounds__(gk::kThreads) gate_topk_kernel(
+__global__ void __launch_bounds__(gk::kThreads, 2) gate_topk_kernel(
     const uint16_t* __restrict__ xn, int64_t T, int d, const float* __restrict__ gw32, int gwp,
     const uint16_t* __restrict__ gb, int E, int k, const uint8_t* __restrict__ finished,
     uint32_t* __restrict__ expert, uint16_t* __restrict__ scale, uint32_t* __restrict__ blockcnt,
@@ -339,48 +348,60 @@ __global__ void __launch_bounds__(gk::kThreads) gate_topk_kernel(
     const float* wg = reinterpret_cast<const float*>(stg + C.xbytes) + (size_t)eg * KC * EPG;
     const int kc = ::min(KC, d - c * KC);
     if (e0 < E) {
-      for (int kk = 0; kk < kc; kk += 8) {
-        // every operand of 8 k-steps first (latency), then the FMAs
-        uint4 xh[RPT];
+      // 4-input steps, operands of step i+1 loaded while step i's FMAs run
+      struct Ops {
+        uint2 xh[RPT];
+        float w[4][EPG];
+      };
+      auto load = [&](Ops& o, int kk) {
 #pragma unroll
         for (int i = 0; i < RPT; ++i)
-          xh[i] = *reinterpret_cast<const uint4*>(xr + i * C.rt * C.xpitch + kk);
-        float wv[8][EPG];
+          o.xh[i] = *reinterpret_cast<const uint2*>(xr + i * C.rt * C.xpitch + kk);
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
+        for (int q = 0; q < 4; ++q) {
           if constexpr (EPG >= 4) {
 #pragma unroll
             for (int j = 0; j < EPG; j += 4) {
               const float4 w4 = *reinterpret_cast<const float4*>(wg + (kk + q) * EPG + j);
-              wv[q][j] = w4.x;
-              wv[q][j + 1] = w4.y;
-              wv[q][j + 2] = w4.z;
-              wv[q][j + 3] = w4.w;
+              o.w[q][j] = w4.x;
+              o.w[q][j + 1] = w4.y;
+              o.w[q][j + 2] = w4.z;
+              o.w[q][j + 3] = w4.w;
             }
           } else {
 #pragma unroll
-            for (int j = 0; j < EPG; ++j) wv[q][j] = wg[(kk + q) * EPG + j];
+            for (int j = 0; j < EPG; ++j) o.w[q][j] = wg[(kk + q) * EPG + j];
           }
         }
+      };
+      auto fma_step = [&](const Ops& o) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
+        for (int q = 0; q < 4; ++q) {
 #pragma unroll
           for (int i = 0; i < RPT; ++i) {
-            const float xq = h2f(reinterpret_cast<const uint16_t*>(&xh[i])[q]);
+            const float xq = h2f(reinterpret_cast<const uint16_t*>(&o.xh[i])[q]);
             if constexpr (EPG >= 2) {
 #pragma unroll
               for (int j = 0; j < NP; ++j)  // exact products, k order kept per chain
-                acc[i][j] = gk::ffma2(xq, make_float2(wv[q][2 * j], wv[q][2 * j + 1]), acc[i][j]);
+                acc[i][j] = gk::ffma2(xq, make_float2(o.w[q][2 * j], o.w[q][2 * j + 1]), acc[i][j]);
             } else {
-              acc[i][0].x = fmaf(xq, wv[q][0], acc[i][0].x);
+              acc[i][0].x = fmaf(xq, o.w[q][0], acc[i][0].x);
             }
           }
         }
+      };
+      Ops a, b;
+      load(a, 0);
+      for (int kk = 0; kk < kc; kk += 8) {
+        load(b, kk + 4);  // kc is a multiple of 8
+        fma_step(a);
+        if (kk + 8 < kc) load(a, kk + 8);
+        fma_step(b);
       }
     }
-    tc += clock64() - tb;
   }
   const long long t_2 = clock64();
+  (void)tc;
   cp_async_wait<0>();
   __syncthreads();  // ring free: reuse as logits / expf buffers
 
@@ -398,54 +419,85 @@ __global__ void __launch_bounds__(gk::kThreads) gate_topk_kernel(
   }
   __syncthreads();
 
-  // ---- top-k selection (routing.cpp:15-31): one warp per row, shuffles
-  for (int r = warp; r < nrow; r += gk::kThreads / 32) {
-    const float* l = lg + r * lp;
-    bool ok = true;
-    for (int j = lane; j < E; j += 32) ok &= isfinite(l[j]);
-    ok = __all_sync(0xffffffffu, ok);
-    if (!ok) {
-      if (lane == 0) {
-        atomicMin(bad_row, (uint32_t)(r0 + r));
-        sel[r * 8] = 0xFFFFFFFFu;
-      }
-      continue;
-    }
-    for (int s = 0; s < k; ++s) {
-      float bv = -INFINITY;
-      int bj = 0x7FFFFFFF;
-      for (int j = lane; j < E; j += 32) {
-        bool taken = false;
-        for (int q = 0; q < s; ++q) taken |= sel[r * 8 + q] == (uint32_t)j;
-        const float v = l[j];
-        if (!taken && (v > bv || bj == 0x7FFFFFFF)) {  // lane-local first maximum
-          bv = v;
-          bj = j;
+  if (E <= 16) {
+    // few experts: one thread per row does the reference's serial selection
+    // (strict '>', index order) and its expf values directly -- no shuffles
+    if (tid < nrow) {
+      const float* l = lg + tid * lp;
+      float* exr = ex + tid * lp;
+      bool ok = true;
+      for (int j = 0; j < E; ++j) ok &= isfinite(l[j]);
+      if (!ok) {
+        atomicMin(bad_row, (uint32_t)(r0 + tid));
+        sel[tid * 8] = 0xFFFFFFFFu;
+      } else {
+        uint32_t taken = 0;  // E <= 16: bitmask
+        for (int s2 = 0; s2 < k; ++s2) {
+          int bj = -1;
+          float bv = 0.f;
+          for (int j = 0; j < E; ++j)
+            if (!((taken >> j) & 1u) && (bj < 0 || l[j] > bv)) {
+              bj = j;
+              bv = l[j];
+            }
+          taken |= 1u << bj;
+          sel[tid * 8 + s2] = (uint32_t)bj;
         }
+        const float mx = l[sel[tid * 8]];
+        for (int j = 0; j < E; ++j) exr[j] = moe_glibc_expf(__fsub_rn(l[j], mx));
       }
+    }
+    __syncthreads();
+  } else {
+    // ---- top-k selection (routing.cpp:15-31): one warp per row, shuffles
+    for (int r = warp; r < nrow; r += gk::kThreads / 32) {
+      const float* l = lg + r * lp;
+      bool ok = true;
+      for (int j = lane; j < E; j += 32) ok &= isfinite(l[j]);
+      ok = __all_sync(0xffffffffu, ok);
+      if (!ok) {
+        if (lane == 0) {
+          atomicMin(bad_row, (uint32_t)(r0 + r));
+          sel[r * 8] = 0xFFFFFFFFu;
+        }
+        continue;
+      }
+      for (int s = 0; s < k; ++s) {
+        float bv = -INFINITY;
+        int bj = 0x7FFFFFFF;
+        for (int j = lane; j < E; j += 32) {
+          bool taken = false;
+          for (int q = 0; q < s; ++q) taken |= sel[r * 8 + q] == (uint32_t)j;
+          const float v = l[j];
+          if (!taken && (v > bv || bj == 0x7FFFFFFF)) {  // lane-local first maximum
+            bv = v;
+            bj = j;
+          }
+        }
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
-        if (oj != 0x7FFFFFFF && (bj == 0x7FFFFFFF || ov > bv || (ov == bv && oj < bj))) {
-          bv = ov;
-          bj = oj;
+        for (int o = 16; o > 0; o >>= 1) {
+          const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+          const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+          if (oj != 0x7FFFFFFF && (bj == 0x7FFFFFFF || ov > bv || (ov == bv && oj < bj))) {
+            bv = ov;
+            bj = oj;
+          }
         }
+        if (lane == 0) sel[r * 8 + s] = (uint32_t)bj;
+        __syncwarp();
       }
-      if (lane == 0) sel[r * 8 + s] = (uint32_t)bj;
-      __syncwarp();
     }
+    __syncthreads();
+    // expf(l_j - mx) for every (row, expert) in parallel (routing.cpp:34)
+    for (int i = tid; i < nrow * E; i += gk::kThreads) {
+      const int r = i / E, j = i % E;
+      const uint32_t s0 = sel[r * 8];
+      if (s0 == 0xFFFFFFFFu) continue;
+      const float* l = lg + r * lp;
+      ex[r * lp + j] = moe_glibc_expf(__fsub_rn(l[j], l[s0]));
+    }
+    __syncthreads();
   }
-  __syncthreads();
-  // expf(l_j - mx) for every (row, expert) in parallel (routing.cpp:34)
-  for (int i = tid; i < nrow * E; i += gk::kThreads) {
-    const int r = i / E, j = i % E;
-    const uint32_t s0 = sel[r * 8];
-    if (s0 == 0xFFFFFFFFu) continue;
-    const float* l = lg + r * lp;
-    ex[r * lp + j] = moe_glibc_expf(__fsub_rn(l[j], l[s0]));
-  }
-  __syncthreads();
   // serial sum in expert order, scales, routing keys (routing.cpp:33-38, 55-62)
   if (tid < nrow) {
     const int r = tid;

@@ -63,7 +63,9 @@ struct Cfg {
   static constexpr int STAGE = BBYTES + WBYTES;
   static constexpr int EPI_WBUF = 32 * 32 * 2;                   // per warp: [32][32] fp16
   static constexpr int EPI = kEpiGroups * 4 * EPI_WBUF;
-  static constexpr int NA = 2;                                   // A stages
+  // A stages: TS keeps as many 32-column stages as TMEM leaves beside the
+  // accumulators (each dequant group then has >= 2 stages to run ahead)
+  static constexpr int NA = TS ? ((512 - 2 * BN) / 32 >= 4 ? 4 : 2) : 2;
   static constexpr int BUDGET = 220 * 1024 - EPI - NA * ABYTES;  // TMA stages
   static constexpr int NS0 = BUDGET / STAGE;
   static constexpr int NS = NS0 > 8 ? 8 : NS0;                   // TMA stages
@@ -87,9 +89,12 @@ struct Tile {
   int64_t e, r0, r1, row0, ft;
 };
 
+// t indexes (token tile, feature-tile group of CL); CTA `rank` of a CL-CTA
+// cluster takes feature tile group*CL + rank of the same token tile
 __device__ __forceinline__ Tile decode(const uint32_t* table, int np, const uint32_t* problems,
-                                       uint32_t t, int64_t nft, int BN) {
-  const uint32_t g = t / (uint32_t)nft;  // global token-tile index
+                                       uint32_t t, int64_t nftg, int BN, int CL = 1,
+                                       int rank = 0) {
+  const uint32_t g = t / (uint32_t)nftg;  // global token-tile index
   int lo = 0, hi = np - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
@@ -101,7 +106,7 @@ __device__ __forceinline__ Tile decode(const uint32_t* table, int np, const uint
   x.r0 = problems[3 * lo + 1];
   x.r1 = problems[3 * lo + 2];
   x.row0 = x.r0 + (int64_t)(g - table[lo]) * BN;
-  x.ft = t % (uint32_t)nft;
+  x.ft = (int64_t)(t % (uint32_t)nftg) * CL + rank;
   return x;
 }
 
@@ -131,11 +136,19 @@ constexpr int kTraceN = 1024;  // events per role slot
       P.trace[(slot) * kTraceN + (idx)] = clock64();                             \
   } while (0)
 
-template <int BITS, int BN, bool TS>
+// CL = 2: CTA pairs (a cluster) work on the same token tile and adjacent
+// feature tiles; each CTA TMA-loads half of the activation tile and
+// multicasts it to both, halving the L2 -> SM traffic of the B operand (the
+// kernel is L2-bandwidth-bound with 128-feature tiles otherwise).  A stage is
+// refilled only after both CTAs' MMAs released it (empty counts 2 commits).
+template <int BITS, int BN, bool TS, int CL>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ OutMaps O,
                    const Params P) {
   using C = Cfg<BITS, BN, TS>;
+  const int rank = CL > 1 ? (int)cluster_ctarank() : 0;
+  const uint32_t cid = blockIdx.x / CL, ncl = gridDim.x / CL;  // cluster id / count
+  const int64_t nftg = P.nft / CL;                               // feature-tile groups
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte alignment for the 128B-swizzle atoms, by pointer arithmetic on
   // the shared array so the compiler keeps shared-space (LDS/STS) accesses.
@@ -159,7 +172,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       for (int i = 0; i < C::NS; ++i) {
         mbar_init(&full[i], 1);
-        mbar_init(&empty[i], 1);
+        mbar_init(&empty[i], CL);  // every CTA of the cluster releases the stage
       }
       for (int i = 0; i < C::NA; ++i) {
         mbar_init(&afull[i], 4);
@@ -192,16 +205,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (CL > 1) cluster_sync_all();  // peers' barriers exist before any multicast
   tc_fence_after();
   const uint32_t tmem = *tmem_ptr;
-  const uint32_t ntiles = table[np] * (uint32_t)P.nft;
+  const uint32_t ntiles = table[np] * (uint32_t)nftg;
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
       uint32_t it = 0;
-      for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const Tile T = decode(table, np, P.problems, t, P.nft, BN);
+      for (uint32_t t = cid; t < ntiles; t += ncl) {
+        const Tile T = decode(table, np, P.problems, t, nftg, BN, CL, rank);
         const uint8_t* wsrc = P.tiled + ((T.e * P.nft + T.ft) * P.nkb) * (int64_t)C::WBYTES;
         for (int64_t kb = 0; kb < P.nkb; ++kb, ++it) {
           const int s = it % C::NS;
@@ -209,7 +223,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           TC_TRACE(0, it);
           uint8_t* sb = smem + s * C::STAGE;
           mbar_arrive_expect_tx(&full[s], (P.dbg & 4) ? C::BBYTES : C::STAGE);
-          tma_load_2d(sb, &tmap_x, &full[s], (int)(kb * 64), (int)T.row0);
+          if constexpr (CL > 1)  // my half of the token rows, to every CTA of the pair
+            tma_load_2d_mc(sb + rank * (C::BBYTES / CL), &tmap_x, &full[s], (int)(kb * 64),
+                           (int)(T.row0 + rank * (BN / CL)), (uint16_t)((1u << CL) - 1));
+          else
+            tma_load_2d(sb, &tmap_x, &full[s], (int)(kb * 64), (int)T.row0);
           if (!(P.dbg & 4)) bulk_load(sb + C::BBYTES, wsrc + kb * C::WBYTES, C::WBYTES, &full[s]);
         }
       }
@@ -220,11 +238,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       const uint32_t smem_base = smem_u32(smem);
       uint32_t it = 0, local = 0;
-      for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
+      for (uint32_t t = cid; t < ntiles; t += ncl, ++local) {
         const int acc = local & 1;
         // a problem's last token tile is usually partial: the MMA N follows
         // the live rows (multiple of 16) so padding costs no tensor time
-        const Tile Tt = decode(table, np, P.problems, t, P.nft, BN);
+        const Tile Tt = decode(table, np, P.problems, t, nftg, BN, CL, rank);
         const int64_t live = Tt.r1 - Tt.row0;
         const int nmma = live >= BN ? BN : (int)((live + 15) / 16 * 16);
         const uint32_t idesc = umma_idesc_f16(128, nmma);
@@ -252,7 +270,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               tc_mma_ss(d_tmem, adesc + (uint64_t)(kk * 2), bdesc + (uint64_t)(kk * 2), idesc,
                         (kb | kk) != 0 ? 1u : 0u);
           }
-          tc_commit(&empty[s]);
+          if constexpr (CL > 1)
+            tc_commit_mc(&empty[s], (uint16_t)((1u << CL) - 1));  // stage reads done here
+          else
+            tc_commit(&empty[s]);
           tc_commit(&aempty[a]);
           TC_TRACE(3, it);
         }
@@ -267,7 +288,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = (warp - 4) & 3, grp = (warp - 4) >> 2;
     const int feat = q * 32 + lane;
     uint32_t it = 0;
-    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    for (uint32_t t = cid; t < ntiles; t += ncl) {
       for (int64_t kb = 0; kb < P.nkb; ++kb, ++it) {
         if ((int)(it % kDqGroups) != grp) continue;
         const int s = it % C::NS, a = it % C::NA;
@@ -340,9 +361,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint16_t* stage0 = reinterpret_cast<uint16_t*>(smem + C::OFF_EPI + ew * C::EPI_WBUF);
     uint32_t cc = 0;  // chunks processed by this warp
     uint32_t local = 0;
-    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
+    for (uint32_t t = cid; t < ntiles; t += ncl, ++local) {
       const int acc = local & 1;
-      const Tile T = decode(table, np, P.problems, t, P.nft, BN);
+      const Tile T = decode(table, np, P.problems, t, nftg, BN, CL, rank);
       const int64_t col = T.ft * 128 + q * 32 + lane;
       float sc = 1.0f, bi = 0.0f;
       if (col < P.n) {
@@ -404,6 +425,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (CL > 1) cluster_sync_all();  // no peer multicast / arrive still in flight
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
@@ -425,7 +447,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-template <int BITS, int BN, bool TS>
+template <int BITS, int BN, bool TS, int CL = 1>
 static int run_tc(const GemmArgs& a, cudaStream_t st) {
   using C = tc::Cfg<BITS, BN, TS>;
   auto encode = get_encode();
@@ -433,7 +455,7 @@ static int run_tc(const GemmArgs& a, cudaStream_t st) {
   CUtensorMap tmap;
   const cuuint64_t dims[2] = {(cuuint64_t)a.m, (cuuint64_t)a.rows};
   const cuuint64_t strides[1] = {(cuuint64_t)a.m * 2};
-  const cuuint32_t box[2] = {64, (cuuint32_t)BN};
+  const cuuint32_t box[2] = {64, (cuuint32_t)(BN / CL)};
   const cuuint32_t estr[2] = {1, 1};
   CUresult r = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<uint16_t*>(a.x), dims,
                       strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -472,7 +494,7 @@ static int run_tc(const GemmArgs& a, cudaStream_t st) {
   }
   static bool attr_set = false;
   if (!attr_set) {
-    MOE_CUDA_TRY(cudaFuncSetAttribute(tc::gemm_tc_kernel<BITS, BN, TS>,
+    MOE_CUDA_TRY(cudaFuncSetAttribute(tc::gemm_tc_kernel<BITS, BN, TS, CL>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr_set = true;
   }
@@ -481,7 +503,23 @@ static int run_tc(const GemmArgs& a, cudaStream_t st) {
   P.dbg = std::getenv("MOE_TC_DBG") ? std::atoi(std::getenv("MOE_TC_DBG")) : 0;
   if (trace_path) MOE_CUDA_TRY(cudaMalloc(&P.trace, 12 * tc::kTraceN * 8));
   if (P.trace) MOE_CUDA_TRY(cudaMemset(P.trace, 0, 12 * tc::kTraceN * 8));
-  tc::gemm_tc_kernel<BITS, BN, TS><<<sm_count(), tc::kThreads, C::SMEM, st>>>(tmap, O, P);
+  if constexpr (CL > 1) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(sm_count() / CL * CL));
+    cfg.blockDim = dim3(tc::kThreads);
+    cfg.dynamicSmemBytes = C::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    MOE_CUDA_TRY(cudaLaunchKernelEx(&cfg, tc::gemm_tc_kernel<BITS, BN, TS, CL>, tmap, O, P));
+  } else {
+    tc::gemm_tc_kernel<BITS, BN, TS, CL><<<sm_count(), tc::kThreads, C::SMEM, st>>>(tmap, O, P);
+  }
   note_launch();
   const int rc = check_launch("gemm_tc");
   if (P.trace) {
@@ -510,6 +548,13 @@ static int run_tc_bits(const GemmArgs& a, cudaStream_t st) {
   if (a.rows_hint >= 160) {
     const int64_t tiles256 = a.np * ((a.rows_hint + 255) / 256) * nft;
     if (tiles256 <= sm_count()) return run_tc<BITS, 256, false>(a, st);
+    static const int force = std::getenv("MOE_TC_BN") ? std::atoi(std::getenv("MOE_TC_BN")) : 0;
+    if (force == 192) return run_tc<BITS, 192, true>(a, st);  // dev experiments
+    if (force == 256) return run_tc<BITS, 256, false>(a, st);
+    // CTA pairs multicasting the activation tile (MOE_TC_CL=2): measured no
+    // faster than single CTAs on B200 (the per-SM fill, not L2, is the limit)
+    static const bool pair = std::getenv("MOE_TC_CL") && std::atoi(std::getenv("MOE_TC_CL")) == 2;
+    if (pair && nft % 2 == 0) return run_tc<BITS, 224, true, 2>(a, st);
     return run_tc<BITS, 224, true>(a, st);
   }
   if (a.rows_hint >= 96) return run_tc<BITS, 128, true>(a, st);

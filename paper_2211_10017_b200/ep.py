@@ -79,11 +79,13 @@ class DistComm:
         self.dist, self.group = dist, group
         self.world = dist.get_world_size(group)
 
-    def all_to_all(self, sends, send_splits, recv_splits):
-        """sends: [tensor (sum(send_splits), ...)] for the one local rank."""
+    def all_to_all(self, sends, send_splits, recv_splits, outs=None):
+        """sends: [tensor (sum(send_splits), ...)] for the one local rank;
+        outs (optional): [preallocated receive tensor] (e.g. a layer buffer)."""
         import torch
         (x,), (ss,), (rs,) = sends, send_splits, recv_splits
-        out = torch.empty((int(sum(rs)),) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
+        out = outs[0] if outs is not None else torch.empty(
+            (int(sum(rs)),) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
         self.dist.all_to_all_single(out, x.contiguous(), [int(v) for v in rs],
                                     [int(v) for v in ss], group=self.group)
         return [out]
@@ -96,14 +98,20 @@ class LoopbackComm:
     def __init__(self, world):
         self.world = world
 
-    def all_to_all(self, sends, send_splits, recv_splits):
+    def all_to_all(self, sends, send_splits, recv_splits, outs=None):
         import torch
         G = self.world
         seg = []
         for g in range(G):
             cuts = np.concatenate([[0], np.cumsum(send_splits[g])]).astype(np.int64)
             seg.append([sends[g][int(cuts[j]):int(cuts[j + 1])] for j in range(G)])
-        return [torch.cat([seg[src][dst] for src in range(G)], 0) for dst in range(G)]
+        res = [torch.cat([seg[src][dst] for src in range(G)], 0) for dst in range(G)]
+        if outs is not None:
+            for o, r in zip(outs, res):
+                if o is not None and r.shape[0]:
+                    o.copy_(r)
+            return outs
+        return res
 
 
 # ------------------------------------------------------------------ compute
@@ -196,15 +204,10 @@ def ep_forward(ranks, comm, xs, fins, k=1, mode=1):
         xe = ranks[i].gather(xrecv[i], perm)
         ye = ranks[i].experts(xe, probs, mode)
         yrecv.append(ranks[i].gather(ye, inverse(perm)))
-    # 6. reverse all-to-all into each rank's sorted y, then local combine
-    yback = comm.all_to_all(yrecv, recv_rows, send_rows)
-    outs = []
-    for i in range(n):
-        ysorted = ranks[i].y_rows(active[i])
-        if active[i]:
-            ysorted.copy_(yback[i])
-        outs.append(ranks[i].combine(xs[i], fins[i], k, ysorted))
-    return outs
+    # 6. reverse all-to-all straight into each rank's sorted y, then local combine
+    ys = [ranks[i].y_rows(active[i]) for i in range(n)]
+    comm.all_to_all(yrecv, recv_rows, send_rows, outs=ys)
+    return [ranks[i].combine(xs[i], fins[i], k, ys[i]) for i in range(n)]
 
 
 class EPMoELayer:

@@ -1,0 +1,6 @@
+timeout 300 python -m pytest tests/test_gpu_kernels.py -x -q -m gpu -k "gemm_fast or gemm_exact" 2>&1 | tail -3
+timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+for w in c2 c4; do timeout 300 python bench.py --workload $w --steps 60 --warmup 5 --no-cpu-baseline 2>&1 | tail -1 | python3 -c "
+import sys,json; j=json.loads(sys.stdin.read()); print(j['config']['workload'][:30], 'us=%.1f'%(1e3*j['ms_per_step']), 'gemm_us=%.1f'%(1e3*j['roofline']['kernel_ms_per_step']), 'frac=%.3f'%j['roofline']['frac'])"; done
+for w in c2 c4; do MOE_TC_BN=1 timeout 300 python bench.py --workload $w --steps 60 --warmup 5 --no-cpu-baseline 2>&1 | tail -1 | python3 -c "
+import sys,json; j=json.loads(sys.stdin.read()); print('CL=1', j['config']['workload'][:30], 'us=%.1f'%(1e3*j['ms_per_step']), 'gemm_us=%.1f'%(1e3*j['roofline']['kernel_ms_per_step']), 'frac=%.3f'%j['roofline']['frac'])"; done

@@ -45,12 +45,8 @@ class OracleRank:
         return _t(self.xp[:n])
 
     def y_rows(self, n):
-        outer = self
-
-        class View:
-            def copy_(self, src):
-                outer.y[:n] = src.numpy().view(np.float16)
-        return View()
+        # a tensor aliasing the sorted-y buffer: the reverse all-to-all lands in it
+        return torch.from_numpy(self.y[:n].view(np.int16)).view(torch.float16)
 
     def gather(self, x, idx):
         return x[torch.as_tensor(idx)]
