@@ -24,6 +24,7 @@
 //   plan_scan (k_route.cu), whose blocks are this kernel's RB*k slots.
 #include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "kernels.cuh"
 
@@ -43,9 +44,25 @@ __host__ __device__ inline size_t smem(int d) {
 }
 }  // namespace lnr
 
+// dev-only timing (MOE_GATE_TRACE): per-CTA [start, end] global time (ns)
+// and CTA 0's phase clocks
+__device__ __forceinline__ long long gtime() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define LN_TRACE(i)                                                            \
+  do {                                                                         \
+    if (trace != nullptr && tid == 0) {                                        \
+      if ((i) == 0) trace[16 + 2 * blockIdx.x] = gtime();                      \
+      if ((i) == 3) trace[16 + 2 * blockIdx.x + 1] = gtime();                  \
+      if (blockIdx.x == 0) trace[i] = clock64();                               \
+    }                                                                          \
+  } while (0)
+
 __global__ void __launch_bounds__(lnr::kThreads) ln_rows_kernel(
     const uint16_t* __restrict__ x, int64_t T, int d, const uint16_t* __restrict__ g,
-    const uint16_t* __restrict__ b, uint16_t* __restrict__ xn) {
+    const uint16_t* __restrict__ b, uint16_t* __restrict__ xn, long long* trace) {
   extern __shared__ __align__(16) uint8_t sm[];
   const int xp = d + 8, fp = d + 4;
   uint16_t* xs = reinterpret_cast<uint16_t*>(sm);
@@ -56,14 +73,20 @@ __global__ void __launch_bounds__(lnr::kThreads) ln_rows_kernel(
   const int64_t r0 = (int64_t)blockIdx.x * lnr::ROWS;
   const int nrow = (int)::min((int64_t)lnr::ROWS, T - r0);
   const int d8 = d / 8, d4 = d / 4;
-  if (tid == 0) {
-    mbar_init(bar, 1);
-    fence_barrier_init();
-    mbar_arrive_expect_tx(bar, (uint32_t)nrow * d * 2);
-    for (int r = 0; r < nrow; ++r) bulk_load(xs + r * xp, x + (r0 + r) * d, (uint32_t)d * 2, bar);
+  if (tid < 32) {  // warp 0 converged, one elected lane issues (uniform copy operands)
+    if (elect_one()) {
+      mbar_init(bar, 1);
+      fence_barrier_init();
+      mbar_arrive_expect_tx(bar, (uint32_t)nrow * d * 2);
+    }
+    __syncwarp();
+    for (int r = 0; r < nrow; ++r)
+      if (elect_one()) bulk_load(xs + r * xp, x + (r0 + r) * d, (uint32_t)d * 2, bar);
   }
+  LN_TRACE(0);
   __syncthreads();
   mbar_wait(bar, 0);
+  LN_TRACE(1);
   for (int i = tid; i < nrow * d8; i += lnr::kThreads) {  // widen (exact)
     const int r = i / d8, c = i % d8;
     const uint4 v = *reinterpret_cast<const uint4*>(xs + r * xp + c * 8);
@@ -109,6 +132,7 @@ __global__ void __launch_bounds__(lnr::kThreads) ln_rows_kernel(
     st[lnr::ROWS + tid] = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(v2, (float)d), 1e-5f)));
   }
   __syncthreads();
+  LN_TRACE(2);
   for (int i = tid; i < nrow * d8; i += lnr::kThreads) {  // model.cpp:193-194
     const int r = i / d8, c = i % d8;
     const float4* src = reinterpret_cast<const float4*>(xf + r * fp + c * 8);
@@ -135,13 +159,14 @@ __global__ void __launch_bounds__(lnr::kThreads) ln_rows_kernel(
     }
     *reinterpret_cast<uint4*>(xn + (r0 + r) * d + c * 8) = o;
   }
+  LN_TRACE(3);
 }
 
 // Large-T form: 32 rows per CTA, conversions inline (higher occupancy; the
 // kernel is issue-bound there, not latency-bound).
 __global__ void __launch_bounds__(128) ln_rows_wide_kernel(
     const uint16_t* __restrict__ x, int64_t T, int d, const uint16_t* __restrict__ g,
-    const uint16_t* __restrict__ b, uint16_t* __restrict__ xn) {
+    const uint16_t* __restrict__ b, uint16_t* __restrict__ xn, long long* trace) {
   constexpr int ROWS = 32;
   extern __shared__ __align__(16) uint8_t sm[];
   const int xp = d + 8;
@@ -152,14 +177,20 @@ __global__ void __launch_bounds__(128) ln_rows_wide_kernel(
   const int64_t r0 = (int64_t)blockIdx.x * ROWS;
   const int nrow = (int)::min((int64_t)ROWS, T - r0);
   const int d8 = d / 8;
-  if (tid == 0) {
-    mbar_init(bar, 1);
-    fence_barrier_init();
-    mbar_arrive_expect_tx(bar, (uint32_t)nrow * d * 2);
-    for (int r = 0; r < nrow; ++r) bulk_load(xs + r * xp, x + (r0 + r) * d, (uint32_t)d * 2, bar);
+  if (tid < 32) {  // warp 0 converged, one elected lane issues (uniform copy operands)
+    if (elect_one()) {
+      mbar_init(bar, 1);
+      fence_barrier_init();
+      mbar_arrive_expect_tx(bar, (uint32_t)nrow * d * 2);
+    }
+    __syncwarp();
+    for (int r = 0; r < nrow; ++r)
+      if (elect_one()) bulk_load(xs + r * xp, x + (r0 + r) * d, (uint32_t)d * 2, bar);
   }
+  LN_TRACE(0);
   __syncthreads();
   mbar_wait(bar, 0);
+  LN_TRACE(1);
   if (tid < nrow) {  // model.cpp:178-192, serial
     const uint4* row = reinterpret_cast<const uint4*>(xs + tid * xp);
     float s = 0.f;
@@ -188,6 +219,7 @@ __global__ void __launch_bounds__(128) ln_rows_wide_kernel(
     st[ROWS + tid] = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(v2, (float)d), 1e-5f)));
   }
   __syncthreads();
+  LN_TRACE(2);
   for (int i = tid; i < nrow * d8; i += 128) {  // model.cpp:193-194
     const int r = i / d8, c = i % d8;
     uint4 v = *reinterpret_cast<const uint4*>(xs + r * xp + c * 8);
@@ -203,6 +235,7 @@ __global__ void __launch_bounds__(128) ln_rows_wide_kernel(
                            h2f(bh[j])));
     *reinterpret_cast<uint4*>(xn + (r0 + r) * d + c * 8) = v;
   }
+  LN_TRACE(3);
 }
 
 // ========================================================== logits + top-k
@@ -270,6 +303,7 @@ __global__ void __launch_bounds__(gk::kThreads, 2) gate_topk_kernel(
   extern __shared__ __align__(16) uint8_t sm[];
   const gk::Cfg C = gk::cfg(E, gwp, EPG, RPT);
   long long tw = 0, tc = 0, t_0 = clock64();  // dev-only phase trace (MOE_GATE_TRACE)
+  if (trace != nullptr && threadIdx.x == 0) trace[16 + 2 * blockIdx.x] = gtime();
   uint32_t* sel = reinterpret_cast<uint32_t*>(sm + C.body);  // [rb][8]
   uint32_t* hist = sel + C.rb * 8;
 
@@ -524,6 +558,7 @@ __global__ void __launch_bounds__(gk::kThreads, 2) gate_topk_kernel(
   }
   __syncthreads();
   for (int i = tid; i <= E; i += gk::kThreads) blockcnt[(int64_t)i * gridDim.x + blockIdx.x] = hist[i];
+  if (trace != nullptr && tid == 0) trace[16 + 2 * blockIdx.x + 1] = gtime();
   if (trace != nullptr && blockIdx.x == 0 && tid == 0) {
     trace[0] = t_1 - t_0;  // prologue (first issues)
     trace[1] = tw;         // chunk waits + barriers
@@ -551,7 +586,7 @@ int launch_widen_gate(const uint16_t* gw, int64_t d, int64_t E, int64_t gwp, flo
   return check_launch("widen_gate");
 }
 
-int64_t gate_fused_pitch(int64_t E) { return (E + 3) / 4 * 4; }
+int64_t gate_fused_pitch(int64_t E) { return (E + 7) / 8 * 8; }  // EPG <= 8 groups stay in-row
 
 // copy descriptors of a config fit the per-thread register arrays
 static bool copies_fit(int64_t E, int epg, const gk::Cfg& c) {
@@ -621,23 +656,55 @@ static int launch_gk(const GateFusedArgs& a, cudaStream_t st) {
     attr = C.total;
   }
   const unsigned grid = (unsigned)((a.T + C.rb - 1) / C.rb);
-  static long long* trace = nullptr;
+  static long long* dtrace = nullptr;
   const bool tr = std::getenv("MOE_GATE_TRACE") != nullptr;
-  if (tr && !trace) MOE_CUDA_TRY(cudaMallocManaged(&trace, 8 * 8));
+  if (tr && !dtrace) MOE_CUDA_TRY(cudaMalloc(&dtrace, 8 * (16 + 2 * 65536)));
   gate_topk_kernel<EPG, RPT><<<grid, gk::kThreads, C.total, st>>>(
       a.xn, a.T, (int)a.d, a.gw32, (int)a.gwp, a.gb, (int)a.E, a.k, a.finished, a.expert,
-      a.scale, a.blockcnt, a.bad_row, tr ? trace : nullptr);
+      a.scale, a.blockcnt, a.bad_row, tr ? dtrace : nullptr);
   note_launch();
   if (tr) {
+    static std::vector<long long> hv;
+    hv.assign(16 + 2 * grid, 0);
     cudaStreamSynchronize(st);
-    std::fprintf(stderr, "gate_trace EPG=%d RPT=%d grid=%u rb=%d kc=%d: pro=%lld wait=%lld comp=%lld loop=%lld tail=%lld nch=%lld\n",
-                 EPG, RPT, grid, C.rb, C.kc, trace[0], trace[1], trace[2], trace[3], trace[4], trace[5]);
+    cudaMemcpy(hv.data(), dtrace, hv.size() * 8, cudaMemcpyDeviceToHost);
+    const long long* trace = hv.data();
+    long long lo = trace[16], hi = trace[17], sum = 0, mx = 0;
+    for (unsigned i = 0; i < grid; ++i) {
+      lo = std::min(lo, trace[16 + 2 * i]);
+      hi = std::max(hi, trace[16 + 2 * i + 1]);
+      sum += trace[16 + 2 * i + 1] - trace[16 + 2 * i];
+      mx = std::max(mx, trace[16 + 2 * i + 1] - trace[16 + 2 * i]);
+    }
+    std::fprintf(stderr, "gate_trace EPG=%d RPT=%d grid=%u rb=%d kc=%d: span=%lld ns cta mean=%lld max=%lld ns; cta0 clocks pro=%lld wait=%lld loop=%lld tail=%lld nch=%lld\n",
+                 EPG, RPT, grid, C.rb, C.kc, hi - lo, sum / grid, mx, trace[0], trace[1], trace[3], trace[4], trace[5]);
   }
   return check_launch("gate_topk");
 }
 
+// dev-only: summarise an LN trace (per-CTA global-time spans, CTA 0 phases)
+static void ln_trace_report(long long* dtr, unsigned grid, const char* name) {
+  static std::vector<long long> h;
+  h.assign(16 + 2 * grid, 0);
+  cudaDeviceSynchronize();
+  cudaMemcpy(h.data(), dtr, h.size() * 8, cudaMemcpyDeviceToHost);
+  const long long* tr = h.data();
+  long long lo = tr[16], hi = tr[17], sum = 0, mx = 0;
+  for (unsigned i = 0; i < grid; ++i) {
+    lo = std::min(lo, tr[16 + 2 * i]);
+    hi = std::max(hi, tr[16 + 2 * i + 1]);
+    sum += tr[16 + 2 * i + 1] - tr[16 + 2 * i];
+    mx = std::max(mx, tr[16 + 2 * i + 1] - tr[16 + 2 * i]);
+  }
+  std::fprintf(stderr, "ln_trace %s grid=%u: span=%lld ns cta mean=%lld max=%lld ns; cta0 clocks load=%lld chains=%lld norm=%lld\n",
+               name, grid, hi - lo, sum / grid, mx, tr[1] - tr[0], tr[2] - tr[1], tr[3] - tr[2]);
+}
+
 int launch_gate_fused(const GateFusedArgs& a, cudaStream_t st) {
   if (a.T == 0) return MOE_OK;
+  static long long* ltr = nullptr;
+  const bool ltrace = std::getenv("MOE_GATE_TRACE") != nullptr;
+  if (ltrace && !ltr) MOE_CUDA_TRY(cudaMalloc(&ltr, 8 * (16 + 2 * 65536)));
   // 1. LayerNorm rows: latency-bound below ~1 row per SM thread group (f32
   //    widening + packed ops), issue-bound above (inline conversions, more CTAs)
   if (a.T <= 2048) {
@@ -648,8 +715,10 @@ int launch_gate_fused(const GateFusedArgs& a, cudaStream_t st) {
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       attr = smem;
     }
-    ln_rows_kernel<<<(unsigned)((a.T + lnr::ROWS - 1) / lnr::ROWS), lnr::kThreads, smem, st>>>(
-        a.x, a.T, (int)a.d, a.g, a.b, a.xn);
+    const unsigned grid = (unsigned)((a.T + lnr::ROWS - 1) / lnr::ROWS);
+    ln_rows_kernel<<<grid, lnr::kThreads, smem, st>>>(a.x, a.T, (int)a.d, a.g, a.b, a.xn,
+                                                      ltrace ? ltr : nullptr);
+    if (ltrace) ln_trace_report(ltr, grid, "ln_rows");
   } else {
     const size_t smem = (size_t)32 * (a.d + 8) * 2 + 64 * 4 + 16;
     static size_t attr = 0;
@@ -658,8 +727,10 @@ int launch_gate_fused(const GateFusedArgs& a, cudaStream_t st) {
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       attr = smem;
     }
-    ln_rows_wide_kernel<<<(unsigned)((a.T + 31) / 32), 128, smem, st>>>(a.x, a.T, (int)a.d, a.g,
-                                                                       a.b, a.xn);
+    const unsigned grid = (unsigned)((a.T + 31) / 32);
+    ln_rows_wide_kernel<<<grid, 128, smem, st>>>(a.x, a.T, (int)a.d, a.g, a.b, a.xn,
+                                                 ltrace ? ltr : nullptr);
+    if (ltrace) ln_trace_report(ltr, grid, "ln_rows_wide");
   }
   note_launch();
   const int s1 = check_launch("ln_rows");

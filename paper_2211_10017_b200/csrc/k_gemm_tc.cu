@@ -55,10 +55,10 @@ constexpr int kMaxProblems = 1024;
 // TS = true: A (dequantised weights) in TMEM, 2 x BN accumulator columns
 // (BN <= 224).  TS = false: A in shared memory (SS MMA), which frees TMEM for
 // two 256-column accumulators -- chosen when 256-token tiles fit one wave.
-template <int BITS, int BN, bool TS>
+template <int BITS, int BN, bool TS, int CL = 1>
 struct Cfg {
   static constexpr int WBYTES = wblock_bytes(BITS);
-  static constexpr int BBYTES = BN * 128;   // BN rows x 64 fp16
+  static constexpr int BBYTES = BN / CL * 128;   // this CTA's BN / CL rows x 64 fp16
   static constexpr int ABYTES = TS ? 0 : 128 * 128;  // SS: 128 features x 64 fp16 per A stage
   static constexpr int STAGE = BBYTES + WBYTES;
   static constexpr int EPI_WBUF = 32 * 32 * 2;                   // per warp: [32][32] fp16
@@ -110,6 +110,15 @@ __device__ __forceinline__ Tile decode(const uint32_t* table, int np, const uint
   return x;
 }
 
+// MMA N of a tile: a problem's last token tile is usually partial, so N
+// follows its live rows (multiple of 16: the pair form splits N in halves of
+// whole 8-row swizzle atoms) and padding costs no tensor time
+template <int BN, int CL>
+__device__ __forceinline__ int tile_n(const Tile& T) {
+  const int64_t live = T.r1 - T.row0;
+  return live >= BN ? BN : (int)((live + 15) / 16 * 16);
+}
+
 // Output tensor maps: box {32 features, 32 >> i rows}, i = 0..5.
 struct OutMaps {
   CUtensorMap map[6];
@@ -136,16 +145,22 @@ constexpr int kTraceN = 1024;  // events per role slot
       P.trace[(slot) * kTraceN + (idx)] = clock64();                             \
   } while (0)
 
-// CL = 2: CTA pairs (a cluster) work on the same token tile and adjacent
-// feature tiles; each CTA TMA-loads half of the activation tile and
-// multicasts it to both, halving the L2 -> SM traffic of the B operand (the
-// kernel is L2-bandwidth-bound with 128-feature tiles otherwise).  A stage is
-// refilled only after both CTAs' MMAs released it (empty counts 2 commits).
+// CL = 2: CTA pairs (a 2-CTA cluster on one TPC) run cta_group::2 MMAs of
+// M = 256 features x N = BN tokens.  Each CTA dequantises its own 128
+// features (adjacent feature tiles) into its own A stage and TMA-loads HALF
+// of the token tile (columns [0, N/2) in rank 0, [N/2, N) in rank 1, same
+// shared-memory offset); rank 0's thread issues the MMA for both.  Versus
+// single CTAs this halves each SM's activation fill and shared-memory reads
+// and halves the MMA instructions per output -- the two limits measured on
+// the single-CTA kernel.  Barriers the MMA waits on live in
+// rank 0: `full` counts both halves' TMA bytes, `afull` / `tempty` take the
+// peer's dequant / epilogue arrivals remotely; commits multicast to both.
 template <int BITS, int BN, bool TS, int CL>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ OutMaps O,
                    const Params P) {
-  using C = Cfg<BITS, BN, TS>;
+  using C = Cfg<BITS, BN, TS, CL>;
+  constexpr bool PAIR = CL == 2;
   const int rank = CL > 1 ? (int)cluster_ctarank() : 0;
   const uint32_t cid = blockIdx.x / CL, ncl = gridDim.x / CL;  // cluster id / count
   const int64_t nftg = P.nft / CL;                               // feature-tile groups
@@ -172,20 +187,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       for (int i = 0; i < C::NS; ++i) {
         mbar_init(&full[i], 1);
-        mbar_init(&empty[i], CL);  // every CTA of the cluster releases the stage
+        mbar_init(&empty[i], 1);
       }
       for (int i = 0; i < C::NA; ++i) {
-        mbar_init(&afull[i], 4);
+        mbar_init(&afull[i], 4 * CL);  // pair: both CTAs' dequant warps (rank 0's copy)
         mbar_init(&aempty[i], 1);
       }
       for (int i = 0; i < 2; ++i) {
         mbar_init(&tfull[i], 1);
-        mbar_init(&tempty[i], 4 * kEpiGroups);
+        mbar_init(&tempty[i], 4 * kEpiGroups * CL);
       }
       fence_barrier_init();
     }
   } else if (warp == 2) {
-    tmem_alloc(tmem_ptr, 512);
+    if constexpr (PAIR) tmem_alloc_pair(tmem_ptr, 512);
+    else tmem_alloc(tmem_ptr, 512);
   } else if (warp == 3) {
     // token-tile prefix over problems: table[p] = sum_{q<p} ceil(len_q / BN)
     uint32_t carry = 0;
@@ -205,50 +221,65 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if constexpr (CL > 1) cluster_sync_all();  // peers' barriers exist before any multicast
+  if constexpr (PAIR) cluster_sync_all();  // peer barriers initialised before remote use
   tc_fence_after();
   const uint32_t tmem = *tmem_ptr;
   const uint32_t ntiles = table[np] * (uint32_t)nftg;
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
-    if (lane == 0) {
+    // converged warp, one elected lane issues (see the MMA issuer below)
+    {
       uint32_t it = 0;
       for (uint32_t t = cid; t < ntiles; t += ncl) {
         const Tile T = decode(table, np, P.problems, t, nftg, BN, CL, rank);
         const uint8_t* wsrc = P.tiled + ((T.e * P.nft + T.ft) * P.nkb) * (int64_t)C::WBYTES;
+        const int row = __shfl_sync(0xffffffffu, (int)(T.row0 + rank * (tile_n<BN, CL>(T) / 2)), 0);
         for (int64_t kb = 0; kb < P.nkb; ++kb, ++it) {
           const int s = it % C::NS;
           mbar_wait(&empty[s], ((it / C::NS) & 1) ^ 1);
           TC_TRACE(0, it);
           uint8_t* sb = smem + s * C::STAGE;
-          mbar_arrive_expect_tx(&full[s], (P.dbg & 4) ? C::BBYTES : C::STAGE);
-          if constexpr (CL > 1)  // my half of the token rows, to every CTA of the pair
-            tma_load_2d_mc(sb + rank * (C::BBYTES / CL), &tmap_x, &full[s], (int)(kb * 64),
-                           (int)(T.row0 + rank * (BN / CL)), (uint16_t)((1u << CL) - 1));
-          else
-            tma_load_2d(sb, &tmap_x, &full[s], (int)(kb * 64), (int)T.row0);
-          if (!(P.dbg & 4)) bulk_load(sb + C::BBYTES, wsrc + kb * C::WBYTES, C::WBYTES, &full[s]);
+          const uint32_t wb = (P.dbg & 4) ? 0u : (uint32_t)C::WBYTES;
+          if (elect_one()) {
+            if constexpr (PAIR) {
+              // rank 0's full[s] counts both token halves plus its weights;
+              // rank 1's counts only its weights (read by its own dequant)
+              mbar_arrive_expect_tx(&full[s], rank == 0 ? 2 * C::BBYTES + wb : wb);
+              tma_load_2d_pair(sb, &tmap_x, mapa_shared(smem_u32(&full[s]), 0), (int)(kb * 64),
+                               row);
+            } else {
+              mbar_arrive_expect_tx(&full[s], C::BBYTES + wb);
+              tma_load_2d(sb, &tmap_x, &full[s], (int)(kb * 64), row);
+            }
+            if (!(P.dbg & 4))
+              bulk_load(sb + C::BBYTES, wsrc + kb * C::WBYTES, C::WBYTES, &full[s]);
+          }
+          __syncwarp();
         }
       }
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------- MMA issuer
-    // The whole loop (waits included) runs on one thread: see header.
-    if (lane == 0) {
+    // The whole warp runs the loop converged, so the tile bookkeeping and
+    // the descriptors stay warp-uniform (uniform registers feed UTCHMMA
+    // directly); one elected lane issues.  A loop run by lane 0 alone makes
+    // ptxas re-uniformise every operand per instruction (ELECT + 6 x
+    // R2UR.BROADCAST waterfall, ~100 cycles per MMA).
+    if (rank == 0) {
       const uint32_t smem_base = smem_u32(smem);
+      const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
       uint32_t it = 0, local = 0;
       for (uint32_t t = cid; t < ntiles; t += ncl, ++local) {
         const int acc = local & 1;
         // a problem's last token tile is usually partial: the MMA N follows
         // the live rows (multiple of 16) so padding costs no tensor time
         const Tile Tt = decode(table, np, P.problems, t, nftg, BN, CL, rank);
-        const int64_t live = Tt.r1 - Tt.row0;
-        const int nmma = live >= BN ? BN : (int)((live + 15) / 16 * 16);
-        const uint32_t idesc = umma_idesc_f16(128, nmma);
+        const uint32_t idesc =
+            __shfl_sync(0xffffffffu, umma_idesc_f16(128 * CL, tile_n<BN, CL>(Tt)), 0);
         mbar_wait(&tempty[acc], ((local >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem + acc * BN;
+        const uint32_t d_tmem = tm + acc * BN;
         for (int64_t kb = 0; kb < P.nkb; ++kb, ++it) {
           const int s = it % C::NS, a = it % C::NA;
           mbar_wait(&full[s], (it / C::NS) & 1);
@@ -257,27 +288,46 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_after();
           TC_TRACE(2, it);
           const uint64_t bdesc = umma_desc_sw128(smem_base + s * C::STAGE);
-          if constexpr (TS) {
-            const uint32_t a_tmem = tmem + C::A_COL + a * 32;
+          if (elect_one()) {
+            if constexpr (TS) {
+              const uint32_t a_tmem = tm + C::A_COL + a * 32;
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk)  // K advance of 16: B 32 bytes (2 desc units), A 8 TMEM cols
-              tc_mma_ts(d_tmem, a_tmem + kk * 8, bdesc + (uint64_t)(kk * 2), idesc,
-                        (kb | kk) != 0 ? 1u : 0u);
-          } else {
-            const uint64_t adesc = umma_desc_sw128(smem_base + C::OFF_A + a * C::ABYTES);
+              for (int kk = 0; kk < 4; ++kk) {  // K advance of 16: B 32 bytes (2 desc units), A 8 TMEM cols
+                if constexpr (PAIR)
+                  tc_mma_ts_pair(d_tmem, a_tmem + kk * 8, bdesc + (uint64_t)(kk * 2), idesc,
+                                 (kb | kk) != 0 ? 1u : 0u);
+                else
+                  tc_mma_ts(d_tmem, a_tmem + kk * 8, bdesc + (uint64_t)(kk * 2), idesc,
+                            (kb | kk) != 0 ? 1u : 0u);
+              }
+            } else {
+              const uint64_t adesc = umma_desc_sw128(smem_base + C::OFF_A + a * C::ABYTES);
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk)  // K advance of 16 fp16 = 32 bytes = 2 desc units
-              tc_mma_ss(d_tmem, adesc + (uint64_t)(kk * 2), bdesc + (uint64_t)(kk * 2), idesc,
-                        (kb | kk) != 0 ? 1u : 0u);
+              for (int kk = 0; kk < 4; ++kk) {  // K advance of 16 fp16 = 32 bytes = 2 desc units
+                if constexpr (PAIR)
+                  tc_mma_ss_pair(d_tmem, adesc + (uint64_t)(kk * 2), bdesc + (uint64_t)(kk * 2),
+                                 idesc, (kb | kk) != 0 ? 1u : 0u);
+                else
+                  tc_mma_ss(d_tmem, adesc + (uint64_t)(kk * 2), bdesc + (uint64_t)(kk * 2),
+                            idesc, (kb | kk) != 0 ? 1u : 0u);
+              }
+            }
+            if constexpr (PAIR) {  // both CTAs' stages are released by the pair's MMAs
+              tc_commit_pair_mc(&empty[s], 3);
+              tc_commit_pair_mc(&aempty[a], 3);
+            } else {
+              tc_commit(&empty[s]);
+              tc_commit(&aempty[a]);
+            }
           }
-          if constexpr (CL > 1)
-            tc_commit_mc(&empty[s], (uint16_t)((1u << CL) - 1));  // stage reads done here
-          else
-            tc_commit(&empty[s]);
-          tc_commit(&aempty[a]);
+          __syncwarp();
           TC_TRACE(3, it);
         }
-        tc_commit(&tfull[acc]);
+        if (elect_one()) {
+          if constexpr (PAIR) tc_commit_pair_mc(&tfull[acc], 3);
+          else tc_commit(&tfull[acc]);
+        }
+        __syncwarp();
       }
     }
   } else if (warp >= 4 && warp < 4 + 4 * kDqGroups) {
@@ -344,7 +394,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           fence_proxy_async_smem();  // generic-proxy stores -> visible to tcgen05.mma
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&afull[a]);
+        if (lane == 0) {
+          if constexpr (PAIR) mbar_arrive_cluster(mapa_shared(smem_u32(&afull[a]), 0));
+          else mbar_arrive(&afull[a]);
+        }
         if (lane == 0 && q == 0) TC_TRACE(5, it);
       }
     }
@@ -418,17 +471,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if constexpr (PAIR) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
+        else mbar_arrive(&tempty[acc]);
+      }
       if (lane == 0 && ew == 0) TC_TRACE(7, local);
     }
     if (lane == 0) bulk_wait<0>();  // all output rows written before the CTA retires
   }
   tc_fence_before();
   __syncthreads();
-  if constexpr (CL > 1) cluster_sync_all();  // no peer multicast / arrive still in flight
+  if constexpr (PAIR) cluster_sync_all();  // no peer commit / arrive still in flight
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem, 512);
+    if constexpr (PAIR) tmem_dealloc_pair(tmem, 512);
+    else tmem_dealloc(tmem, 512);
   }
 }
 
@@ -449,7 +506,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 
 template <int BITS, int BN, bool TS, int CL = 1>
 static int run_tc(const GemmArgs& a, cudaStream_t st) {
-  using C = tc::Cfg<BITS, BN, TS>;
+  using C = tc::Cfg<BITS, BN, TS, CL>;
   auto encode = get_encode();
   if (!encode) return set_error(MOE_ECUDA, "cuTensorMapEncodeTiled unavailable");
   CUtensorMap tmap;
@@ -516,6 +573,11 @@ static int run_tc(const GemmArgs& a, cudaStream_t st) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    if (trace_path) {
+      int nc = 0;
+      cudaOccupancyMaxActiveClusters(&nc, tc::gemm_tc_kernel<BITS, BN, TS, CL>, &cfg);
+      std::fprintf(stderr, "gemm_tc pair BN=%d TS=%d: max active clusters %d\n", BN, (int)TS, nc);
+    }
     MOE_CUDA_TRY(cudaLaunchKernelEx(&cfg, tc::gemm_tc_kernel<BITS, BN, TS, CL>, tmap, O, P));
   } else {
     tc::gemm_tc_kernel<BITS, BN, TS, CL><<<sm_count(), tc::kThreads, C::SMEM, st>>>(tmap, O, P);
@@ -541,20 +603,24 @@ template <int BITS>
 static int run_tc_bits(const GemmArgs& a, cudaStream_t st) {
   // token-tile width from the expected rows per problem (wider MMAs amortise
   // the per-instruction issue cost; narrower ones waste less on small
-  // experts).  256-token tiles (A in shared memory, double-buffered 256-col
-  // accumulators) when they fit one wave -- e.g. an FFN2 with few feature
-  // tiles -- else 224-token tiles with A in TMEM.
+  // experts).  Large problems run on CTA pairs (cta_group::2, M = 256) when
+  // the feature tiles pair up: 256-token tiles with A in shared memory or
+  // 224-token tiles with A in TMEM, whichever quantises into fewer pair
+  // waves x tile width.  Single CTAs otherwise (MOE_TC_PAIR=0 forces them).
   const int64_t nft = (a.n + 127) / 128;
   if (a.rows_hint >= 160) {
-    const int64_t tiles256 = a.np * ((a.rows_hint + 255) / 256) * nft;
-    if (tiles256 <= sm_count()) return run_tc<BITS, 256, false>(a, st);
     static const int force = std::getenv("MOE_TC_BN") ? std::atoi(std::getenv("MOE_TC_BN")) : 0;
-    if (force == 192) return run_tc<BITS, 192, true>(a, st);  // dev experiments
-    if (force == 256) return run_tc<BITS, 256, false>(a, st);
-    // CTA pairs multicasting the activation tile (MOE_TC_CL=2): measured no
-    // faster than single CTAs on B200 (the per-SM fill, not L2, is the limit)
-    static const bool pair = std::getenv("MOE_TC_CL") && std::atoi(std::getenv("MOE_TC_CL")) == 2;
-    if (pair && nft % 2 == 0) return run_tc<BITS, 224, true, 2>(a, st);
+    static const bool pair_ok = !(std::getenv("MOE_TC_PAIR") && std::atoi(std::getenv("MOE_TC_PAIR")) == 0);
+    if (pair_ok && nft % 2 == 0) {
+      const int64_t pairs = sm_count() / 2;
+      const int64_t w256 = (a.np * ((a.rows_hint + 255) / 256) * (nft / 2) + pairs - 1) / pairs;
+      const int64_t w224 = (a.np * ((a.rows_hint + 223) / 224) * (nft / 2) + pairs - 1) / pairs;
+      if (force == 224 || (force != 256 && w224 * 224 < w256 * 256))
+        return run_tc<BITS, 224, true, 2>(a, st);
+      return run_tc<BITS, 256, false, 2>(a, st);
+    }
+    const int64_t tiles256 = a.np * ((a.rows_hint + 255) / 256) * nft;
+    if (tiles256 <= sm_count() || force == 256) return run_tc<BITS, 256, false>(a, st);
     return run_tc<BITS, 224, true>(a, st);
   }
   if (a.rows_hint >= 96) return run_tc<BITS, 128, true>(a, st);

@@ -226,7 +226,9 @@ __global__ void __launch_bounds__(kThreads, 3) gemv_kernel(const Params P) {
 
   if (warp == kWarps) {
     // ------------------------------------------------------------- producer
-    if (lane == 0) {
+    // converged warp, one elected lane issues: a lane-0-only loop makes
+    // ptxas re-uniformise the copy operands per instruction (R2UR waterfall)
+    {
       int s = 0;
       uint32_t ph = 0;
       int n = 0;
@@ -240,8 +242,11 @@ __global__ void __launch_bounds__(kThreads, 3) gemv_kernel(const Params P) {
         for (int pass = 0; pass < npass; ++pass)
           for (int kb = it.kb0; kb < it.kb1; ++kb, ++n) {
             if (n >= RG::NST) mbar_wait(&empty[s], ph ^ 1u);
-            mbar_arrive_expect_tx(&full[s], RG::WB);
-            bulk_load(ring + s * RG::WB, wb + (int64_t)kb * RG::WB, RG::WB, &full[s]);
+            if (elect_one()) {
+              mbar_arrive_expect_tx(&full[s], RG::WB);
+              bulk_load(ring + s * RG::WB, wb + (int64_t)kb * RG::WB, RG::WB, &full[s]);
+            }
+            __syncwarp();
             if (++s == RG::NST) {
               s = 0;
               ph ^= 1u;

@@ -1,0 +1,645 @@
+// k_ln_gate.cu -- K2 gating as ONE kernel per block of token rows:
+//   LayerNorm (proj/src/model.cpp:175-205) -> f32 gate logits (:273-297) ->
+//   top-k softmax gate (proj/src/routing.cpp:11-41, top-k extension) ->
+//   per-block routing-key histogram (routing.cpp:55-62, first counting-sort
+//   pass, consumed by plan_scan in k_route.cu).  Bit-exact with the oracle.
+//
+// Everything on this path is a serial f32 chain: per row the LN mean and
+// variance chains (2*d dependent FADDs), per (row, expert) the k-ordered
+// logit chain (d dependent FMAs -- fp16 x fp16 products are exact in f32, so
+// fmaf == the reference's multiply-then-add).  The floor is therefore chain
+// LATENCY (~4 cycles per step), not bandwidth or FLOPs, unless the chains
+// outnumber the FMA lanes.  The kernel is sized for that:
+//
+// * rb rows per CTA, rb = ceil(T / (148 * waves)) -- every SM gets rows, one
+//   CTA per SM; waves > 1 only when the rows' fp16 copies exceed the
+//   shared-memory budget (d = 1024: 79 rows).
+// * The rows arrive by bulk copies issued by one elected lane; the f32 gate
+//   weights stream through a ring of bulk-copied k-chunks (the whole matrix
+//   when it fits, E = 8 / d = 512: 16 KB).
+// * LN: one thread per row runs both chains over the fp16 row (conversion
+//   inline, loads prefetched); then all threads normalise in place (fp16 xn
+//   stays in shared memory for the logits) and write xn for the FFN gather.
+// * Logits: a thread owns RPT rows x EPG experts of chains (EPG >= 2 as
+//   FFMA2 pairs).  (EPG, RPT) is the smallest that fits 256 threads, so small
+//   T runs many short-latency threads and large T few FMA-dense ones.
+// * Tail: logits + bias -> shared memory; selection (strict '>', first
+//   maximum) one thread per row; every expf (glibc port) in parallel; the
+//   softmax denominator summed serially per row in expert order; scales,
+//   expert ids and the key histogram.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "kernels.cuh"
+
+namespace moecu {
+
+namespace g3 {
+constexpr int kMaxRows = 256;
+constexpr size_t kXBudget = 160 * 1024;   // fp16 rows in shared memory
+constexpr size_t kXfBudget = 64 * 1024;   // f32 row copies for the LN chains
+constexpr size_t kWBudget = 128 * 1024;   // f32 gate weights resident whole
+constexpr size_t kSmemMax = 220 * 1024;
+
+struct Cfg {
+  int nt, rb, epg, rpt, ng, nrg, ntask, kc, nch, ns, xp, wide;
+  size_t off_xf, off_w, wslot, off_st, off_sel, off_hist, off_gb, off_bias, off_tab, off_fin,
+      off_bar, total;
+};
+
+// nt threads; wide: the LN chains read an f32 copy of the rows (and of the
+// squared deviations) made by all threads, so the chain thread issues only
+// its dependent FADDs
+__host__ __device__ inline Cfg cfg1(int64_t d, int64_t E, int64_t gwp, int rb, int epg, int rpt,
+                                    int nt, bool whole) {
+  Cfg c;
+  c.nt = nt;
+  c.rb = rb;
+  c.epg = epg;
+  c.rpt = rpt;
+  c.ng = (int)((E + epg - 1) / epg);
+  c.nrg = (rb + rpt - 1) / rpt;
+  c.ntask = c.ng * c.nrg;
+  // the whole weight matrix when it fits (no per-chunk barriers), else
+  // 16 KB chunks through a 3-slot ring
+  int kc = whole && (size_t)d * gwp * 4 <= kWBudget ? (int)d : (int)(16384 / (gwp * 4)) / 8 * 8;
+  if (kc < 8) kc = 8;
+  if (kc > d) kc = (int)d;  // d % 8 == 0
+  c.kc = kc;
+  c.nch = (int)((d + kc - 1) / kc);
+  c.ns = c.nch < 3 ? c.nch : 3;
+  c.xp = (int)d + 8;  // 16-byte row pitch, rows on distinct 16-byte bank groups
+  // (rb + rpt) rows + slack: a thread's last row group and the operand
+  // prefetch may read past the rows (never used)
+  const size_t xbytes = ((size_t)(rb + rpt) * c.xp * 2 + 256 + 127) & ~size_t(127);
+  const size_t xf = (size_t)rb * (d + 4) * 4;  // pitch d + 4: chain rows on distinct banks
+  c.wide = xf <= kXfBudget ? 1 : 0;
+  c.off_xf = xbytes;
+  c.off_w = c.off_xf + (c.wide ? (xf + 127) & ~size_t(127) : 0);
+  c.wslot = (size_t)kc * gwp * 4;
+  const size_t wring = (size_t)c.ns * c.wslot + (size_t)48 * gwp * 4;  // + prefetch slack
+  const size_t lg = (size_t)2 * rb * (E + 1) * 4;  // logits | expf values (reuse the ring)
+  const size_t body = (wring > lg ? wring : lg) + 64;
+  c.off_st = (c.off_w + body + 15) & ~size_t(15);
+  c.off_sel = c.off_st + (size_t)2 * rb * 4;
+  c.off_hist = c.off_sel + (size_t)rb * 8 * 4;
+  c.off_gb = (c.off_hist + (size_t)(E + 1) * 4 + 15) & ~size_t(15);  // LN gamma | beta, f32
+  c.off_bias = c.off_gb + (size_t)2 * d * 4;
+  c.off_tab = (c.off_bias + (size_t)E * 4 + 15) & ~size_t(15);
+  c.off_fin = c.off_tab + 32 * 8;
+  c.off_bar = (c.off_fin + rb + 15) & ~size_t(15);
+  c.total = c.off_bar + 8 * 4 + 16;
+  return c;
+}
+__host__ __device__ inline Cfg cfg(int64_t d, int64_t E, int64_t gwp, int rb, int epg, int rpt,
+                                   int nt) {
+  const Cfg c = cfg1(d, E, gwp, rb, epg, rpt, nt, true);
+  return c.total <= kSmemMax ? c : cfg1(d, E, gwp, rb, epg, rpt, nt, false);
+}
+
+// c += a * b on two lanes (FFMA2), each RN: exact products, k order per chain
+__device__ __forceinline__ float2 ffma2(float a, float2 b, float2 c) {
+  uint64_t r;
+  const uint64_t bb = (uint64_t)__float_as_uint(b.x) | ((uint64_t)__float_as_uint(b.y) << 32);
+  const uint64_t cc = (uint64_t)__float_as_uint(c.x) | ((uint64_t)__float_as_uint(c.y) << 32);
+  const uint64_t aa = (uint64_t)__float_as_uint(a) | ((uint64_t)__float_as_uint(a) << 32);
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(aa), "l"(bb), "l"(cc));
+  return make_float2(__uint_as_float((uint32_t)r), __uint_as_float((uint32_t)(r >> 32)));
+}
+
+__device__ __forceinline__ long long gtime() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+}  // namespace g3
+
+// dev-only trace (MOE_GATE_TRACE): [0..7] CTA 0 phase clocks, [16 + 2b] per-CTA
+// global-time span
+#define G3_TRACE(i)                                                                \
+  do {                                                                             \
+    if (trace != nullptr && tid == 0) {                                            \
+      if ((i) == 0) trace[16 + 2 * blockIdx.x] = g3::gtime();                      \
+      if ((i) == 5) trace[16 + 2 * blockIdx.x + 1] = g3::gtime();                  \
+      if (blockIdx.x == 0) trace[i] = clock64();                                   \
+    }                                                                              \
+  } while (0)
+
+template <int EPG, int RPT, int NT>
+__global__ void __launch_bounds__(NT, 1) ln_gate_kernel(
+    const uint16_t* __restrict__ x, int64_t T, int d, const uint16_t* __restrict__ lng,
+    const uint16_t* __restrict__ lnb, const float* __restrict__ gw32, int gwp,
+    const uint16_t* __restrict__ gb, int E, int k, const uint8_t* __restrict__ finished,
+    uint16_t* __restrict__ xn, uint32_t* __restrict__ expert, uint16_t* __restrict__ scale,
+    uint32_t* __restrict__ blockcnt, uint32_t* bad_row, int rb, long long* trace) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  const g3::Cfg C = g3::cfg(d, E, gwp, rb, EPG, RPT, NT);
+  uint16_t* xs = reinterpret_cast<uint16_t*>(sm);
+  float* xf = reinterpret_cast<float*>(sm + C.off_xf);  // [rb][d + 4] (wide form only)
+  const int fp = d + 4;
+  float* st = reinterpret_cast<float*>(sm + C.off_st);  // mean[rb] | inv[rb]
+  uint32_t* sel = reinterpret_cast<uint32_t*>(sm + C.off_sel);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(sm + C.off_hist);
+  float* gsm = reinterpret_cast<float*>(sm + C.off_gb);  // gamma[d] | beta[d]
+  float* bsm = reinterpret_cast<float*>(sm + C.off_bias);
+  uint64_t* tab = reinterpret_cast<uint64_t*>(sm + C.off_tab);
+  uint8_t* fsm = sm + C.off_fin;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + C.off_bar);  // [0] rows, [1 + s] weight slots
+  const int tid = threadIdx.x;
+  const int64_t r0 = (int64_t)blockIdx.x * rb;
+  const int nrow = (int)::min((int64_t)rb, T - r0);
+  const int d8 = d / 8, xp = C.xp;
+  G3_TRACE(0);
+
+  if (tid < 32) {  // warp 0 converged, one elected lane issues every copy
+    if (elect_one()) {
+      mbar_init(&bars[0], 1);
+      for (int s = 0; s < C.ns; ++s) mbar_init(&bars[1 + s], 1);
+      fence_barrier_init();
+      mbar_arrive_expect_tx(&bars[0], (uint32_t)nrow * d * 2);
+    }
+    __syncwarp();
+    for (int r = 0; r < nrow; ++r)
+      if (elect_one()) bulk_load(xs + (size_t)r * xp, x + (r0 + r) * d, (uint32_t)d * 2, &bars[0]);
+    for (int c = 0; c < C.ns; ++c) {
+      const uint32_t bytes = (uint32_t)::min(C.kc, d - c * C.kc) * gwp * 4;
+      if (elect_one()) {
+        mbar_arrive_expect_tx(&bars[1 + c], bytes);
+        bulk_load(sm + C.off_w + c * C.wslot, gw32 + (size_t)c * C.kc * gwp, bytes, &bars[1 + c]);
+      }
+    }
+  } else {
+    // the small operands every later phase reads, fetched while the rows
+    // land (each would otherwise cost an L2 round trip on the critical path)
+    for (int i = tid - 32; i < d; i += NT - 32) {
+      gsm[i] = h2f(lng[i]);
+      gsm[d + i] = h2f(lnb[i]);
+    }
+    for (int i = tid - 32; i < E; i += NT - 32) bsm[i] = h2f(gb[i]);
+    for (int i = tid - 32; i < 32; i += NT - 32) tab[i] = moe_expf_tab_dev[i];
+    for (int i = tid - 32; i < nrow; i += NT - 32) fsm[i] = finished != nullptr ? finished[r0 + i] : 0;
+  }
+  for (int i = tid; i <= E; i += NT) hist[i] = 0;
+  __syncthreads();
+  mbar_wait(&bars[0], 0);
+  G3_TRACE(1);
+
+  // ---- LayerNorm chains (model.cpp:178-192): one thread per row, serial RN
+  if (C.wide) {
+    for (int i = tid; i < nrow * d8; i += NT) {  // widen (exact)
+      const int r = i / d8, c = i - r * d8;
+      const uint4 v = *reinterpret_cast<const uint4*>(xs + (size_t)r * xp + c * 8);
+      const uint16_t* h = reinterpret_cast<const uint16_t*>(&v);
+      float4* dst = reinterpret_cast<float4*>(xf + (size_t)r * fp + c * 8);
+      dst[0] = make_float4(h2f(h[0]), h2f(h[1]), h2f(h[2]), h2f(h[3]));
+      dst[1] = make_float4(h2f(h[4]), h2f(h[5]), h2f(h[6]), h2f(h[7]));
+    }
+    __syncthreads();
+    const int d4 = d / 4;
+    if (tid < nrow) {  // sum chain: loads run three pieces ahead of the FADDs
+      const float4* row = reinterpret_cast<const float4*>(xf + (size_t)tid * fp);
+      float s = 0.f;
+      float4 c0 = row[0], c1 = row[::min(1, d4 - 1)], c2 = row[::min(2, d4 - 1)];
+      for (int c = 0; c < d4; ++c) {
+        const float4 v = c0;
+        c0 = c1;
+        c1 = c2;
+        c2 = row[::min(c + 3, d4 - 1)];
+        s = __fadd_rn(s, v.x);
+        s = __fadd_rn(s, v.y);
+        s = __fadd_rn(s, v.z);
+        s = __fadd_rn(s, v.w);
+      }
+      st[tid] = __fdiv_rn(s, (float)d);
+    }
+    __syncthreads();
+    for (int i = tid; i < nrow * d4; i += NT) {  // squared deviations, in place
+      const int r = i / d4;
+      float4* p = reinterpret_cast<float4*>(xf + (size_t)r * fp + (size_t)(i - r * d4) * 4);
+      const float mean = st[r];
+      float4 v = *p;
+      const float a = __fsub_rn(v.x, mean), b = __fsub_rn(v.y, mean);
+      const float c = __fsub_rn(v.z, mean), e = __fsub_rn(v.w, mean);
+      v = make_float4(__fmul_rn(a, a), __fmul_rn(b, b), __fmul_rn(c, c), __fmul_rn(e, e));
+      *p = v;
+    }
+    __syncthreads();
+    if (tid < nrow) {
+      const float4* row = reinterpret_cast<const float4*>(xf + (size_t)tid * fp);
+      float v2 = 0.f;
+      float4 c0 = row[0], c1 = row[::min(1, d4 - 1)], c2 = row[::min(2, d4 - 1)];
+      for (int c = 0; c < d4; ++c) {
+        const float4 v = c0;
+        c0 = c1;
+        c1 = c2;
+        c2 = row[::min(c + 3, d4 - 1)];
+        v2 = __fadd_rn(v2, v.x);
+        v2 = __fadd_rn(v2, v.y);
+        v2 = __fadd_rn(v2, v.z);
+        v2 = __fadd_rn(v2, v.w);
+      }
+      st[rb + tid] = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(v2, (float)d), 1e-5f)));
+    }
+  } else if (tid < nrow) {
+    const uint4* row = reinterpret_cast<const uint4*>(xs + (size_t)tid * xp);
+    float s = 0.f;
+    uint4 cur = row[0];
+    for (int c = 0; c < d8; ++c) {
+      const uint4 nxt = row[c + 1 < d8 ? c + 1 : c];
+      const uint16_t* h = reinterpret_cast<const uint16_t*>(&cur);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) s = __fadd_rn(s, h2f(h[i]));
+      cur = nxt;
+    }
+    const float mean = __fdiv_rn(s, (float)d);
+    float v2 = 0.f;
+    cur = row[0];
+    for (int c = 0; c < d8; ++c) {
+      const uint4 nxt = row[c + 1 < d8 ? c + 1 : c];
+      const uint16_t* h = reinterpret_cast<const uint16_t*>(&cur);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float dx = __fsub_rn(h2f(h[i]), mean);
+        v2 = __fadd_rn(v2, __fmul_rn(dx, dx));
+      }
+      cur = nxt;
+    }
+    st[tid] = mean;
+    st[rb + tid] = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(v2, (float)d), 1e-5f)));
+  }
+  __syncthreads();
+  G3_TRACE(2);
+
+  // ---- normalise in place (model.cpp:193-194); xn also to global for the gather
+  for (int i = tid; i < nrow * d8; i += NT) {
+    const int r = i / d8, c = i - r * d8;
+    uint4 v = *reinterpret_cast<const uint4*>(xs + (size_t)r * xp + c * 8);
+    uint16_t* h = reinterpret_cast<uint16_t*>(&v);
+    const float4 g0 = reinterpret_cast<const float4*>(gsm)[2 * c];
+    const float4 g1 = reinterpret_cast<const float4*>(gsm)[2 * c + 1];
+    const float4 b0 = reinterpret_cast<const float4*>(gsm + d)[2 * c];
+    const float4 b1 = reinterpret_cast<const float4*>(gsm + d)[2 * c + 1];
+    const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+    const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+    const float mean = st[r], inv = st[rb + r];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      h[j] = f2h(__fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(h2f(h[j]), mean), inv), gg[j]), bb[j]));
+    *reinterpret_cast<uint4*>(xs + (size_t)r * xp + c * 8) = v;
+    *reinterpret_cast<uint4*>(xn + (r0 + r) * d + c * 8) = v;
+  }
+  __syncthreads();
+  G3_TRACE(3);
+
+  // ---- logit chains (model.cpp:273-297): RPT rows x EPG experts per thread.
+  // Operands of KS inputs per step; with few chains per thread the chain
+  // latency leaves room for a three-step-deep prefetch ring.
+  constexpr int NP = EPG >= 2 ? EPG / 2 : 1;
+  constexpr int KS = EPG * RPT <= 4 ? 8 : 4;
+  const int rg = tid % C.nrg, eg = tid / C.nrg, e0 = eg * EPG;
+  const bool active = tid < C.ntask;
+  float2 acc[RPT][NP];
+#pragma unroll
+  for (int i = 0; i < RPT; ++i)
+#pragma unroll
+    for (int j = 0; j < NP; ++j) acc[i][j] = make_float2(0.f, 0.f);
+
+  struct Step {
+    uint32_t xh[RPT][KS / 2];
+    float w[KS][EPG];
+  };
+  for (int c = 0; c < C.nch; ++c) {
+    const int s = c % C.ns;
+    mbar_wait(&bars[1 + s], (uint32_t)((c / C.ns) & 1));
+    if (active) {
+      const float* wg = reinterpret_cast<const float*>(sm + C.off_w + s * C.wslot) + e0;
+      const uint16_t* xr = xs + (size_t)rg * xp + c * C.kc;
+      const int kn = ::min(C.kc, d - c * C.kc);  // multiple of 8
+      auto load = [&](Step& o, int kk) {
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+          const uint16_t* p = xr + (size_t)i * C.nrg * xp + kk;
+          if constexpr (KS == 8) {
+            const uint4 v = *reinterpret_cast<const uint4*>(p);
+            o.xh[i][0] = v.x;
+            o.xh[i][1] = v.y;
+            o.xh[i][2] = v.z;
+            o.xh[i][3] = v.w;
+          } else {
+            const uint2 v = *reinterpret_cast<const uint2*>(p);
+            o.xh[i][0] = v.x;
+            o.xh[i][1] = v.y;
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < KS; ++q) {
+          const float* wq = wg + (size_t)(kk + q) * gwp;
+          if constexpr (EPG >= 4) {
+#pragma unroll
+            for (int j = 0; j < EPG; j += 4) {
+              const float4 w4 = *reinterpret_cast<const float4*>(wq + j);
+              o.w[q][j] = w4.x;
+              o.w[q][j + 1] = w4.y;
+              o.w[q][j + 2] = w4.z;
+              o.w[q][j + 3] = w4.w;
+            }
+          } else if constexpr (EPG == 2) {
+            const float2 w2 = *reinterpret_cast<const float2*>(wq);
+            o.w[q][0] = w2.x;
+            o.w[q][1] = w2.y;
+          } else {
+            o.w[q][0] = wq[0];
+          }
+        }
+      };
+      auto fma_step = [&](const Step& o) {
+#pragma unroll
+        for (int q = 0; q < KS; ++q) {
+#pragma unroll
+          for (int i = 0; i < RPT; ++i) {
+            const uint32_t hw = o.xh[i][q / 2];
+            const float xq = h2f((uint16_t)((q & 1) ? (hw >> 16) : (hw & 0xFFFFu)));
+            if constexpr (EPG >= 2) {
+#pragma unroll
+              for (int j = 0; j < NP; ++j)
+                acc[i][j] = g3::ffma2(xq, make_float2(o.w[q][2 * j], o.w[q][2 * j + 1]), acc[i][j]);
+            } else {
+              acc[i][0].x = fmaf(xq, o.w[q][0], acc[i][0].x);
+            }
+          }
+        }
+      };
+      if constexpr (KS == 8) {  // 3-deep ring; loads past kn read padding (unused)
+        Step a, b, e;
+        load(a, 0);
+        load(b, 8);
+        load(e, 16);
+        for (int kk = 0; kk < kn; kk += 24) {
+          fma_step(a);
+          load(a, kk + 24);
+          if (kk + 8 < kn) {
+            fma_step(b);
+            load(b, kk + 32);
+          }
+          if (kk + 16 < kn) {
+            fma_step(e);
+            load(e, kk + 40);
+          }
+        }
+      } else {  // FMA-dense threads: 2-deep ring
+        Step a, b;
+        load(a, 0);
+        for (int kk = 0; kk < kn; kk += 8) {
+          load(b, kk + 4);
+          fma_step(a);
+          load(a, kk + 8);
+          fma_step(b);
+        }
+      }
+    }
+    __syncthreads();  // slot s fully read
+    if (c + C.ns < C.nch && tid < 32) {
+      const int cn = c + C.ns;
+      const uint32_t bytes = (uint32_t)::min(C.kc, d - cn * C.kc) * gwp * 4;
+      if (elect_one()) {
+        mbar_arrive_expect_tx(&bars[1 + s], bytes);
+        bulk_load(sm + C.off_w + s * C.wslot, gw32 + (size_t)cn * C.kc * gwp, bytes, &bars[1 + s]);
+      }
+      __syncwarp();
+    }
+  }
+  G3_TRACE(4);
+
+  // ---- logits + bias into shared memory (the weight ring is drained)
+  float* lg = reinterpret_cast<float*>(sm + C.off_w);
+  const int lp = E + 1;
+  float* ex = lg + (size_t)rb * lp;
+  if (active) {
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      const int r = rg + i * C.nrg;
+#pragma unroll
+      for (int j = 0; j < EPG; ++j) {
+        const float a = (j & 1) ? acc[i][j / 2].y : acc[i][j / 2].x;
+        if (e0 + j < E && r < nrow) lg[r * lp + e0 + j] = __fadd_rn(a, bsm[e0 + j]);
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- top-k selection (routing.cpp:15-31): strict '>', lowest index first
+  if (E <= 16) {
+    if (tid < nrow) {
+      const float* l = lg + tid * lp;
+      float lv[16];
+      bool ok = true;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        lv[j] = j < E ? l[j] : 0.f;
+        ok &= j >= E || isfinite(lv[j]);
+      }
+      if (!ok) {
+        atomicMin(bad_row, (uint32_t)(r0 + tid));
+        sel[tid * 8] = 0xFFFFFFFFu;
+      } else {
+        uint32_t taken = 0;
+        for (int s2 = 0; s2 < k; ++s2) {
+          int bj = -1;
+          float bv = 0.f;
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (j < E && !((taken >> j) & 1u) && (bj < 0 || lv[j] > bv)) {
+              bj = j;
+              bv = lv[j];
+            }
+          taken |= 1u << bj;
+          sel[tid * 8 + s2] = (uint32_t)bj;
+        }
+      }
+    }
+  } else {
+    const int warp = tid >> 5, lane = tid & 31;
+    for (int r = warp; r < nrow; r += NT / 32) {
+      const float* l = lg + r * lp;
+      bool ok = true;
+      for (int j = lane; j < E; j += 32) ok &= isfinite(l[j]);
+      ok = __all_sync(0xffffffffu, ok);
+      if (!ok) {
+        if (lane == 0) {
+          atomicMin(bad_row, (uint32_t)(r0 + r));
+          sel[r * 8] = 0xFFFFFFFFu;
+        }
+        continue;
+      }
+      for (int s2 = 0; s2 < k; ++s2) {
+        float bv = -INFINITY;
+        int bj = 0x7FFFFFFF;
+        for (int j = lane; j < E; j += 32) {
+          bool tk = false;
+          for (int q = 0; q < s2; ++q) tk |= sel[r * 8 + q] == (uint32_t)j;
+          const float v = l[j];
+          if (!tk && (v > bv || bj == 0x7FFFFFFF)) {  // lane-local first maximum
+            bv = v;
+            bj = j;
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+          const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+          if (oj != 0x7FFFFFFF && (bj == 0x7FFFFFFF || ov > bv || (ov == bv && oj < bj))) {
+            bv = ov;
+            bj = oj;
+          }
+        }
+        if (lane == 0) sel[r * 8 + s2] = (uint32_t)bj;
+        __syncwarp();
+      }
+    }
+  }
+  __syncthreads();
+  // ---- expf(l_j - max) for every (row, expert) in parallel (routing.cpp:34)
+  for (int i = tid; i < nrow * E; i += NT) {
+    const int r = i / E, j = i - r * E;
+    const uint32_t s0 = sel[r * 8];
+    if (s0 == 0xFFFFFFFFu) continue;
+    const float* l = lg + r * lp;
+    ex[r * lp + j] = moe_glibc_expf_t(__fsub_rn(l[j], l[s0]), tab);
+  }
+  __syncthreads();
+  // ---- serial sum in expert order, scales, routing keys (routing.cpp:33-38, 55-62)
+  if (tid < nrow) {
+    const int r = tid;
+    const int64_t row = r0 + r;
+    const bool fin = fsm[r] != 0;
+    if (sel[r * 8] == 0xFFFFFFFFu) {
+      for (int s2 = 0; s2 < k; ++s2) {
+        expert[row * k + s2] = 0;
+        scale[row * k + s2] = 0;
+        atomicAdd(&hist[fin ? E : 0], 1u);
+      }
+    } else {
+      const float* exr = ex + r * lp;
+      float sum = 0.f;
+      int j = 0;
+      for (; j + 8 <= E; j += 8) {  // loads ahead of the dependent adds
+        float v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = exr[j + q];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) sum = __fadd_rn(sum, v[q]);
+      }
+      for (; j < E; ++j) sum = __fadd_rn(sum, exr[j]);
+      for (int s2 = 0; s2 < k; ++s2) {
+        const uint32_t e = sel[r * 8 + s2];
+        const float num = s2 == 0 ? 1.0f : exr[e];
+        expert[row * k + s2] = e;
+        scale[row * k + s2] = f2h(__fdiv_rn(num, sum));
+        atomicAdd(&hist[fin ? (uint32_t)E : e], 1u);
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i <= E; i += NT) blockcnt[(int64_t)i * gridDim.x + blockIdx.x] = hist[i];
+  G3_TRACE(5);
+}
+
+// ============================================================ host side
+// rows per CTA and (EPG, RPT, threads): every SM gets rows (waves only when
+// the fp16 rows overflow the shared-memory budget), then the fewest chains
+// per thread that fit 256 threads.
+struct G3Pick {
+  int rb, epg, rpt, nt;
+};
+
+static bool g3_fits(int64_t d, int64_t E, int64_t gwp, int rb, int epg, int rpt, int nt, int k) {
+  const g3::Cfg c = g3::cfg(d, E, gwp, rb, epg, rpt, nt);
+  return c.ntask <= nt && c.total <= g3::kSmemMax && (int64_t)rb * k <= 1024;
+}
+
+static bool g3_pick(int64_t T, int64_t d, int64_t E, int k, G3Pick* p) {
+  const int64_t gwp = gate_fused_pitch(E);
+  const int64_t sms = sm_count();
+  int64_t rbmax = (int64_t)(g3::kXBudget / ((size_t)(d + 8) * 2)) - 2;
+  rbmax = std::min<int64_t>(rbmax, g3::kMaxRows);
+  rbmax = std::min<int64_t>(rbmax, 1024 / k);
+  if (rbmax < 1) return false;
+  const int64_t per_sm = (T + sms - 1) / sms;
+  const int64_t waves = (per_sm + rbmax - 1) / rbmax;
+  int rb = (int)std::max<int64_t>(1, (T + sms * waves - 1) / (sms * waves));
+  static const int kE[] = {2, 4, 8, 8};
+  static const int kR[] = {1, 1, 1, 2};
+  static const int kT[] = {256, 256, 256, 256};
+  for (;;) {
+    for (int i = 0; i < 4; ++i)
+      if (g3_fits(d, E, gwp, rb, kE[i], kR[i], kT[i], k)) {
+        *p = G3Pick{rb, kE[i], kR[i], kT[i]};
+        return true;
+      }
+    if (rb == 1) return false;
+    rb = (rb + 1) / 2;  // too many chains for one CTA: halve the rows
+  }
+}
+
+bool ln_gate_supported(int64_t T, int64_t d, int64_t E, int k) {
+  if (d % 8 != 0 || k < 1 || k > 8 || E < 1 || E > 256 || T < 1) return false;
+  G3Pick p;
+  return g3_pick(T, d, E, k, &p);
+}
+
+int ln_gate_rows(int64_t T, int64_t d, int64_t E, int k) {
+  G3Pick p;
+  return g3_pick(T, d, E, k, &p) ? p.rb : 0;
+}
+
+template <int EPG, int RPT, int NT>
+static int launch_g3(const GateFusedArgs& a, int rb, cudaStream_t st) {
+  const g3::Cfg C = g3::cfg(a.d, a.E, a.gwp, rb, EPG, RPT, NT);
+  static size_t attr = 0;
+  if (C.total > 48 * 1024 && C.total > attr) {
+    MOE_CUDA_TRY(cudaFuncSetAttribute(ln_gate_kernel<EPG, RPT, NT>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C.total));
+    attr = C.total;
+  }
+  const unsigned grid = (unsigned)((a.T + rb - 1) / rb);
+  static long long* dtrace = nullptr;
+  const bool tr = std::getenv("MOE_GATE_TRACE") != nullptr;
+  if (tr && !dtrace) MOE_CUDA_TRY(cudaMalloc(&dtrace, 8 * (16 + 2 * 65536)));
+  ln_gate_kernel<EPG, RPT, NT><<<grid, NT, C.total, st>>>(
+      a.x, a.T, (int)a.d, a.g, a.b, a.gw32, (int)a.gwp, a.gb, (int)a.E, a.k, a.finished, a.xn,
+      a.expert, a.scale, a.blockcnt, a.bad_row, rb, tr ? dtrace : nullptr);
+  note_launch();
+  if (tr && grid <= 65536) {
+    std::vector<long long> h(16 + 2 * grid);
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h.data(), dtrace, h.size() * 8, cudaMemcpyDeviceToHost);
+    long long lo = h[16], hi = h[17], sum = 0;
+    for (unsigned i = 0; i < grid; ++i) {
+      lo = std::min(lo, h[16 + 2 * i]);
+      hi = std::max(hi, h[17 + 2 * i]);
+      sum += h[17 + 2 * i] - h[16 + 2 * i];
+    }
+    std::fprintf(stderr,
+                 "ln_gate EPG=%d RPT=%d NT=%d grid=%u rb=%d kc=%d nch=%d tasks=%d wide=%d: "
+                 "span=%lld ns cta mean=%lld ns; cta0 clocks rows=%lld chains=%lld norm=%lld "
+                 "logits=%lld tail=%lld\n",
+                 EPG, RPT, NT, grid, rb, C.kc, C.nch, C.ntask, C.wide, hi - lo, sum / grid,
+                 h[1] - h[0], h[2] - h[1], h[3] - h[2], h[4] - h[3], h[5] - h[4]);
+  }
+  return check_launch("ln_gate");
+}
+
+int launch_ln_gate(const GateFusedArgs& a, cudaStream_t st) {
+  if (a.T == 0) return MOE_OK;
+  G3Pick p;
+  if (!g3_pick(a.T, a.d, a.E, a.k, &p)) return set_error(MOE_EINVAL, "ln_gate: unsupported shape");
+  if (p.rb != a.rows) return set_error(MOE_EINVAL, "ln_gate: row block mismatch");
+  if (p.epg == 2) return launch_g3<2, 1, 256>(a, p.rb, st);
+  if (p.epg == 4) return launch_g3<4, 1, 256>(a, p.rb, st);
+  if (p.rpt == 1) return launch_g3<8, 1, 256>(a, p.rb, st);
+  return launch_g3<8, 2, 256>(a, p.rb, st);
+}
+
+}  // namespace moecu

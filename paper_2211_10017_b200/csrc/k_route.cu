@@ -183,6 +183,139 @@ __global__ void __launch_bounds__(1024) plan_place_kernel(int spb,
   }
 }
 
+// Scan + place + gather in ONE kernel for plans whose (block x key)
+// histogram is small (every CTA re-derives the key offsets and its own
+// bases from the whole histogram -- (E+1) x nblk words from L2 -- instead of
+// waiting on a single-CTA scan kernel), then ranks its slots exactly as
+// plan_place_kernel and gathers the rows it placed with all its threads
+// (loads batched ahead of the stores).
+constexpr int kPlaceThreads = 256;
+constexpr int64_t kFusedScanMax = 16384;  // (E+1) * nblk words
+
+__global__ void __launch_bounds__(1024) plan_place_fused_kernel(int spb,
+    const uint32_t* __restrict__ expert, const uint8_t* __restrict__ finished, int64_t S, int k,
+    int64_t E, const uint32_t* __restrict__ blockcnt, uint32_t* __restrict__ perm,
+    uint32_t* __restrict__ inv, uint32_t* __restrict__ offsets, uint32_t* __restrict__ problems,
+    uint32_t* __restrict__ active, const uint16_t* __restrict__ src, int64_t cols,
+    uint16_t* __restrict__ dst, uint32_t* bad) {
+  extern __shared__ uint32_t sh[];
+  const int64_t keys = E + 1, nblk = gridDim.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
+  uint32_t* tot = sh;                 // [keys]  totals, then exclusive offsets
+  uint32_t* base = tot + keys + 1;    // [keys]  this block's first position per key
+  uint32_t* wcnt = base + keys;       // [nwarp][keys]
+  uint32_t* pos_l = wcnt + nwarp * keys;  // [blockDim]
+  const int64_t b = blockIdx.x;
+  // 1. per key: total over all blocks and the count in blocks before b
+  for (int64_t key = warp; key < keys; key += nwarp) {
+    const uint32_t* row = blockcnt + key * nblk;
+    uint32_t t = 0, pre = 0;
+    for (int64_t b0 = 0; b0 < nblk; b0 += 256) {
+      uint32_t v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int64_t bb = b0 + j * 32 + lane;
+        v[j] = bb < nblk ? row[bb] : 0u;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        t += v[j];
+        if (b0 + j * 32 + lane < b) pre += v[j];
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      t += __shfl_xor_sync(0xffffffffu, t, o);
+      pre += __shfl_xor_sync(0xffffffffu, pre, o);
+    }
+    if (lane == 0) {
+      tot[key] = t;
+      base[key] = pre;
+    }
+  }
+  for (int64_t i = threadIdx.x; i < nwarp * keys; i += blockDim.x) wcnt[i] = 0;
+  __syncthreads();
+  // 2. exclusive scan of the key totals (keys <= 1024: warp 0, 32 per lane)
+  if (warp == 0) {
+    uint32_t v[32], run = 0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int64_t key = lane * 32 + j;
+      v[j] = key < keys ? tot[key] : 0u;
+      run += v[j];
+    }
+    uint32_t in = run;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, in, o);
+      if (lane >= o) in += u;
+    }
+    uint32_t ex = in - run;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int64_t key = lane * 32 + j;
+      if (key < keys) {
+        tot[key] = ex;
+        base[key] += ex;
+      }
+      ex += v[j];
+    }
+  }
+  __syncthreads();
+  if (b == 0) {
+    for (int64_t key = threadIdx.x; key < keys; key += blockDim.x) offsets[key] = tot[key];
+    for (int64_t e = threadIdx.x; e < E; e += blockDim.x)
+      if (problems != nullptr) {
+        problems[3 * e] = (uint32_t)e;
+        problems[3 * e + 1] = tot[e];
+        problems[3 * e + 2] = tot[e + 1];
+      }
+    if (threadIdx.x == 0 && active != nullptr) *active = tot[E];
+  }
+  // 3. place (as plan_place_kernel): rank among equal keys in slot order
+  const int64_t slot = b * spb + threadIdx.x;
+  const bool live = (int)threadIdx.x < spb && slot < S;
+  const uint32_t key = live ? slot_key(expert, finished, slot, k, E, bad) : 0xFFFFFFFFu;
+  const uint32_t peers = __match_any_sync(0xffffffffu, key);
+  const uint32_t rank_w = __popc(peers & ((1u << lane) - 1u));
+  if (live && (peers >> lane) == 1u) wcnt[warp * keys + key] = __popc(peers);
+  __syncthreads();
+  if (live) {
+    uint32_t before = 0;
+    for (int w = 0; w < warp; ++w) before += wcnt[w * keys + key];
+    const uint32_t pos = base[key] + before + rank_w;
+    perm[pos] = (uint32_t)slot;
+    inv[slot] = pos;
+    pos_l[threadIdx.x] = pos;
+  }
+  if (dst == nullptr) return;
+  __syncthreads();
+  // 4. gather dst[pos] = src[slot / k]: 16-byte pieces, 4 loads in flight per
+  //    thread (32-bit index math: a 64-bit division per piece costs more
+  //    than the copy)
+  const int nslots = (int)::min((int64_t)spb, S - b * spb);
+  const int c8 = (int)(cols / 8), total = nslots * c8;
+  const int64_t slot0 = b * spb;
+  for (int i0 = threadIdx.x; i0 < total; i0 += 4 * (int)blockDim.x) {
+    uint4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * (int)blockDim.x;
+      if (i < total) {
+        const int sl = i / c8, c = i - sl * c8;
+        v[u] = reinterpret_cast<const uint4*>(src + ((slot0 + sl) / k) * cols)[c];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * (int)blockDim.x;
+      if (i < total) {
+        const int sl = i / c8, c = i - sl * c8;
+        reinterpret_cast<uint4*>(dst + (int64_t)pos_l[sl] * cols)[c] = v[u];
+      }
+    }
+  }
+}
+
 int launch_routing_plan(const uint32_t* expert, const uint8_t* finished, int64_t T, int k,
                         int64_t E, uint32_t* perm, uint32_t* inv, uint32_t* offsets,
                         uint32_t* problems, uint32_t* active, const PlanWork& w,
@@ -220,6 +353,15 @@ int launch_plan_from_counts(const uint32_t* expert, const uint8_t* finished, int
   if (S == 0) return MOE_OK;
   if (E + 1 > 1024) return set_error(MOE_EINVAL, "routing plan: at most 1023 experts");
   const int64_t nblk = (S + spb - 1) / spb;
+  if ((E + 1) * nblk <= kFusedScanMax && (cols % 8) == 0 && spb <= 1024) {
+    const int threads = (int)std::max<int64_t>(kPlaceThreads, (spb + 31) / 32 * 32);
+    const size_t smem = ((E + 1) * 2 + 1 + (threads / 32) * (E + 1) + threads) * 4;
+    plan_place_fused_kernel<<<(unsigned)nblk, threads, smem, st>>>(
+        (int)spb, expert, finished, S, k, E, w.blockcnt, perm, inv, offsets, problems, active,
+        gather_src, cols, gather_dst, w.bad);
+    note_launch();
+    return check_launch("plan_place_fused");
+  }
   plan_scan_kernel<<<1, 1024, 0, st>>>(w.blockcnt, nblk, E, w.blockbase, offsets, problems,
                                        active);
   note_launch();

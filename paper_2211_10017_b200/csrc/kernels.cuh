@@ -58,9 +58,14 @@ struct GateFusedArgs {
   uint32_t* bad_row;
   int rows;            // gate_fused_rows(T, E, k)
 };
+int64_t gate_fused_pitch(int64_t E);  // f32 gate weight row pitch (multiple of 8)
 int gate_fused_rows(int64_t T, int64_t E, int k);  // rows per gate block (plan block = rows*k slots)
 bool gate_fused_supported(int64_t d, int64_t E, int k);
 int launch_gate_fused(const GateFusedArgs& a, cudaStream_t st);
+// k_ln_gate.cu: the same stage as ONE kernel (LN + logits + top-k + histogram)
+bool ln_gate_supported(int64_t T, int64_t d, int64_t E, int k);
+int ln_gate_rows(int64_t T, int64_t d, int64_t E, int k);  // rows per block (GateFusedArgs::rows)
+int launch_ln_gate(const GateFusedArgs& a, cudaStream_t st);
 int launch_widen_gate(const uint16_t* gw, int64_t d, int64_t E, int64_t gwp, float* out,
                       cudaStream_t st);
 

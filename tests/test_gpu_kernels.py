@@ -290,6 +290,41 @@ def test_gemm_fast_equals_exact_semantics_large(cuda, oracle):
 
 
 @pytest.mark.parametrize("bits", [4, 8, 16])
+@pytest.mark.parametrize("sizes,m,n", [
+    ([1000, 17, 1, 1500, 257, 999, 2048, 2182], 512, 2048),   # CTA pairs, 256-token SS tiles
+    ([672] * 8, 512, 2048),                                   # CTA pairs, 224-token TS tiles
+    ([300, 15, 33, 224, 225, 480, 600, 0, 431], 520, 1024),   # pairs, ragged + K tail
+])
+def test_gemm_fast_cta_pair_ragged(cuda, sizes, m, n, bits):
+    """cta_group::2 tiles (M = 256 over two SMs, each CTA holding half of the
+    token tile): problem sizes that leave every kind of partial last tile
+    (1..255 rows, empty problems, a K tail), fast vs exact on the GPU."""
+    ops = _ops()
+    rng = np.random.default_rng(sum(sizes) + m + n + bits)
+    E = len(sizes)
+    rows = sum(sizes)
+    off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.uint32)
+    probs = np.stack([np.arange(E, dtype=np.uint32), off[:-1], off[1:]], 1)
+    x = rng.standard_normal((rows, m)).astype(np.float16)
+    w = (0.25 * rng.standard_normal((E, m, n))).astype(np.float16)
+    bias = (0.05 * rng.standard_normal((E, n))).astype(np.float16)
+    if bits == 16:
+        tiled, sc = ops.tile_weights(to_dev(w), E, m, n, 16), None
+    else:
+        packed, sc = ops.quantize(to_dev(w), bits)
+        tiled = ops.tile_weights(packed, E, m, n, bits)
+    xs, pr, bd = to_dev(x), to_dev(probs), to_dev(bias)
+    a = ops.grouped_gemm(xs, pr, tiled, sc, bits, E, n, bd, True, ops.MODE_EXACT)
+    b = ops.grouped_gemm(xs, pr, tiled, sc, bits, E, n, bd, True, ops.MODE_FAST)
+    got, want = to_np(b), to_np(a)
+    assert np.isfinite(got.astype(np.float32)).all()
+    for e in range(E):  # every problem on its own: a missed tail tile cannot hide
+        lo, hi = int(off[e]), int(off[e + 1])
+        if hi > lo:
+            assert norm_err(got[lo:hi], want[lo:hi]) <= TOL_FAST, (e, lo, hi)
+
+
+@pytest.mark.parametrize("bits", [4, 8, 16])
 @pytest.mark.parametrize("shape", [(1, 1, 1024, 4096), (8, 4, 1024, 512), (64, 32, 256, 1024),
                                    (40, 3, 4096, 256), (3, 5, 72, 136), (200, 8, 512, 2048)])
 def test_gemm_gemv_decode_within_tolerance(cuda, oracle, bits, shape):
