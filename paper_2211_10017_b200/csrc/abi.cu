@@ -444,8 +444,9 @@ static int layer_create_impl(const moe_layer_desc* D, moe_layer** out, bool devi
       (st = up(&L->b1, D->b1, El * f)) || (st = up(&L->b2, D->b2, El * d)))
     return fail(st);
   L->gwp = gate_fused_pitch(E);
-  if ((st = L->alloc(&L->gw32, d * L->gwp * 4)) ||
-      (st = launch_widen_gate(L->gw, d, E, L->gwp, L->gw32, nullptr)))
+  if (d % 8 == 0 &&  // the fused gate's envelope; other shapes take the unfused kernels
+      ((st = L->alloc(&L->gw32, d * L->gwp * 4)) ||
+       (st = launch_widen_gate(L->gw, d, E, L->gwp, L->gw32, nullptr))))
     return fail(st);
   // experts: upload the reference-layout payload once, tile, drop the source
   auto tile = [&](void** dst, const void* src, int64_t m, int64_t n) -> int {
@@ -560,24 +561,12 @@ static int layer_route(moe_layer* L, const uint16_t* x, const uint8_t* fin, int6
   MOE_CUDA_TRY(cudaMemsetAsync(L->bad_row, 0xFF, 8, st));  // bad_row + bad_expert
   TRY(mark());
   PlanWork w{L->blockcnt, L->blockbase, L->bad_expert};
-  static const bool old_gate = std::getenv("MOE_GATE_OLD") != nullptr;  // dev A/B
   const bool aligned = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
-  if (aligned && !old_gate && ln_gate_supported(T, d, E, k)) {
+  if (aligned && L->gw32 != nullptr && ln_gate_supported(T, d, E, k)) {
     // one kernel: LN + logits + top-k + key histogram; then scan/place/gather
     GateFusedArgs ga{x, T, d, L->ln_g, L->ln_b, L->gw32, L->gwp, L->gb, E, k, fin, L->xn,
                      L->expert, L->scale, L->blockcnt, L->bad_row, ln_gate_rows(T, d, E, k)};
     TRY(launch_ln_gate(ga, st));
-    TRY(mark());
-    TRY(mark());
-    TRY(mark());
-    TRY(launch_plan_from_counts(L->expert, fin, T, k, E, (int64_t)ga.rows * k, w, L->perm,
-                                L->inv, L->offsets, L->problems, L->active, L->xn, d, L->xp,
-                                st));
-  } else if (gate_fused_supported(d, E, k) && aligned) {
-    // two kernels: LN rows, then logits + top-k + key histogram
-    GateFusedArgs ga{x, T, d, L->ln_g, L->ln_b, L->gw32, L->gwp, L->gb, E, k, fin, L->xn,
-                     L->expert, L->scale, L->blockcnt, L->bad_row, gate_fused_rows(T, E, k)};
-    TRY(launch_gate_fused(ga, st));
     TRY(mark());
     TRY(mark());
     TRY(mark());

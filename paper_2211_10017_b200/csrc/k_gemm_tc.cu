@@ -86,7 +86,7 @@ struct Cfg {
 
 struct Tile {
   int p;
-  int64_t e, r0, r1, row0, ft;
+  int64_t e, r0, r1, row0, row1, ft;  // problem rows [r0, r1); this tile's [row0, row1)
 };
 
 // t indexes (token tile, feature-tile group of CL); CTA `rank` of a CL-CTA
@@ -105,7 +105,11 @@ __device__ __forceinline__ Tile decode(const uint32_t* table, int np, const uint
   x.e = problems[3 * lo];
   x.r0 = problems[3 * lo + 1];
   x.r1 = problems[3 * lo + 2];
-  x.row0 = x.r0 + (int64_t)(g - table[lo]) * BN;
+  // a problem's ceil(len / BN) token tiles split its rows evenly (sizes
+  // differ by at most one): no 224 + 32 tails whose MMAs would be issue-bound
+  const int64_t nt = table[lo + 1] - table[lo], j = g - table[lo], len = x.r1 - x.r0;
+  x.row0 = x.r0 + (j * len) / nt;
+  x.row1 = x.r0 + ((j + 1) * len) / nt;
   x.ft = (int64_t)(t % (uint32_t)nftg) * CL + rank;
   return x;
 }
@@ -115,7 +119,7 @@ __device__ __forceinline__ Tile decode(const uint32_t* table, int np, const uint
 // whole 8-row swizzle atoms) and padding costs no tensor time
 template <int BN, int CL>
 __device__ __forceinline__ int tile_n(const Tile& T) {
-  const int64_t live = T.r1 - T.row0;
+  const int64_t live = T.row1 - T.row0;
   return live >= BN ? BN : (int)((live + 15) / 16 * 16);
 }
 
@@ -282,7 +286,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t d_tmem = tm + acc * BN;
         for (int64_t kb = 0; kb < P.nkb; ++kb, ++it) {
           const int s = it % C::NS, a = it % C::NA;
-          mbar_wait(&full[s], (it / C::NS) & 1);
+          // one barrier per k-block: every dequant warp waited on full[s]
+          // (rank 0's counts both token halves) before arriving on afull[a],
+          // so afull also orders the activation tile (each try_wait costs
+          // ~90 cycles of this thread even when already complete)
           TC_TRACE(1, it);
           mbar_wait(&afull[a], (it / C::NA) & 1);
           tc_fence_after();
@@ -427,7 +434,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       if (lane == 0 && ew == 0) TC_TRACE(6, local);
       // only the columns holding this tile's rows need draining
-      const int64_t live = T.r1 - T.row0;
+      const int64_t live = T.row1 - T.row0;
       const int ncols = (int)(live < BN ? (live + 31) / 32 * 32 : BN);
       const bool slice_live = T.ft * 128 + q * 32 < P.n;
 #pragma unroll 1
@@ -457,7 +464,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0 && ew == 0) TC_TRACE(10, cc);
         // read back as 16-byte vectors: lane -> (row lane/4 + 8i, 8 features)
-        const int nrow = (int)::min((int64_t)32, T.r1 - (T.row0 + c0));
+        const int nrow = (int)::min((int64_t)32, T.row1 - (T.row0 + c0));
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int row = i * 8 + (lane >> 2), ch = lane & 3;

@@ -173,9 +173,13 @@ __global__ void __launch_bounds__(NT, 1) ln_gate_kernel(
   } else {
     // the small operands every later phase reads, fetched while the rows
     // land (each would otherwise cost an L2 round trip on the critical path)
-    for (int i = tid - 32; i < d; i += NT - 32) {
-      gsm[i] = h2f(lng[i]);
-      gsm[d + i] = h2f(lnb[i]);
+    for (int i = tid - 32; i < 2 * d8; i += NT - 32) {  // 16-byte loads, all in flight
+      const int c = i < d8 ? i : i - d8;
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(i < d8 ? lng : lnb) + c);
+      const uint16_t* h = reinterpret_cast<const uint16_t*>(&v);
+      float4* o = reinterpret_cast<float4*>(gsm + (i < d8 ? 0 : d) + c * 8);
+      o[0] = make_float4(h2f(h[0]), h2f(h[1]), h2f(h[2]), h2f(h[3]));
+      o[1] = make_float4(h2f(h[4]), h2f(h[5]), h2f(h[6]), h2f(h[7]));
     }
     for (int i = tid - 32; i < E; i += NT - 32) bsm[i] = h2f(gb[i]);
     for (int i = tid - 32; i < 32; i += NT - 32) tab[i] = moe_expf_tab_dev[i];
@@ -314,7 +318,11 @@ __global__ void __launch_bounds__(NT, 1) ln_gate_kernel(
     const int s = c % C.ns;
     mbar_wait(&bars[1 + s], (uint32_t)((c / C.ns) & 1));
     if (active) {
-      const float* wg = reinterpret_cast<const float*>(sm + C.off_w + s * C.wslot) + e0;
+      // weights blocked by (input pair, expert pair) (k_gate_fused.cu):
+      // inputs 2j, 2j+1 of experts e0.. are the contiguous floats
+      // [j * 2 * gwp + 2 * e0, ... + 2 * EPG)
+      const float* wg = reinterpret_cast<const float*>(sm + C.off_w + s * C.wslot) + 2 * e0;
+      const int wstride = 2 * gwp;  // floats per input pair
       const uint16_t* xr = xs + (size_t)rg * xp + c * C.kc;
       const int kn = ::min(C.kc, d - c * C.kc);  // multiple of 8
       auto load = [&](Step& o, int kk) {
@@ -333,24 +341,17 @@ __global__ void __launch_bounds__(NT, 1) ln_gate_kernel(
             o.xh[i][1] = v.y;
           }
         }
+        const float* w0 = wg + (size_t)(kk >> 1) * wstride;
 #pragma unroll
-        for (int q = 0; q < KS; ++q) {
-          const float* wq = wg + (size_t)(kk + q) * gwp;
-          if constexpr (EPG >= 4) {
+        for (int q = 0; q < KS; q += 2) {  // one input pair: 2 * EPG floats
+          const float* wq = w0 + (q >> 1) * wstride;
 #pragma unroll
-            for (int j = 0; j < EPG; j += 4) {
-              const float4 w4 = *reinterpret_cast<const float4*>(wq + j);
-              o.w[q][j] = w4.x;
-              o.w[q][j + 1] = w4.y;
-              o.w[q][j + 2] = w4.z;
-              o.w[q][j + 3] = w4.w;
-            }
-          } else if constexpr (EPG == 2) {
-            const float2 w2 = *reinterpret_cast<const float2*>(wq);
-            o.w[q][0] = w2.x;
-            o.w[q][1] = w2.y;
-          } else {
-            o.w[q][0] = wq[0];
+          for (int j = 0; j < EPG; j += 2) {  // experts e0+j, e0+j+1 x inputs q, q+1
+            const float4 w4 = *reinterpret_cast<const float4*>(wq + 2 * j);
+            o.w[q][j] = w4.x;
+            o.w[q][j + 1] = w4.y;
+            o.w[q + 1][j] = w4.z;
+            o.w[q + 1][j + 1] = w4.w;
           }
         }
       };
@@ -371,24 +372,22 @@ __global__ void __launch_bounds__(NT, 1) ln_gate_kernel(
           }
         }
       };
-      if constexpr (KS == 8) {  // 3-deep ring; loads past kn read padding (unused)
-        Step a, b, e;
+      if constexpr (KS == 8) {
+        // two-step ring over 16-input periods with no branches in the body
+        // (a guarded load keeps ptxas from hoisting it above the previous
+        // step's FMAs); loads past kn read padding and are never used
+        Step a, b;
         load(a, 0);
         load(b, 8);
-        load(e, 16);
-        for (int kk = 0; kk < kn; kk += 24) {
+        int kk = 0;
+        for (; kk + 16 <= kn; kk += 16) {
           fma_step(a);
-          load(a, kk + 24);
-          if (kk + 8 < kn) {
-            fma_step(b);
-            load(b, kk + 32);
-          }
-          if (kk + 16 < kn) {
-            fma_step(e);
-            load(e, kk + 40);
-          }
+          load(a, kk + 16);
+          fma_step(b);
+          load(b, kk + 24);
         }
-      } else {  // FMA-dense threads: 2-deep ring
+        if (kk < kn) fma_step(a);  // kn % 16 == 8
+      } else {  // FMA-dense threads: 2-deep ring of 4-input steps
         Step a, b;
         load(a, 0);
         for (int kk = 0; kk < kn; kk += 8) {

@@ -13,6 +13,11 @@
 //              16-byte vector copies (permute_rows, routing.cpp:89-97).
 // Everything is integer and order-deterministic: bit-identical to the
 // reference counting sort.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
 #include "kernels.cuh"
 
 namespace moecu {
@@ -190,74 +195,79 @@ __global__ void __launch_bounds__(1024) plan_place_kernel(int spb,
 // plan_place_kernel and gathers the rows it placed with all its threads
 // (loads batched ahead of the stores).
 constexpr int kPlaceThreads = 256;
-constexpr int64_t kFusedScanMax = 16384;  // (E+1) * nblk words
+constexpr int64_t kFusedScanMax = 8192;  // (E+1) * nblk words, staged in shared memory
 
 __global__ void __launch_bounds__(1024) plan_place_fused_kernel(int spb,
     const uint32_t* __restrict__ expert, const uint8_t* __restrict__ finished, int64_t S, int k,
     int64_t E, const uint32_t* __restrict__ blockcnt, uint32_t* __restrict__ perm,
     uint32_t* __restrict__ inv, uint32_t* __restrict__ offsets, uint32_t* __restrict__ problems,
     uint32_t* __restrict__ active, const uint16_t* __restrict__ src, int64_t cols,
-    uint16_t* __restrict__ dst, uint32_t* bad) {
+    uint16_t* __restrict__ dst, uint32_t* bad, long long* trace) {
   extern __shared__ uint32_t sh[];
   const int64_t keys = E + 1, nblk = gridDim.x;
+#define PL_TRACE(i)                                                               \
+  do {                                                                            \
+    if (trace != nullptr && threadIdx.x == 0) {                                   \
+      long long g_;                                                               \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_));                      \
+      if ((i) == 0) trace[16 + 2 * blockIdx.x] = g_;                              \
+      if ((i) == 5) trace[16 + 2 * blockIdx.x + 1] = g_;                          \
+      if (blockIdx.x == 0) trace[i] = clock64();                                  \
+    }                                                                             \
+  } while (0)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
   uint32_t* tot = sh;                 // [keys]  totals, then exclusive offsets
   uint32_t* base = tot + keys + 1;    // [keys]  this block's first position per key
   uint32_t* wcnt = base + keys;       // [nwarp][keys]
   uint32_t* pos_l = wcnt + nwarp * keys;  // [blockDim]
+  uint32_t* cnt = pos_l + blockDim.x;     // [keys][nblk + 1] staged histogram
   const int64_t b = blockIdx.x;
-  // 1. per key: total over all blocks and the count in blocks before b
-  for (int64_t key = warp; key < keys; key += nwarp) {
-    const uint32_t* row = blockcnt + key * nblk;
-    uint32_t t = 0, pre = 0;
-    for (int64_t b0 = 0; b0 < nblk; b0 += 256) {
-      uint32_t v[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int64_t bb = b0 + j * 32 + lane;
-        v[j] = bb < nblk ? row[bb] : 0u;
-      }
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        t += v[j];
-        if (b0 + j * 32 + lane < b) pre += v[j];
-      }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      t += __shfl_xor_sync(0xffffffffu, t, o);
-      pre += __shfl_xor_sync(0xffffffffu, pre, o);
-    }
-    if (lane == 0) {
-      tot[key] = t;
-      base[key] = pre;
-    }
+  PL_TRACE(0);
+  // this thread's slot key, loaded up front (overlaps the histogram loads)
+  const int64_t slot = b * spb + threadIdx.x;
+  const bool live = (int)threadIdx.x < spb && slot < S;
+  const uint32_t key = live ? slot_key(expert, finished, slot, k, E, bad) : 0xFFFFFFFFu;
+  // 1. stage the whole (key x block) histogram (all loads in flight at once),
+  //    then per key: total over all blocks and the count in blocks before b
+  // (pitch nblk + 1: one thread per key walks its row without bank conflicts)
+  const int ncnt = (int)(keys * nblk), cp = (int)nblk + 1;
+  for (int i = threadIdx.x; i < ncnt; i += blockDim.x) {
+    const int kk = i / (int)nblk;
+    cnt[kk * cp + (i - kk * (int)nblk)] = blockcnt[i];
   }
   for (int64_t i = threadIdx.x; i < nwarp * keys; i += blockDim.x) wcnt[i] = 0;
   __syncthreads();
-  // 2. exclusive scan of the key totals (keys <= 1024: warp 0, 32 per lane)
+  for (int64_t kk = threadIdx.x; kk < keys; kk += blockDim.x) {
+    const uint32_t* row = cnt + kk * cp;
+    uint32_t t = 0, pre = 0;
+#pragma unroll 4
+    for (int bb = 0; bb < (int)nblk; ++bb) {
+      const uint32_t v = row[bb];
+      t += v;
+      pre += bb < b ? v : 0u;
+    }
+    tot[kk] = t;
+    base[kk] = pre;
+  }
+  __syncthreads();
+  PL_TRACE(1);
+  // 2. exclusive scan of the key totals: warp 0, 32 keys per round
+  //    (lane-interleaved, conflict-free), carry across rounds
   if (warp == 0) {
-    uint32_t v[32], run = 0;
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const int64_t key = lane * 32 + j;
-      v[j] = key < keys ? tot[key] : 0u;
-      run += v[j];
-    }
-    uint32_t in = run;
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t u = __shfl_up_sync(0xffffffffu, in, o);
-      if (lane >= o) in += u;
-    }
-    uint32_t ex = in - run;
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const int64_t key = lane * 32 + j;
-      if (key < keys) {
-        tot[key] = ex;
-        base[key] += ex;
+    uint32_t carry = 0;
+    for (int64_t k0 = 0; k0 < keys; k0 += 32) {
+      const int64_t key = k0 + lane;
+      const uint32_t v = key < keys ? tot[key] : 0u;
+      uint32_t in = v;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, in, o);
+        if (lane >= o) in += u;
       }
-      ex += v[j];
+      if (key < keys) {
+        tot[key] = carry + in - v;
+        base[key] += carry + in - v;
+      }
+      carry += __shfl_sync(0xffffffffu, in, 31);
     }
   }
   __syncthreads();
@@ -271,10 +281,8 @@ __global__ void __launch_bounds__(1024) plan_place_fused_kernel(int spb,
       }
     if (threadIdx.x == 0 && active != nullptr) *active = tot[E];
   }
+  PL_TRACE(2);
   // 3. place (as plan_place_kernel): rank among equal keys in slot order
-  const int64_t slot = b * spb + threadIdx.x;
-  const bool live = (int)threadIdx.x < spb && slot < S;
-  const uint32_t key = live ? slot_key(expert, finished, slot, k, E, bad) : 0xFFFFFFFFu;
   const uint32_t peers = __match_any_sync(0xffffffffu, key);
   const uint32_t rank_w = __popc(peers & ((1u << lane) - 1u));
   if (live && (peers >> lane) == 1u) wcnt[warp * keys + key] = __popc(peers);
@@ -289,16 +297,18 @@ __global__ void __launch_bounds__(1024) plan_place_fused_kernel(int spb,
   }
   if (dst == nullptr) return;
   __syncthreads();
-  // 4. gather dst[pos] = src[slot / k]: 16-byte pieces, 4 loads in flight per
+  PL_TRACE(3);
+  // 4. gather dst[pos] = src[slot / k]: 16-byte pieces, 8 loads in flight per
   //    thread (32-bit index math: a 64-bit division per piece costs more
   //    than the copy)
   const int nslots = (int)::min((int64_t)spb, S - b * spb);
   const int c8 = (int)(cols / 8), total = nslots * c8;
   const int64_t slot0 = b * spb;
-  for (int i0 = threadIdx.x; i0 < total; i0 += 4 * (int)blockDim.x) {
-    uint4 v[4];
+  constexpr int U = 8;
+  for (int i0 = threadIdx.x; i0 < total; i0 += U * (int)blockDim.x) {
+    uint4 v[U];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < U; ++u) {
       const int i = i0 + u * (int)blockDim.x;
       if (i < total) {
         const int sl = i / c8, c = i - sl * c8;
@@ -306,7 +316,7 @@ __global__ void __launch_bounds__(1024) plan_place_fused_kernel(int spb,
       }
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < U; ++u) {
       const int i = i0 + u * (int)blockDim.x;
       if (i < total) {
         const int sl = i / c8, c = i - sl * c8;
@@ -314,6 +324,8 @@ __global__ void __launch_bounds__(1024) plan_place_fused_kernel(int spb,
       }
     }
   }
+  PL_TRACE(5);
+#undef PL_TRACE
 }
 
 int launch_routing_plan(const uint32_t* expert, const uint8_t* finished, int64_t T, int k,
@@ -355,11 +367,38 @@ int launch_plan_from_counts(const uint32_t* expert, const uint8_t* finished, int
   const int64_t nblk = (S + spb - 1) / spb;
   if ((E + 1) * nblk <= kFusedScanMax && (cols % 8) == 0 && spb <= 1024) {
     const int threads = (int)std::max<int64_t>(kPlaceThreads, (spb + 31) / 32 * 32);
-    const size_t smem = ((E + 1) * 2 + 1 + (threads / 32) * (E + 1) + threads) * 4;
+    // tot | base | wcnt[warps] | pos | staged histogram [(E+1) x nblk]
+    const size_t smem = ((E + 1) * 2 + 1 + (threads / 32) * (E + 1) + threads + (E + 1) * (nblk + 1)) * 4;
+    if (smem > 48 * 1024) {
+      static size_t attr = 0;
+      if (smem > attr) {
+        MOE_CUDA_TRY(cudaFuncSetAttribute(plan_place_fused_kernel,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = smem;
+      }
+    }
+    static long long* dtr = nullptr;
+    const bool tr = std::getenv("MOE_GATE_TRACE") != nullptr && nblk <= 65536;
+    if (tr && !dtr) MOE_CUDA_TRY(cudaMalloc(&dtr, 8 * (16 + 2 * 65536)));
     plan_place_fused_kernel<<<(unsigned)nblk, threads, smem, st>>>(
         (int)spb, expert, finished, S, k, E, w.blockcnt, perm, inv, offsets, problems, active,
-        gather_src, cols, gather_dst, w.bad);
+        gather_src, cols, gather_dst, w.bad, tr ? dtr : nullptr);
     note_launch();
+    if (tr) {
+      std::vector<long long> h(16 + 2 * nblk);
+      cudaStreamSynchronize(st);
+      cudaMemcpy(h.data(), dtr, h.size() * 8, cudaMemcpyDeviceToHost);
+      long long lo = h[16], hi = h[17], sum = 0;
+      for (int64_t i = 0; i < nblk; ++i) {
+        lo = std::min(lo, h[16 + 2 * i]);
+        hi = std::max(hi, h[17 + 2 * i]);
+        sum += h[17 + 2 * i] - h[16 + 2 * i];
+      }
+      std::fprintf(stderr, "plan_place_fused grid=%lld threads=%d spb=%lld: span=%lld ns cta mean=%lld ns; "
+                   "cta0 clocks counts=%lld scan=%lld place=%lld gather=%lld\n",
+                   (long long)nblk, threads, (long long)spb, hi - lo, sum / nblk, h[1] - h[0],
+                   h[2] - h[1], h[3] - h[2], h[5] - h[3]);
+    }
     return check_launch("plan_place_fused");
   }
   plan_scan_kernel<<<1, 1024, 0, st>>>(w.blockcnt, nblk, E, w.blockbase, offsets, problems,

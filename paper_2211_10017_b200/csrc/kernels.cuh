@@ -45,7 +45,7 @@ struct GateFusedArgs {
   const uint16_t* x;
   int64_t T, d;
   const uint16_t *g, *b;
-  const float* gw32;  // (d, gwp) f32, zero-padded columns
+  const float* gw32;  // (d/2, gwp, 2) f32 k-pair interleaved, zero-padded experts
   int64_t gwp;
   const uint16_t* gb;
   int64_t E;
@@ -56,13 +56,10 @@ struct GateFusedArgs {
   uint16_t* scale;
   uint32_t* blockcnt;  // ceil(T/rows) * (E+1)
   uint32_t* bad_row;
-  int rows;            // gate_fused_rows(T, E, k)
+  int rows;            // ln_gate_rows(T, d, E, k)
 };
-int64_t gate_fused_pitch(int64_t E);  // f32 gate weight row pitch (multiple of 8)
-int gate_fused_rows(int64_t T, int64_t E, int k);  // rows per gate block (plan block = rows*k slots)
-bool gate_fused_supported(int64_t d, int64_t E, int k);
-int launch_gate_fused(const GateFusedArgs& a, cudaStream_t st);
-// k_ln_gate.cu: the same stage as ONE kernel (LN + logits + top-k + histogram)
+int64_t gate_fused_pitch(int64_t E);  // f32 gate weight pitch (multiple of 8)
+// k_ln_gate.cu: LN + logits + top-k + routing-key histogram, one kernel
 bool ln_gate_supported(int64_t T, int64_t d, int64_t E, int k);
 int ln_gate_rows(int64_t T, int64_t d, int64_t E, int k);  // rows per block (GateFusedArgs::rows)
 int launch_ln_gate(const GateFusedArgs& a, cudaStream_t st);

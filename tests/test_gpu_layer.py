@@ -147,10 +147,14 @@ def test_layer_decode_shapes(cuda, oracle, T):
 
 
 @pytest.mark.parametrize("E,d,T,k", [(8, 512, 4096, 2), (64, 1024, 600, 1), (128, 256, 300, 2),
-                                     (3, 40, 50, 3), (130, 64, 20, 1), (300, 32, 40, 2)])
+                                     (3, 40, 50, 3), (130, 64, 20, 1), (300, 32, 40, 2),
+                                     (32, 1024, 4096, 2), (64, 1024, 16384, 1), (8, 512, 1, 1),
+                                     (256, 2048, 700, 8)])
 def test_layer_fused_gate_routing_exact(cuda, oracle, E, d, T, k):
     """Fused LN+logits+top-k+histogram kernel (and the unfused fallback for
-    E > 128): routing identical to the oracle at BASELINE-like shapes."""
+    E > 256): routing identical to the oracle at BASELINE-like shapes --
+    f32-widened and fp16 LN chain forms, one and two waves of row blocks,
+    chunked and resident gate weights, E <= 16 and warp-per-row selection."""
     from oracle.oracle import random_layer
     lw = random_layer(d, 64, E, seed=E + d + T)
     rng = np.random.default_rng(T)
