@@ -37,6 +37,7 @@
 // activation tiles in L2.
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -65,7 +66,12 @@ struct Cfg {
   static constexpr int EPI = kEpiGroups * 4 * EPI_WBUF;
   // A stages: TS keeps as many 32-column stages as TMEM leaves beside the
   // accumulators (each dequant group then has >= 2 stages to run ahead)
-  static constexpr int NA = TS ? ((512 - 2 * BN) / 32 >= 4 ? 4 : 2) : 2;
+  // accumulators: double-buffered (the epilogue of tile i overlaps the
+  // mainloop of tile i+1) except TS with 256-token tiles, whose A ring
+  // needs the TMEM -- chosen for launches of at most one wave, where there
+  // is no next tile to overlap
+  static constexpr int NACC = (TS && BN > 224) ? 1 : 2;
+  static constexpr int NA = TS ? ((512 - NACC * BN) / 32 >= 4 ? 4 : 2) : 2;
   static constexpr int BUDGET = 220 * 1024 - EPI - NA * ABYTES;  // TMA stages
   static constexpr int NS0 = BUDGET / STAGE;
   static constexpr int NS = NS0 > 8 ? 8 : NS0;                   // TMA stages
@@ -77,9 +83,9 @@ struct Cfg {
   static constexpr int OFF_TMEMPTR = OFF_BAR + NBAR * 8;
   static constexpr int OFF_TABLE = OFF_TMEMPTR + 16;
   static constexpr int SMEM = OFF_TABLE + (kMaxProblems + 1) * 4 + 1024;  // + align slack
-  static constexpr int A_COL = 2 * BN;                           // TMEM: acc0 | acc1 | [TS: A ring]
+  static constexpr int A_COL = NACC * BN;                        // TMEM: acc0 | acc1 | [TS: A ring]
   static_assert(NS >= 2, "pipeline too shallow");
-  static_assert(2 * BN + (TS ? NA * 32 : 0) <= 512, "TMEM overflow");
+  static_assert(NACC * BN + (TS ? NA * 32 : 0) <= 512, "TMEM overflow");
   static_assert(BBYTES % 1024 == 0 && WBYTES % 1024 == 0, "stage alignment");
   static_assert(SMEM <= 227 * 1024, "shared memory");
 };
@@ -275,13 +281,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
       uint32_t it = 0, local = 0;
       for (uint32_t t = cid; t < ntiles; t += ncl, ++local) {
-        const int acc = local & 1;
+        const int acc = (int)(local % C::NACC);
         // a problem's last token tile is usually partial: the MMA N follows
         // the live rows (multiple of 16) so padding costs no tensor time
         const Tile Tt = decode(table, np, P.problems, t, nftg, BN, CL, rank);
         const uint32_t idesc =
             __shfl_sync(0xffffffffu, umma_idesc_f16(128 * CL, tile_n<BN, CL>(Tt)), 0);
-        mbar_wait(&tempty[acc], ((local >> 1) & 1) ^ 1);
+        mbar_wait(&tempty[acc], ((local / C::NACC) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tm + acc * BN;
         for (int64_t kb = 0; kb < P.nkb; ++kb, ++it) {
@@ -422,7 +428,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t cc = 0;  // chunks processed by this warp
     uint32_t local = 0;
     for (uint32_t t = cid; t < ntiles; t += ncl, ++local) {
-      const int acc = local & 1;
+      const int acc = (int)(local % C::NACC);
       const Tile T = decode(table, np, P.problems, t, nftg, BN, CL, rank);
       const int64_t col = T.ft * 128 + q * 32 + lane;
       float sc = 1.0f, bi = 0.0f;
@@ -430,7 +436,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (BITS != 16) sc = h2f(P.scales[T.e * P.n + col]);
         bi = h2f(P.bias[T.e * P.n + col]);
       }
-      mbar_wait(&tfull[acc], (local >> 1) & 1);
+      mbar_wait(&tfull[acc], (local / C::NACC) & 1);
       tc_fence_after();
       if (lane == 0 && ew == 0) TC_TRACE(6, local);
       // only the columns holding this tile's rows need draining
@@ -608,24 +614,36 @@ static int run_tc(const GemmArgs& a, cudaStream_t st) {
 
 template <int BITS>
 static int run_tc_bits(const GemmArgs& a, cudaStream_t st) {
-  // token-tile width from the expected rows per problem (wider MMAs amortise
-  // the per-instruction issue cost; narrower ones waste less on small
-  // experts).  Large problems run on CTA pairs (cta_group::2, M = 256) when
-  // the feature tiles pair up: 256-token tiles with A in shared memory or
-  // 224-token tiles with A in TMEM, whichever quantises into fewer pair
-  // waves x tile width.  Single CTAs otherwise (MOE_TC_PAIR=0 forces them).
+  // Large problems run on CTA pairs (cta_group::2, M = 256 features) when
+  // the feature tiles pair up.  Token-tile width, from B200 measurements
+  // (scripts/gpu_g52.sh / g53.sh; C2 and C4 routed and uniform):
+  //   * at most one wave of 256-token tiles: TS-256 with a single
+  //     accumulator (A in TMEM, MMA-bound k-blocks; nothing to overlap);
+  //   * big experts (>= 3 tiles of 256 rows): SS-256 (fewest tiles);
+  //   * otherwise TS-192 (4 A stages; the evenly split tiles of ~128-190
+  //     rows absorb the spread of routed expert sizes).
+  // Single CTAs below that (MOE_TC_PAIR=0 forces them; MOE_TC_BN forces a
+  // width: 128/160/192/224 TS, 256 SS, 257 TS single-accumulator).
   const int64_t nft = (a.n + 127) / 128;
-  if (a.rows_hint >= 160) {
-    static const int force = std::getenv("MOE_TC_BN") ? std::atoi(std::getenv("MOE_TC_BN")) : 0;
+  static const int force = std::getenv("MOE_TC_BN") ? std::atoi(std::getenv("MOE_TC_BN")) : 0;
+  if (a.rows_hint >= 96) {
     static const bool pair_ok = !(std::getenv("MOE_TC_PAIR") && std::atoi(std::getenv("MOE_TC_PAIR")) == 0);
     if (pair_ok && nft % 2 == 0) {
       const int64_t pairs = sm_count() / 2;
-      const int64_t w256 = (a.np * ((a.rows_hint + 255) / 256) * (nft / 2) + pairs - 1) / pairs;
-      const int64_t w224 = (a.np * ((a.rows_hint + 223) / 224) * (nft / 2) + pairs - 1) / pairs;
-      if (force == 224 || (force != 256 && w224 * 224 < w256 * 256))
-        return run_tc<BITS, 224, true, 2>(a, st);
-      return run_tc<BITS, 256, false, 2>(a, st);
+      const int64_t tiles256 = a.np * ((a.rows_hint + 255) / 256) * (nft / 2);
+      int bn = force;
+      if (bn == 0) bn = tiles256 <= pairs ? 257 : a.rows_hint >= 768 ? 256 : 192;
+      switch (bn) {
+        case 128: return run_tc<BITS, 128, true, 2>(a, st);
+        case 160: return run_tc<BITS, 160, true, 2>(a, st);
+        case 192: return run_tc<BITS, 192, true, 2>(a, st);
+        case 224: return run_tc<BITS, 224, true, 2>(a, st);
+        case 257: return run_tc<BITS, 256, true, 2>(a, st);
+        default: return run_tc<BITS, 256, false, 2>(a, st);
+      }
     }
+  }
+  if (a.rows_hint >= 160) {
     const int64_t tiles256 = a.np * ((a.rows_hint + 255) / 256) * nft;
     if (tiles256 <= sm_count() || force == 256) return run_tc<BITS, 256, false>(a, st);
     return run_tc<BITS, 224, true>(a, st);

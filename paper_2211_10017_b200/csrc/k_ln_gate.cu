@@ -127,6 +127,98 @@ __device__ __forceinline__ long long gtime() {
     }                                                                              \
   } while (0)
 
+// One weight chunk of the logit chains: inputs [0, kn) of the rows
+// xr + i*rstride (i < RPT; f32 when XF, else fp16) against the pair-blocked
+// weights wg.  Operands of KS inputs per step stream through a DEPTH-step
+// register ring with no branches in the loop body (a guarded load lets
+// ptxas sink it under the previous step's FMAs); loads past kn read padding
+// and are never used.  x arrives converted (f32 copy) when XF.
+template <int EPG, int RPT, int KS, int DEPTH, bool XF>
+__device__ __forceinline__ void logit_chunk(float2 (&acc)[RPT][EPG >= 2 ? EPG / 2 : 1],
+                                            const void* xr, int rstride, const float* wg,
+                                            int wstride, int kn) {
+  constexpr int NP = EPG >= 2 ? EPG / 2 : 1;
+  struct Step {
+    float x[RPT][KS];
+    uint32_t xh[RPT][KS / 2];
+    float w[KS][EPG];
+  };
+  auto load = [&](Step& o, int kk) {
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      if constexpr (XF) {
+        const float* p = reinterpret_cast<const float*>(xr) + (size_t)i * rstride + kk;
+#pragma unroll
+        for (int q = 0; q < KS; q += 4) {
+          const float4 v = *reinterpret_cast<const float4*>(p + q);
+          o.x[i][q] = v.x;
+          o.x[i][q + 1] = v.y;
+          o.x[i][q + 2] = v.z;
+          o.x[i][q + 3] = v.w;
+        }
+      } else {
+        const uint16_t* p = reinterpret_cast<const uint16_t*>(xr) + (size_t)i * rstride + kk;
+        if constexpr (KS == 8) {
+          const uint4 v = *reinterpret_cast<const uint4*>(p);
+          o.xh[i][0] = v.x;
+          o.xh[i][1] = v.y;
+          o.xh[i][2] = v.z;
+          o.xh[i][3] = v.w;
+        } else {
+          const uint2 v = *reinterpret_cast<const uint2*>(p);
+          o.xh[i][0] = v.x;
+          o.xh[i][1] = v.y;
+        }
+      }
+    }
+    const float* w0 = wg + (size_t)(kk >> 1) * wstride;
+#pragma unroll
+    for (int q = 0; q < KS; q += 2) {  // one input pair: 2 * EPG floats
+      const float* wq = w0 + (q >> 1) * wstride;
+#pragma unroll
+      for (int j = 0; j < EPG; j += 2) {  // experts e0+j, e0+j+1 x inputs q, q+1
+        const float4 w4 = *reinterpret_cast<const float4*>(wq + 2 * j);
+        o.w[q][j] = w4.x;
+        o.w[q][j + 1] = w4.y;
+        o.w[q + 1][j] = w4.z;
+        o.w[q + 1][j + 1] = w4.w;
+      }
+    }
+  };
+  auto fma_step = [&](const Step& o) {
+#pragma unroll
+    for (int q = 0; q < KS; ++q) {
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) {
+        float xq;
+        if constexpr (XF) {
+          xq = o.x[i][q];
+        } else {
+          const uint32_t hw = o.xh[i][q / 2];
+          xq = h2f((uint16_t)((q & 1) ? (hw >> 16) : (hw & 0xFFFFu)));
+        }
+#pragma unroll
+        for (int j = 0; j < NP; ++j)
+          acc[i][j] = g3::ffma2(xq, make_float2(o.w[q][2 * j], o.w[q][2 * j + 1]), acc[i][j]);
+      }
+    }
+  };
+  Step r[DEPTH];
+#pragma unroll
+  for (int d = 0; d < DEPTH; ++d) load(r[d], d * KS);
+  int kk = 0;
+  for (; kk + DEPTH * KS <= kn; kk += DEPTH * KS) {
+#pragma unroll
+    for (int d = 0; d < DEPTH; ++d) {
+      fma_step(r[d]);
+      load(r[d], kk + (DEPTH + d) * KS);
+    }
+  }
+#pragma unroll
+  for (int d = 0; d < DEPTH; ++d)  // remaining kn % (DEPTH * KS) inputs (multiple of 8)
+    if (kk + d * KS < kn) fma_step(r[d]);
+}
+
 template <int EPG, int RPT, int NT>
 __global__ void __launch_bounds__(NT, 1) ln_gate_kernel(
     const uint16_t* __restrict__ x, int64_t T, int d, const uint16_t* __restrict__ lng,
@@ -293,6 +385,11 @@ __global__ void __launch_bounds__(NT, 1) ln_gate_kernel(
       h[j] = f2h(__fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(h2f(h[j]), mean), inv), gg[j]), bb[j]));
     *reinterpret_cast<uint4*>(xs + (size_t)r * xp + c * 8) = v;
     *reinterpret_cast<uint4*>(xn + (r0 + r) * d + c * 8) = v;
+    if (C.wide) {  // f32 copy for the logit chains (no conversion on their path)
+      float4* dst = reinterpret_cast<float4*>(xf + (size_t)r * fp + c * 8);
+      dst[0] = make_float4(h2f(h[0]), h2f(h[1]), h2f(h[2]), h2f(h[3]));
+      dst[1] = make_float4(h2f(h[4]), h2f(h[5]), h2f(h[6]), h2f(h[7]));
+    }
   }
   __syncthreads();
   G3_TRACE(3);
@@ -310,10 +407,6 @@ __global__ void __launch_bounds__(NT, 1) ln_gate_kernel(
 #pragma unroll
     for (int j = 0; j < NP; ++j) acc[i][j] = make_float2(0.f, 0.f);
 
-  struct Step {
-    uint32_t xh[RPT][KS / 2];
-    float w[KS][EPG];
-  };
   for (int c = 0; c < C.nch; ++c) {
     const int s = c % C.ns;
     mbar_wait(&bars[1 + s], (uint32_t)((c / C.ns) & 1));
@@ -322,81 +415,13 @@ __global__ void __launch_bounds__(NT, 1) ln_gate_kernel(
       // inputs 2j, 2j+1 of experts e0.. are the contiguous floats
       // [j * 2 * gwp + 2 * e0, ... + 2 * EPG)
       const float* wg = reinterpret_cast<const float*>(sm + C.off_w + s * C.wslot) + 2 * e0;
-      const int wstride = 2 * gwp;  // floats per input pair
-      const uint16_t* xr = xs + (size_t)rg * xp + c * C.kc;
       const int kn = ::min(C.kc, d - c * C.kc);  // multiple of 8
-      auto load = [&](Step& o, int kk) {
-#pragma unroll
-        for (int i = 0; i < RPT; ++i) {
-          const uint16_t* p = xr + (size_t)i * C.nrg * xp + kk;
-          if constexpr (KS == 8) {
-            const uint4 v = *reinterpret_cast<const uint4*>(p);
-            o.xh[i][0] = v.x;
-            o.xh[i][1] = v.y;
-            o.xh[i][2] = v.z;
-            o.xh[i][3] = v.w;
-          } else {
-            const uint2 v = *reinterpret_cast<const uint2*>(p);
-            o.xh[i][0] = v.x;
-            o.xh[i][1] = v.y;
-          }
-        }
-        const float* w0 = wg + (size_t)(kk >> 1) * wstride;
-#pragma unroll
-        for (int q = 0; q < KS; q += 2) {  // one input pair: 2 * EPG floats
-          const float* wq = w0 + (q >> 1) * wstride;
-#pragma unroll
-          for (int j = 0; j < EPG; j += 2) {  // experts e0+j, e0+j+1 x inputs q, q+1
-            const float4 w4 = *reinterpret_cast<const float4*>(wq + 2 * j);
-            o.w[q][j] = w4.x;
-            o.w[q][j + 1] = w4.y;
-            o.w[q + 1][j] = w4.z;
-            o.w[q + 1][j + 1] = w4.w;
-          }
-        }
-      };
-      auto fma_step = [&](const Step& o) {
-#pragma unroll
-        for (int q = 0; q < KS; ++q) {
-#pragma unroll
-          for (int i = 0; i < RPT; ++i) {
-            const uint32_t hw = o.xh[i][q / 2];
-            const float xq = h2f((uint16_t)((q & 1) ? (hw >> 16) : (hw & 0xFFFFu)));
-            if constexpr (EPG >= 2) {
-#pragma unroll
-              for (int j = 0; j < NP; ++j)
-                acc[i][j] = g3::ffma2(xq, make_float2(o.w[q][2 * j], o.w[q][2 * j + 1]), acc[i][j]);
-            } else {
-              acc[i][0].x = fmaf(xq, o.w[q][0], acc[i][0].x);
-            }
-          }
-        }
-      };
-      if constexpr (KS == 8) {
-        // two-step ring over 16-input periods with no branches in the body
-        // (a guarded load keeps ptxas from hoisting it above the previous
-        // step's FMAs); loads past kn read padding and are never used
-        Step a, b;
-        load(a, 0);
-        load(b, 8);
-        int kk = 0;
-        for (; kk + 16 <= kn; kk += 16) {
-          fma_step(a);
-          load(a, kk + 16);
-          fma_step(b);
-          load(b, kk + 24);
-        }
-        if (kk < kn) fma_step(a);  // kn % 16 == 8
-      } else {  // FMA-dense threads: 2-deep ring of 4-input steps
-        Step a, b;
-        load(a, 0);
-        for (int kk = 0; kk < kn; kk += 8) {
-          load(b, kk + 4);
-          fma_step(a);
-          load(a, kk + 8);
-          fma_step(b);
-        }
-      }
+      if (C.wide)  // f32 copy of xn (written by the normalise pass)
+        logit_chunk<EPG, RPT, KS, (EPG * RPT <= 2 ? 4 : 2), true>(
+            acc, xf + (size_t)rg * fp + c * C.kc, C.nrg * fp, wg, 2 * gwp, kn);
+      else
+        logit_chunk<EPG, RPT, KS, 2, false>(acc, xs + (size_t)rg * xp + c * C.kc, C.nrg * xp,
+                                            wg, 2 * gwp, kn);
     }
     __syncthreads();  // slot s fully read
     if (c + C.ns < C.nch && tid < 32) {
