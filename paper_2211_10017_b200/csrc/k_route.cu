@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(1024) plan_place_fused_kernel(int spb,
   uint32_t* base = tot + keys + 1;    // [keys]  this block's first position per key
   uint32_t* wcnt = base + keys;       // [nwarp][keys]
   uint32_t* pos_l = wcnt + nwarp * keys;  // [blockDim]
-  uint32_t* cnt = pos_l + blockDim.x;     // [keys][nblk + 1] staged histogram
+  uint32_t* cnt = pos_l + blockDim.x;     // [keys][nblk + 1] staged histogram (then srow)
   const int64_t b = blockIdx.x;
   PL_TRACE(0);
   // this thread's slot key, loaded up front (overlaps the histogram loads)
@@ -230,10 +230,24 @@ __global__ void __launch_bounds__(1024) plan_place_fused_kernel(int spb,
   // 1. stage the whole (key x block) histogram (all loads in flight at once),
   //    then per key: total over all blocks and the count in blocks before b
   // (pitch nblk + 1: one thread per key walks its row without bank conflicts)
+  // (loads batched 8 per thread ahead of the stores: one L2 round trip,
+  // not one per element)
   const int ncnt = (int)(keys * nblk), cp = (int)nblk + 1;
-  for (int i = threadIdx.x; i < ncnt; i += blockDim.x) {
-    const int kk = i / (int)nblk;
-    cnt[kk * cp + (i - kk * (int)nblk)] = blockcnt[i];
+  for (int i0 = threadIdx.x; i0 < ncnt; i0 += 8 * (int)blockDim.x) {
+    uint32_t v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + u * (int)blockDim.x;
+      v[u] = i < ncnt ? blockcnt[i] : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + u * (int)blockDim.x;
+      if (i < ncnt) {
+        const int kk = i / (int)nblk;
+        cnt[kk * cp + (i - kk * (int)nblk)] = v[u];
+      }
+    }
   }
   for (int64_t i = threadIdx.x; i < nwarp * keys; i += blockDim.x) wcnt[i] = 0;
   __syncthreads();
@@ -296,6 +310,9 @@ __global__ void __launch_bounds__(1024) plan_place_fused_kernel(int spb,
     pos_l[threadIdx.x] = pos;
   }
   if (dst == nullptr) return;
+  // source row of each slot (one 64-bit division per slot, not per piece)
+  uint32_t* srow = cnt;  // the staged histogram is no longer needed
+  if (live) srow[threadIdx.x] = (uint32_t)(slot / k);
   __syncthreads();
   PL_TRACE(3);
   // 4. gather dst[pos] = src[slot / k]: 16-byte pieces, 8 loads in flight per
@@ -303,7 +320,8 @@ __global__ void __launch_bounds__(1024) plan_place_fused_kernel(int spb,
   //    than the copy)
   const int nslots = (int)::min((int64_t)spb, S - b * spb);
   const int c8 = (int)(cols / 8), total = nslots * c8;
-  const int64_t slot0 = b * spb;
+  const bool pow2 = (c8 & (c8 - 1)) == 0;
+  const int sh_c8 = __ffs(c8) - 1;
   constexpr int U = 8;
   for (int i0 = threadIdx.x; i0 < total; i0 += U * (int)blockDim.x) {
     uint4 v[U];
@@ -311,15 +329,15 @@ __global__ void __launch_bounds__(1024) plan_place_fused_kernel(int spb,
     for (int u = 0; u < U; ++u) {
       const int i = i0 + u * (int)blockDim.x;
       if (i < total) {
-        const int sl = i / c8, c = i - sl * c8;
-        v[u] = reinterpret_cast<const uint4*>(src + ((slot0 + sl) / k) * cols)[c];
+        const int sl = pow2 ? i >> sh_c8 : i / c8, c = i - sl * c8;
+        v[u] = reinterpret_cast<const uint4*>(src + (int64_t)srow[sl] * cols)[c];
       }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int i = i0 + u * (int)blockDim.x;
       if (i < total) {
-        const int sl = i / c8, c = i - sl * c8;
+        const int sl = pow2 ? i >> sh_c8 : i / c8, c = i - sl * c8;
         reinterpret_cast<uint4*>(dst + (int64_t)pos_l[sl] * cols)[c] = v[u];
       }
     }
@@ -368,7 +386,8 @@ int launch_plan_from_counts(const uint32_t* expert, const uint8_t* finished, int
   if ((E + 1) * nblk <= kFusedScanMax && (cols % 8) == 0 && spb <= 1024) {
     const int threads = (int)std::max<int64_t>(kPlaceThreads, (spb + 31) / 32 * 32);
     // tot | base | wcnt[warps] | pos | staged histogram [(E+1) x nblk]
-    const size_t smem = ((E + 1) * 2 + 1 + (threads / 32) * (E + 1) + threads + (E + 1) * (nblk + 1)) * 4;
+    const size_t smem = ((E + 1) * 2 + 1 + (threads / 32) * (E + 1) + threads +
+                         std::max<int64_t>((E + 1) * (nblk + 1), threads)) * 4;
     if (smem > 48 * 1024) {
       static size_t attr = 0;
       if (smem > attr) {
