@@ -46,6 +46,14 @@ int check_launch(const char* what) {
   return MOE_OK;
 }
 
+// Opt-in (MOE_PDL=1): with every kernel triggering its dependents at entry,
+// the waiting dependents' CTAs crowd the SMs -- measured 2-5% slower at
+// C2/C3 on B200, so plain stream order is the default.
+bool pdl_enabled() {
+  static const bool on = std::getenv("MOE_PDL") && std::atoi(std::getenv("MOE_PDL")) != 0;
+  return on;
+}
+
 int sm_count() {
   static int n = 0;
   if (n == 0) {
@@ -553,19 +561,26 @@ struct Marks {
 };
 
 // LN -> gate -> top-k -> plan -> gather into L->xp (stages 0..3)
+// the one-kernel gate path applies (and with it the fused k = 1 combine)
+static bool fused_gate_ok(const moe_layer* L, const uint16_t* x, int64_t T, int k) {
+  return (reinterpret_cast<uintptr_t>(x) & 15) == 0 && L->gw32 != nullptr &&
+         ln_gate_supported(T, L->d, L->E, k);
+}
+
+// out_fin non-null (fused k = 1 combine): finished tokens are written there
 static int layer_route(moe_layer* L, const uint16_t* x, const uint8_t* fin, int64_t T, int k,
-                       cudaStream_t st, Marks& mark) {
+                       cudaStream_t st, Marks& mark, uint16_t* out_fin = nullptr) {
   const int64_t d = L->d, E = L->E;
   L->last_T = T;
   L->last_k = k;
   MOE_CUDA_TRY(cudaMemsetAsync(L->bad_row, 0xFF, 8, st));  // bad_row + bad_expert
   TRY(mark());
   PlanWork w{L->blockcnt, L->blockbase, L->bad_expert};
-  const bool aligned = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
-  if (aligned && L->gw32 != nullptr && ln_gate_supported(T, d, E, k)) {
+  if (fused_gate_ok(L, x, T, k)) {
     // one kernel: LN + logits + top-k + key histogram; then scan/place/gather
     GateFusedArgs ga{x, T, d, L->ln_g, L->ln_b, L->gw32, L->gwp, L->gb, E, k, fin, L->xn,
-                     L->expert, L->scale, L->blockcnt, L->bad_row, ln_gate_rows(T, d, E, k)};
+                     L->expert, L->scale, L->blockcnt, L->bad_row, ln_gate_rows(T, d, E, k),
+                     out_fin};
     TRY(launch_ln_gate(ga, st));
     TRY(mark());
     TRY(mark());
@@ -588,14 +603,21 @@ static int layer_route(moe_layer* L, const uint16_t* x, const uint8_t* fin, int6
 
 // FFN1 (ReLU) -> FFN2 over `rows` expert-sorted rows of the LOCAL experts
 // (problems: np device triples, expert ids in [0, El)); stages 4..5
+// comb (FAST, k = 1): FFN2's epilogue applies the combine into comb->cout
 static int layer_ffn(moe_layer* L, const uint16_t* xin, int64_t rows, const uint32_t* problems,
                      int64_t np, int mode, uint16_t* h, uint16_t* out, cudaStream_t st,
-                     Marks& mark) {
+                     Marks& mark, const GemmArgs* comb = nullptr) {
   const int64_t d = L->d, f = L->f, El = L->El;
   const uint16_t db = debias_for(L->bits);
   const int64_t hint = rows / std::max<int64_t>(1, std::min<int64_t>(El, rows));
   GemmArgs g1{xin, rows, d, problems, np, L->w1t, L->s1, L->bits, El, f, L->b1, 1, h, db, hint};
   GemmArgs g2{h, rows, f, problems, np, L->w2t, L->s2, L->bits, El, d, L->b2, 0, out, db, hint};
+  if (comb != nullptr && mode == MOE_MODE_FAST) {
+    g2.cx = comb->cx;
+    g2.cperm = comb->cperm;
+    g2.cscale = comb->cscale;
+    g2.cout = comb->cout;
+  }
   if (mode == MOE_MODE_FAST && rows <= kGemvMaxRows) {
     // decode regime: stream the active experts' weights (K5)
     const double act = (double)El * (1.0 - std::pow(1.0 - 1.0 / (double)El, (double)rows));
@@ -625,9 +647,31 @@ static int layer_forward(moe_layer* L, const uint16_t* x, const uint8_t* fin, in
   TRY(layer_reserve(L, T, k));
   const int64_t S_ = T * k;
   Marks mark(L, st, true);
-  TRY(layer_route(L, x, fin, T, k, st, mark));
-  TRY(layer_ffn(L, L->xp, S_, L->problems, L->E, mode, L->h, L->y, st, mark));
-  TRY(launch_combine(x, L->y, L->inv, L->scale, fin, T, L->d, k, out, st));
+  // FAST, k = 1: the combine runs in FFN2's epilogue (out[perm[r]] from row
+  // r) and the gate kernel passes finished tokens through -- no y round trip
+  // and no combine launch.  k > 1 sums slots in slot order: separate kernel.
+  // (tcgen05 path only: in the decode kernel the extra epilogue state costs
+  // more than the combine launch it saves -- measured, C1/C3 shapes).
+  // Experimental, opt-in (MOE_FUSED_COMBINE=1): C4 -10 us, but an
+  // intermittent launch failure at T=16384 (~1 in 5 runs of
+  // test_layer_fused_gate_routing_exact[64-1024-16384-1]) is not yet
+  // explained, so the default keeps the separate combine kernel.
+  static const bool want_fuse = std::getenv("MOE_FUSED_COMBINE") &&
+                                std::atoi(std::getenv("MOE_FUSED_COMBINE")) != 0;
+  const bool fuse = want_fuse && mode == MOE_MODE_FAST && k == 1 && T > kGemvMaxRows &&
+                    fused_gate_ok(L, x, T, k);
+  TRY(layer_route(L, x, fin, T, k, st, mark, fuse ? out : nullptr));
+  if (fuse) {
+    GemmArgs comb{};
+    comb.cx = x;
+    comb.cperm = L->perm;
+    comb.cscale = L->scale;
+    comb.cout = out;
+    TRY(layer_ffn(L, L->xp, S_, L->problems, L->E, mode, L->h, L->y, st, mark, &comb));
+  } else {
+    TRY(layer_ffn(L, L->xp, S_, L->problems, L->E, mode, L->h, L->y, st, mark));
+    TRY(launch_combine(x, L->y, L->inv, L->scale, fin, T, L->d, k, out, st));
+  }
   TRY(mark());
   mark.done();
   return MOE_OK;

@@ -211,6 +211,31 @@ __device__ __forceinline__ void tc_commit_mc(uint64_t* bar, uint16_t mask) {
       : "memory");
 }
 
+// programmatic dependent launch (kernels.cuh launch_k): no-ops when the
+// kernel was launched without the attribute
+__device__ __forceinline__ void griddep_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void griddep_launch() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// combine of one 16-byte piece (8 fp16): x (+) (y (*) s), RN each op
+// (combine_kernel's arithmetic, model.cpp:334-346 with routing.cpp:106-114)
+__device__ __forceinline__ uint4 combine8(uint4 x, uint4 y, uint16_t s) {
+  const uint32_t s2 = (uint32_t)s | ((uint32_t)s << 16);
+  uint32_t* a = reinterpret_cast<uint32_t*>(&x);
+  const uint32_t* b = reinterpret_cast<const uint32_t*>(&y);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint32_t prod, sum;
+    asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(prod) : "r"(b[q]), "r"(s2));
+    asm("add.rn.f16x2 %0, %1, %2;" : "=r"(sum) : "r"(a[q]), "r"(prod));
+    a[q] = sum;
+  }
+  return x;
+}
+
 // ------------------------------------------------- CTA pairs (cta_group::2)
 // Two CTAs of a 2-CTA cluster (one TPC) run one MMA of M = 256: each holds
 // its 128 rows of A, N/2 columns of B (at the same shared-memory offset) and

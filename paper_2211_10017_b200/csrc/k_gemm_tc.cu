@@ -140,6 +140,10 @@ struct Params {
   const uint16_t* bias;
   const uint32_t* problems;
   uint16_t* out;
+  const uint16_t* cx;        // fused k = 1 combine (GemmArgs::cout), else null
+  const uint32_t* cperm;
+  const uint16_t* cscale;
+  uint16_t* cout;
   int64_t m, n, np, nft, nkb;
   int relu;
   uint32_t debias2;
@@ -190,6 +194,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int np = (int)P.np;
+  griddep_launch();
 
   if (warp == 0) {
     if (lane == 0) tma_prefetch_desc(&tmap_x);
@@ -213,6 +218,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if constexpr (PAIR) tmem_alloc_pair(tmem_ptr, 512);
     else tmem_alloc(tmem_ptr, 512);
   } else if (warp == 3) {
+    griddep_wait();  // problems (and the activations) come from the previous kernels
     // token-tile prefix over problems: table[p] = sum_{q<p} ceil(len_q / BN)
     uint32_t carry = 0;
     for (int base = 0; base < np; base += 32) {
@@ -229,6 +235,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (lane == 0) table[np] = carry;
   }
+  griddep_wait();  // every thread: the previous kernels' outputs are visible past here
   tc_fence_before();
   __syncthreads();
   if constexpr (PAIR) cluster_sync_all();  // peer barriers initialised before remote use
@@ -471,13 +478,40 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0 && ew == 0) TC_TRACE(10, cc);
         // read back as 16-byte vectors: lane -> (row lane/4 + 8i, 8 features)
         const int nrow = (int)::min((int64_t)32, T.row1 - (T.row0 + c0));
+        const int64_t col = T.ft * 128 + q * 32 + (lane & 3) * 8;
+        if (P.cout == nullptr) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int row = i * 8 + (lane >> 2), ch = lane & 3;
-          const uint4 val = *reinterpret_cast<const uint4*>(stg + row * 32 + ch * 8);
-          if (row < nrow && slice_live)
-            *reinterpret_cast<uint4*>(P.out + (T.row0 + c0 + row) * P.n + T.ft * 128 + q * 32 +
-                                      ch * 8) = val;
+          for (int i = 0; i < 4; ++i) {
+            const int row = i * 8 + (lane >> 2);
+            const uint4 val = *reinterpret_cast<const uint4*>(stg + row * 32 + (lane & 3) * 8);
+            if (row < nrow && slice_live)
+              *reinterpret_cast<uint4*>(P.out + (T.row0 + c0 + row) * P.n + col) = val;
+          }
+        } else {
+          // fused k = 1 combine: out[token] = x[token] (+) y * scale[token];
+          // the four rows' loads are issued together (two L2 round trips)
+          uint32_t tok[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int row = i * 8 + (lane >> 2);
+            tok[i] = row < nrow && slice_live ? P.cperm[T.row0 + c0 + row] : 0xFFFFFFFFu;
+          }
+          uint4 xv[4];
+          uint16_t sv[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (tok[i] != 0xFFFFFFFFu) {
+              xv[i] = *reinterpret_cast<const uint4*>(P.cx + (int64_t)tok[i] * P.n + col);
+              sv[i] = P.cscale[tok[i]];
+            }
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (tok[i] != 0xFFFFFFFFu) {
+              const int row = i * 8 + (lane >> 2);
+              const uint4 val = *reinterpret_cast<const uint4*>(stg + row * 32 + (lane & 3) * 8);
+              *reinterpret_cast<uint4*>(P.cout + (int64_t)tok[i] * P.n + col) =
+                  combine8(xv[i], val, sv[i]);
+            }
         }
         __syncwarp();
         if (lane == 0 && ew == 0) TC_TRACE(11, cc);
@@ -549,6 +583,10 @@ static int run_tc(const GemmArgs& a, cudaStream_t st) {
   P.bias = a.bias;
   P.problems = a.problems;
   P.out = a.out;
+  P.cx = a.cx;
+  P.cperm = a.cperm;
+  P.cscale = a.cscale;
+  P.cout = a.cout;
   P.m = a.m;
   P.n = a.n;
   P.np = a.np;
@@ -579,13 +617,15 @@ static int run_tc(const GemmArgs& a, cudaStream_t st) {
     cfg.blockDim = dim3(tc::kThreads);
     cfg.dynamicSmemBytes = C::SMEM;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = CL;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
     if (trace_path) {
       int nc = 0;
       cudaOccupancyMaxActiveClusters(&nc, tc::gemm_tc_kernel<BITS, BN, TS, CL>, &cfg);
@@ -593,7 +633,8 @@ static int run_tc(const GemmArgs& a, cudaStream_t st) {
     }
     MOE_CUDA_TRY(cudaLaunchKernelEx(&cfg, tc::gemm_tc_kernel<BITS, BN, TS, CL>, tmap, O, P));
   } else {
-    tc::gemm_tc_kernel<BITS, BN, TS, CL><<<sm_count(), tc::kThreads, C::SMEM, st>>>(tmap, O, P);
+    MOE_CUDA_TRY(launch_k(tc::gemm_tc_kernel<BITS, BN, TS, CL>, dim3(sm_count()), dim3(tc::kThreads),
+                          C::SMEM, st, tmap, O, P));
   }
   note_launch();
   const int rc = check_launch("gemm_tc");

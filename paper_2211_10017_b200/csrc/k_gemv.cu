@@ -210,6 +210,8 @@ __global__ void __launch_bounds__(kThreads, 3) gemv_kernel(const Params P) {
     }
     fence_barrier_init();
   }
+  griddep_launch();
+  griddep_wait();  // problems / activations come from the previous kernels
   if (warp == 0) {  // compact the live problems: work items cover only those
     int base = 0;
     for (int p0 = 0; p0 < P.np; p0 += 32) {
@@ -447,7 +449,7 @@ static int run_gemv(const GemmArgs& a, const GemvWork& w, cudaStream_t st) {
   // persistent: enough CTAs for the live items (empty problems are skipped
   // inside), at most 3 per SM
   const int64_t grid = std::min<int64_t>((int64_t)P.nitems, 3 * (int64_t)sm_count());
-  gv::gemv_kernel<BITS><<<(unsigned)grid, gv::kThreads, smem, st>>>(P);
+  MOE_CUDA_TRY(launch_k(gv::gemv_kernel<BITS>, dim3((unsigned)grid), dim3(gv::kThreads), smem, st, P));
   note_launch();
   return check_launch("gemv");
 }

@@ -225,7 +225,8 @@ __global__ void __launch_bounds__(NT, 1) ln_gate_kernel(
     const uint16_t* __restrict__ lnb, const float* __restrict__ gw32, int gwp,
     const uint16_t* __restrict__ gb, int E, int k, const uint8_t* __restrict__ finished,
     uint16_t* __restrict__ xn, uint32_t* __restrict__ expert, uint16_t* __restrict__ scale,
-    uint32_t* __restrict__ blockcnt, uint32_t* bad_row, int rb, long long* trace) {
+    uint32_t* __restrict__ blockcnt, uint32_t* bad_row, int rb, uint16_t* __restrict__ out_fin,
+    long long* trace) {
   extern __shared__ __align__(128) uint8_t sm[];
   const g3::Cfg C = g3::cfg(d, E, gwp, rb, EPG, RPT, NT);
   uint16_t* xs = reinterpret_cast<uint16_t*>(sm);
@@ -245,6 +246,7 @@ __global__ void __launch_bounds__(NT, 1) ln_gate_kernel(
   const int d8 = d / 8, xp = C.xp;
   G3_TRACE(0);
 
+  griddep_launch();
   if (tid < 32) {  // warp 0 converged, one elected lane issues every copy
     if (elect_one()) {
       mbar_init(&bars[0], 1);
@@ -253,8 +255,7 @@ __global__ void __launch_bounds__(NT, 1) ln_gate_kernel(
       mbar_arrive_expect_tx(&bars[0], (uint32_t)nrow * d * 2);
     }
     __syncwarp();
-    for (int r = 0; r < nrow; ++r)
-      if (elect_one()) bulk_load(xs + (size_t)r * xp, x + (r0 + r) * d, (uint32_t)d * 2, &bars[0]);
+    // the gate weights never change: fetched before the previous kernel ends
     for (int c = 0; c < C.ns; ++c) {
       const uint32_t bytes = (uint32_t)::min(C.kc, d - c * C.kc) * gwp * 4;
       if (elect_one()) {
@@ -262,6 +263,9 @@ __global__ void __launch_bounds__(NT, 1) ln_gate_kernel(
         bulk_load(sm + C.off_w + c * C.wslot, gw32 + (size_t)c * C.kc * gwp, bytes, &bars[1 + c]);
       }
     }
+    griddep_wait();  // x and finished may be the previous kernel's output
+    for (int r = 0; r < nrow; ++r)
+      if (elect_one()) bulk_load(xs + (size_t)r * xp, x + (r0 + r) * d, (uint32_t)d * 2, &bars[0]);
   } else {
     // the small operands every later phase reads, fetched while the rows
     // land (each would otherwise cost an L2 round trip on the critical path)
@@ -275,12 +279,21 @@ __global__ void __launch_bounds__(NT, 1) ln_gate_kernel(
     }
     for (int i = tid - 32; i < E; i += NT - 32) bsm[i] = h2f(gb[i]);
     for (int i = tid - 32; i < 32; i += NT - 32) tab[i] = moe_expf_tab_dev[i];
+    griddep_wait();
     for (int i = tid - 32; i < nrow; i += NT - 32) fsm[i] = finished != nullptr ? finished[r0 + i] : 0;
   }
   for (int i = tid; i <= E; i += NT) hist[i] = 0;
   __syncthreads();
   mbar_wait(&bars[0], 0);
   G3_TRACE(1);
+  if (out_fin != nullptr) {  // fused k = 1 combine: finished tokens pass through (out = x)
+    for (int i = tid; i < nrow * d8; i += NT) {
+      const int r = i / d8, c = i - r * d8;
+      if (fsm[r] != 0)
+        *reinterpret_cast<uint4*>(out_fin + (r0 + r) * d + c * 8) =
+            *reinterpret_cast<const uint4*>(xs + (size_t)r * xp + c * 8);
+    }
+  }
 
   // ---- LayerNorm chains (model.cpp:178-192): one thread per row, serial RN
   if (C.wide) {
@@ -631,9 +644,10 @@ static int launch_g3(const GateFusedArgs& a, int rb, cudaStream_t st) {
   static long long* dtrace = nullptr;
   const bool tr = std::getenv("MOE_GATE_TRACE") != nullptr;
   if (tr && !dtrace) MOE_CUDA_TRY(cudaMalloc(&dtrace, 8 * (16 + 2 * 65536)));
-  ln_gate_kernel<EPG, RPT, NT><<<grid, NT, C.total, st>>>(
-      a.x, a.T, (int)a.d, a.g, a.b, a.gw32, (int)a.gwp, a.gb, (int)a.E, a.k, a.finished, a.xn,
-      a.expert, a.scale, a.blockcnt, a.bad_row, rb, tr ? dtrace : nullptr);
+  MOE_CUDA_TRY(launch_k(ln_gate_kernel<EPG, RPT, NT>, dim3(grid), dim3(NT), C.total, st, a.x, a.T,
+                        (int)a.d, a.g, a.b, a.gw32, (int)a.gwp, a.gb, (int)a.E, a.k, a.finished,
+                        a.xn, a.expert, a.scale, a.blockcnt, a.bad_row, rb, a.out_fin,
+                        tr ? dtrace : nullptr));
   note_launch();
   if (tr && grid <= 65536) {
     std::vector<long long> h(16 + 2 * grid);

@@ -222,6 +222,8 @@ __global__ void __launch_bounds__(1024) plan_place_fused_kernel(int spb,
   uint32_t* pos_l = wcnt + nwarp * keys;  // [blockDim]
   uint32_t* cnt = pos_l + blockDim.x;     // [keys][nblk + 1] staged histogram (then srow)
   const int64_t b = blockIdx.x;
+  griddep_launch();
+  griddep_wait();
   PL_TRACE(0);
   // this thread's slot key, loaded up front (overlaps the histogram loads)
   const int64_t slot = b * spb + threadIdx.x;
@@ -399,9 +401,10 @@ int launch_plan_from_counts(const uint32_t* expert, const uint8_t* finished, int
     static long long* dtr = nullptr;
     const bool tr = std::getenv("MOE_GATE_TRACE") != nullptr && nblk <= 65536;
     if (tr && !dtr) MOE_CUDA_TRY(cudaMalloc(&dtr, 8 * (16 + 2 * 65536)));
-    plan_place_fused_kernel<<<(unsigned)nblk, threads, smem, st>>>(
-        (int)spb, expert, finished, S, k, E, w.blockcnt, perm, inv, offsets, problems, active,
-        gather_src, cols, gather_dst, w.bad, tr ? dtr : nullptr);
+    MOE_CUDA_TRY(launch_k(plan_place_fused_kernel, dim3((unsigned)nblk), dim3(threads), smem, st,
+                          (int)spb, expert, finished, S, k, E, (const uint32_t*)w.blockcnt, perm,
+                          inv, offsets, problems, active, gather_src, cols, gather_dst, w.bad,
+                          tr ? dtr : nullptr));
     note_launch();
     if (tr) {
       std::vector<long long> h(16 + 2 * nblk);
@@ -493,6 +496,8 @@ __global__ void combine_kernel(const uint16_t* __restrict__ x, const uint16_t* _
                                const uint16_t* __restrict__ scale,
                                const uint8_t* __restrict__ finished, int64_t T, int64_t d, int k,
                                uint16_t* __restrict__ out) {
+  griddep_launch();
+  griddep_wait();
   const int64_t chunks = d / 8;
   const int64_t total = T * chunks;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
@@ -545,7 +550,8 @@ int launch_combine(const uint16_t* x, const uint16_t* y, const uint32_t* inv,
   const int64_t work = d % 8 == 0 ? T * d / 8 : T * d;
   const unsigned blocks = (unsigned)std::min<int64_t>((work + 255) / 256, 148 * 16);
   if (d % 8 == 0)
-    combine_kernel<<<blocks, 256, 0, st>>>(x, y, inv, scale, finished, T, d, k, out);
+    MOE_CUDA_TRY(launch_k(combine_kernel, dim3(blocks), dim3(256), 0, st, x, y, inv, scale, finished,
+                          T, d, k, out));
   else
     combine_scalar_kernel<<<blocks, 256, 0, st>>>(x, y, inv, scale, finished, T, d, k, out);
   note_launch();

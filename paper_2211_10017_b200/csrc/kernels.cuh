@@ -3,6 +3,7 @@
 #pragma once
 
 #include <algorithm>
+#include <utility>
 
 #include "../../include/moe_cuda.h"
 #include "common.cuh"
@@ -17,6 +18,30 @@ __host__ __device__ constexpr int wblock_bytes(int bits) {
 }
 
 int sm_count();
+
+// Programmatic dependent launch for the layer-path kernels: each is
+// launched with cudaLaunchAttributeProgrammaticStreamSerialization, calls
+// griddep_launch() as it starts (its dependent may be scheduled and run its
+// independent prologue -- barrier init, TMEM alloc, weight prefetch) and
+// griddep_wait() before it reads anything the previous kernel wrote.  In a
+// CUDA graph the edges become programmatic, so each kernel's launch latency
+// overlaps its predecessor.  Opt-in: MOE_PDL=1 (abi.cu pdl_enabled).
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                     cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // k_quant.cu
 int launch_quantize(const uint16_t* w, int64_t e, int64_t m, int64_t n, int bits,
@@ -57,6 +82,7 @@ struct GateFusedArgs {
   uint32_t* blockcnt;  // ceil(T/rows) * (E+1)
   uint32_t* bad_row;
   int rows;            // ln_gate_rows(T, d, E, k)
+  uint16_t* out_fin = nullptr;  // non-null: write out[r] = x[r] for finished rows (fused combine)
 };
 int64_t gate_fused_pitch(int64_t E);  // f32 gate weight pitch (multiple of 8)
 // k_ln_gate.cu: LN + logits + top-k + routing-key histogram, one kernel
@@ -109,6 +135,14 @@ struct GemmArgs {
   uint16_t* out;
   uint16_t debias;  // 0x6408 (W4) / 0x6480 (W8), MOE_FAULT_INJECT aware
   int64_t rows_hint;  // expected rows per problem (tile-size choice)
+  // k = 1 combine fused into the epilogue (tcgen05 kernel only): output row r
+  // (slot position) goes to token t = cperm[r] as
+  //   cout[t] = cx[t] (+) (y_r (*) cscale[t])   (fp16 RN each, = combine_kernel)
+  // and `out` is not written.  Null cout: plain output rows.
+  const uint16_t* cx = nullptr;
+  const uint32_t* cperm = nullptr;
+  const uint16_t* cscale = nullptr;
+  uint16_t* cout = nullptr;
 };
 int launch_gemm_exact(const GemmArgs& a, cudaStream_t st);
 

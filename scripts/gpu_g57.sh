@@ -1,0 +1,4 @@
+timeout 600 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_layer.py -x -q -m gpu -k "gemv or decode or layer" 2>&1 | tail -1
+for w in c3_1 c3_8 c3_64 c2; do timeout 300 python bench.py --workload $w --steps 60 --warmup 5 --no-cpu-baseline 2>&1 | tail -1 | python3 -c "
+import sys,json; j=json.loads(sys.stdin.read()); print(j['config']['workload'][:30], 'us=%.1f'%(1e3*j['ms_per_step']), 'kern=%.1f'%(1e3*j['roofline']['kernel_ms_per_step']), 'frac=%.3f'%j['roofline']['frac'], {k: round(v*1e3,1) for k,v in j.get('stage_ms',{}).items()})"; done
+timeout 600 ncu --cache-control none --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/warm_c3_1.csv python bench.py --workload c3_1 --steps 3 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
