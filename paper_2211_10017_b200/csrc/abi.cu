@@ -46,12 +46,13 @@ int check_launch(const char* what) {
   return MOE_OK;
 }
 
-// Opt-in (MOE_PDL=1): with every kernel triggering its dependents at entry,
-// the waiting dependents' CTAs crowd the SMs -- measured 2-5% slower at
-// C2/C3 on B200, so plain stream order is the default.
-bool pdl_enabled() {
-  static const bool on = std::getenv("MOE_PDL") && std::atoi(std::getenv("MOE_PDL")) != 0;
-  return on;
+// Opt-in (MOE_PDL=1 all layer kernels, MOE_PDL=2 the GEMMs only): with
+// every kernel triggering its dependents at entry, the parked dependent
+// CTAs crowd the SMs -- measured 2-5% slower at C2/C3 on B200 for "all", so
+// plain stream order is the default.
+bool pdl_enabled(int kind) {
+  static const int mode = std::getenv("MOE_PDL") ? std::atoi(std::getenv("MOE_PDL")) : 0;
+  return mode == 1 || (mode == 2 && kind == 1);
 }
 
 int sm_count() {

@@ -449,7 +449,7 @@ static int run_gemv(const GemmArgs& a, const GemvWork& w, cudaStream_t st) {
   // persistent: enough CTAs for the live items (empty problems are skipped
   // inside), at most 3 per SM
   const int64_t grid = std::min<int64_t>((int64_t)P.nitems, 3 * (int64_t)sm_count());
-  MOE_CUDA_TRY(launch_k(gv::gemv_kernel<BITS>, dim3((unsigned)grid), dim3(gv::kThreads), smem, st, P));
+  MOE_CUDA_TRY(launch_k(0, gv::gemv_kernel<BITS>, dim3((unsigned)grid), dim3(gv::kThreads), smem, st, P));
   note_launch();
   return check_launch("gemv");
 }

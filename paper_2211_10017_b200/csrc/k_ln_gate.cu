@@ -644,7 +644,7 @@ static int launch_g3(const GateFusedArgs& a, int rb, cudaStream_t st) {
   static long long* dtrace = nullptr;
   const bool tr = std::getenv("MOE_GATE_TRACE") != nullptr;
   if (tr && !dtrace) MOE_CUDA_TRY(cudaMalloc(&dtrace, 8 * (16 + 2 * 65536)));
-  MOE_CUDA_TRY(launch_k(ln_gate_kernel<EPG, RPT, NT>, dim3(grid), dim3(NT), C.total, st, a.x, a.T,
+  MOE_CUDA_TRY(launch_k(0, ln_gate_kernel<EPG, RPT, NT>, dim3(grid), dim3(NT), C.total, st, a.x, a.T,
                         (int)a.d, a.g, a.b, a.gw32, (int)a.gwp, a.gb, (int)a.E, a.k, a.finished,
                         a.xn, a.expert, a.scale, a.blockcnt, a.bad_row, rb, a.out_fin,
                         tr ? dtrace : nullptr));

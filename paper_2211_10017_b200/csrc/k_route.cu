@@ -401,7 +401,7 @@ int launch_plan_from_counts(const uint32_t* expert, const uint8_t* finished, int
     static long long* dtr = nullptr;
     const bool tr = std::getenv("MOE_GATE_TRACE") != nullptr && nblk <= 65536;
     if (tr && !dtr) MOE_CUDA_TRY(cudaMalloc(&dtr, 8 * (16 + 2 * 65536)));
-    MOE_CUDA_TRY(launch_k(plan_place_fused_kernel, dim3((unsigned)nblk), dim3(threads), smem, st,
+    MOE_CUDA_TRY(launch_k(0, plan_place_fused_kernel, dim3((unsigned)nblk), dim3(threads), smem, st,
                           (int)spb, expert, finished, S, k, E, (const uint32_t*)w.blockcnt, perm,
                           inv, offsets, problems, active, gather_src, cols, gather_dst, w.bad,
                           tr ? dtr : nullptr));
@@ -550,7 +550,7 @@ int launch_combine(const uint16_t* x, const uint16_t* y, const uint32_t* inv,
   const int64_t work = d % 8 == 0 ? T * d / 8 : T * d;
   const unsigned blocks = (unsigned)std::min<int64_t>((work + 255) / 256, 148 * 16);
   if (d % 8 == 0)
-    MOE_CUDA_TRY(launch_k(combine_kernel, dim3(blocks), dim3(256), 0, st, x, y, inv, scale, finished,
+    MOE_CUDA_TRY(launch_k(0, combine_kernel, dim3(blocks), dim3(256), 0, st, x, y, inv, scale, finished,
                           T, d, k, out));
   else
     combine_scalar_kernel<<<blocks, 256, 0, st>>>(x, y, inv, scale, finished, T, d, k, out);

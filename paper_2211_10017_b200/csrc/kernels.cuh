@@ -26,9 +26,11 @@ int sm_count();
 // griddep_wait() before it reads anything the previous kernel wrote.  In a
 // CUDA graph the edges become programmatic, so each kernel's launch latency
 // overlaps its predecessor.  Opt-in: MOE_PDL=1 (abi.cu pdl_enabled).
-bool pdl_enabled();
+// kind 0: routing/combine kernels, 1: the grouped GEMMs (MOE_PDL=1: all,
+// MOE_PDL=2: GEMMs only)
+bool pdl_enabled(int kind = 0);
 template <typename... KArgs, typename... Args>
-cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+cudaError_t launch_k(int pdl_kind, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
                      cudaStream_t st, Args&&... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
@@ -39,7 +41,7 @@ cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = pdl_enabled(pdl_kind) ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
