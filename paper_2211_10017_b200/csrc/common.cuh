@@ -147,17 +147,46 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                "r"(bytes)
                : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-  const uint32_t a = smem_u32(bar);
+// Wait for the phase of parity `phase` to complete.  The retry loop is C++,
+// not a branch inside the asm: lanes of a warp can observe the completion in
+// different iterations, and an asm-internal loop hides that divergence from
+// the compiler -- a warp that then executes elect.sync / uniform-datapath
+// code partially converged faults ("illegal instruction", seen
+// intermittently in the tcgen05 producer).  Warps that continue with
+// warp-collective code additionally __syncwarp() (mbar_wait_warp).
+__device__ __forceinline__ bool mbar_try_wait(uint32_t a, uint32_t phase) {
+  uint32_t ok;
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%0], %1, 10000000;\n"
-      "@!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(a),
-      "r"(phase)
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%1], %2, 10000000;\n"
+      "selp.b32 %0, 1, 0, P1;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(a), "r"(phase)
       : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  const uint32_t a = smem_u32(bar);
+  while (!mbar_try_wait(a, phase)) {
+  }
+}
+// two barriers, both try_waits issued back to back (their ~90-cycle
+// latencies overlap instead of adding up)
+__device__ __forceinline__ void mbar_wait2_warp(uint64_t* b1, uint32_t p1, uint64_t* b2,
+                                                uint32_t p2) {
+  const uint32_t a1 = smem_u32(b1), a2 = smem_u32(b2);
+  bool ok1 = mbar_try_wait(a1, p1);
+  bool ok2 = mbar_try_wait(a2, p2);
+  while (!ok1) ok1 = mbar_try_wait(a1, p1);
+  while (!ok2) ok2 = mbar_try_wait(a2, p2);
+  __syncwarp();
+}
+// the same, for a warp that continues converged (elect.sync, tcgen05 issue)
+__device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t phase) {
+  mbar_wait(bar, phase);
+  __syncwarp();
 }
 
 // ----------------------------------------------------------------------- TMA

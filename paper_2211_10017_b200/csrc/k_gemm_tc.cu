@@ -74,7 +74,12 @@ struct Cfg {
   static constexpr int NA = TS ? ((512 - NACC * BN) / 32 >= 4 ? 4 : 2) : 2;
   static constexpr int BUDGET = 220 * 1024 - EPI - NA * ABYTES;  // TMA stages
   static constexpr int NS0 = BUDGET / STAGE;
-  static constexpr int NS = NS0 > 8 ? 8 : NS0;                   // TMA stages
+  // TMA stages, an even count: with an odd count the two dequant groups
+  // (alternate k-blocks) share stages in alternating order, and fp16-weight
+  // layers (NS = 3 / 7) faulted or gave non-deterministic outputs under
+  // repeated route+FFN stress (scripts/stress_layer.py; root cause not yet
+  // isolated); every measured config keeps its stage count or loses one
+  static constexpr int NS = NS0 > 8 ? 8 : (NS0 & ~1);
   // [TMA stages][B | W] | [SS: A stages] | epilogue staging | barriers | table
   static constexpr int OFF_A = NS * STAGE;
   static constexpr int OFF_EPI = OFF_A + NA * ABYTES;
@@ -254,7 +259,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int row = __shfl_sync(0xffffffffu, (int)(T.row0 + rank * (tile_n<BN, CL>(T) / 2)), 0);
         for (int64_t kb = 0; kb < P.nkb; ++kb, ++it) {
           const int s = it % C::NS;
-          mbar_wait(&empty[s], ((it / C::NS) & 1) ^ 1);
+          mbar_wait_warp(&empty[s], ((it / C::NS) & 1) ^ 1);
           TC_TRACE(0, it);
           uint8_t* sb = smem + s * C::STAGE;
           const uint32_t wb = (P.dbg & 4) ? 0u : (uint32_t)C::WBYTES;
@@ -294,7 +299,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const Tile Tt = decode(table, np, P.problems, t, nftg, BN, CL, rank);
         const uint32_t idesc =
             __shfl_sync(0xffffffffu, umma_idesc_f16(128 * CL, tile_n<BN, CL>(Tt)), 0);
-        mbar_wait(&tempty[acc], ((local / C::NACC) & 1) ^ 1);
+        mbar_wait_warp(&tempty[acc], ((local / C::NACC) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tm + acc * BN;
         for (int64_t kb = 0; kb < P.nkb; ++kb, ++it) {
@@ -304,7 +309,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           // so afull also orders the activation tile (each try_wait costs
           // ~90 cycles of this thread even when already complete)
           TC_TRACE(1, it);
-          mbar_wait(&afull[a], (it / C::NA) & 1);
+          if (P.dbg & 8) mbar_wait_warp(&full[s], (it / C::NS) & 1);  // dev A/B: double wait
+          mbar_wait_warp(&afull[a], (it / C::NA) & 1);
           tc_fence_after();
           TC_TRACE(2, it);
           const uint64_t bdesc = umma_desc_sw128(smem_base + s * C::STAGE);
@@ -362,8 +368,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int64_t kb = 0; kb < P.nkb; ++kb, ++it) {
         if ((int)(it % kDqGroups) != grp) continue;
         const int s = it % C::NS, a = it % C::NA;
-        mbar_wait(&full[s], (it / C::NS) & 1);
-        mbar_wait(&aempty[a], ((it / C::NA) & 1) ^ 1);
+        mbar_wait_warp(&full[s], (it / C::NS) & 1);
+        mbar_wait_warp(&aempty[a], ((it / C::NA) & 1) ^ 1);
         if (lane == 0 && q == 0) TC_TRACE(4, it);
         const uint4* wblk = reinterpret_cast<const uint4*>(smem + s * C::STAGE + C::BBYTES);
         uint32_t v[32];
@@ -443,7 +449,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (BITS != 16) sc = h2f(P.scales[T.e * P.n + col]);
         bi = h2f(P.bias[T.e * P.n + col]);
       }
-      mbar_wait(&tfull[acc], (local / C::NACC) & 1);
+      mbar_wait_warp(&tfull[acc], (local / C::NACC) & 1);
       tc_fence_after();
       if (lane == 0 && ew == 0) TC_TRACE(6, local);
       // only the columns holding this tile's rows need draining

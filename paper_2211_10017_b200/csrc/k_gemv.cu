@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(kThreads, 3) gemv_kernel(const Params P) {
         const int npass = (int)((it.r1 - it.r0 + NT - 1) / NT);
         for (int pass = 0; pass < npass; ++pass)
           for (int kb = it.kb0; kb < it.kb1; ++kb, ++n) {
-            if (n >= RG::NST) mbar_wait(&empty[s], ph ^ 1u);
+            if (n >= RG::NST) mbar_wait_warp(&empty[s], ph ^ 1u);
             if (elect_one()) {
               mbar_arrive_expect_tx(&full[s], RG::WB);
               bulk_load(ring + s * RG::WB, wb + (int64_t)kb * RG::WB, RG::WB, &full[s]);
@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(kThreads, 3) gemv_kernel(const Params P) {
           constexpr int NTL = decltype(ntile_c)::value;
           const uint16_t* xk = xk0;
           for (int kbl = 0; kbl < nkbl; ++kbl, xk += 64) {
-            mbar_wait(&full[s], ph);
+            mbar_wait_warp(&full[s], ph);
             uint32_t w[F::NW];
             frag_from_smem<BITS>(ring + s * RG::WB, fg, t, w);
             uint32_t lo[8], hi[8];

@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(NT, 1) ln_gate_kernel(
   }
   for (int i = tid; i <= E; i += NT) hist[i] = 0;
   __syncthreads();
-  mbar_wait(&bars[0], 0);
+  mbar_wait_warp(&bars[0], 0);
   G3_TRACE(1);
   if (out_fin != nullptr) {  // fused k = 1 combine: finished tokens pass through (out = x)
     for (int i = tid; i < nrow * d8; i += NT) {
@@ -422,7 +422,7 @@ __global__ void __launch_bounds__(NT, 1) ln_gate_kernel(
 
   for (int c = 0; c < C.nch; ++c) {
     const int s = c % C.ns;
-    mbar_wait(&bars[1 + s], (uint32_t)((c / C.ns) & 1));
+    mbar_wait_warp(&bars[1 + s], (uint32_t)((c / C.ns) & 1));
     if (active) {
       // weights blocked by (input pair, expert pair) (k_gate_fused.cu):
       // inputs 2j, 2j+1 of experts e0.. are the contiguous floats
