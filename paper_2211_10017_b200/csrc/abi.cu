@@ -653,12 +653,9 @@ static int layer_forward(moe_layer* L, const uint16_t* x, const uint8_t* fin, in
   // and no combine launch.  k > 1 sums slots in slot order: separate kernel.
   // (tcgen05 path only: in the decode kernel the extra epilogue state costs
   // more than the combine launch it saves -- measured, C1/C3 shapes).
-  // Experimental, opt-in (MOE_FUSED_COMBINE=1): C4 -10 us, but an
-  // intermittent launch failure at T=16384 (~1 in 5 runs of
-  // test_layer_fused_gate_routing_exact[64-1024-16384-1]) is not yet
-  // explained, so the default keeps the separate combine kernel.
-  static const bool want_fuse = std::getenv("MOE_FUSED_COMBINE") &&
-                                std::atoi(std::getenv("MOE_FUSED_COMBINE")) != 0;
+  // MOE_FUSED_COMBINE=0 turns it off (A/B).
+  static const bool want_fuse = !(std::getenv("MOE_FUSED_COMBINE") &&
+                                  std::atoi(std::getenv("MOE_FUSED_COMBINE")) == 0);
   const bool fuse = want_fuse && mode == MOE_MODE_FAST && k == 1 && T > kGemvMaxRows &&
                     fused_gate_ok(L, x, T, k);
   TRY(layer_route(L, x, fin, T, k, st, mark, fuse ? out : nullptr));

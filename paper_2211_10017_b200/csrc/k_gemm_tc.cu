@@ -309,7 +309,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           // so afull also orders the activation tile (each try_wait costs
           // ~90 cycles of this thread even when already complete)
           TC_TRACE(1, it);
-          if (P.dbg & 8) mbar_wait_warp(&full[s], (it / C::NS) & 1);  // dev A/B: double wait
           mbar_wait_warp(&afull[a], (it / C::NA) & 1);
           tc_fence_after();
           TC_TRACE(2, it);
