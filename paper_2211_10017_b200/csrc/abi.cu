@@ -343,7 +343,7 @@ struct moe_layer {
   uint32_t *expert = nullptr, *perm = nullptr, *inv = nullptr, *offsets = nullptr,
            *problems = nullptr, *active = nullptr, *bad_row = nullptr;
   uint16_t* scale = nullptr;
-  uint32_t *blockcnt = nullptr, *blockbase = nullptr, *bad_expert = nullptr;
+  uint32_t *blockcnt = nullptr, *blockbase = nullptr, *bad_expert = nullptr, *keytot = nullptr;
   // EP: hidden activations of rows received from peers
   uint16_t* ep_h = nullptr;
   int64_t ep_cap = 0;
@@ -505,8 +505,9 @@ static int layer_reserve(moe_layer* L, int64_t T, int k) {
   TRY(L->alloc(&L->perm, cS * 4));
   TRY(L->alloc(&L->inv, cS * 4));
   TRY(L->alloc(&L->scale, cS * 2));
-  TRY(L->alloc(&L->blockcnt, (2 * nblk * (E + 1)) * 4));
+  TRY(L->alloc(&L->blockcnt, (2 * nblk * (E + 1) + (E + 1)) * 4));  // cnt | base | key totals
   L->blockbase = L->blockcnt + nblk * (E + 1);
+  L->keytot = L->blockbase + nblk * (E + 1);
   TRY(L->alloc(&L->dx, cT * d * 2));
   TRY(L->alloc(&L->dout, cT * d * 2));
   TRY(L->alloc(&L->dfin, cT));
@@ -576,7 +577,7 @@ static int layer_route(moe_layer* L, const uint16_t* x, const uint8_t* fin, int6
   L->last_k = k;
   MOE_CUDA_TRY(cudaMemsetAsync(L->bad_row, 0xFF, 8, st));  // bad_row + bad_expert
   TRY(mark());
-  PlanWork w{L->blockcnt, L->blockbase, L->bad_expert};
+  PlanWork w{L->blockcnt, L->blockbase, L->bad_expert, L->keytot};
   if (fused_gate_ok(L, x, T, k)) {
     // one kernel: LN + logits + top-k + key histogram; then scan/place/gather
     GateFusedArgs ga{x, T, d, L->ln_g, L->ln_b, L->gw32, L->gwp, L->gb, E, k, fin, L->xn,

@@ -448,7 +448,12 @@ static int run_gemv(const GemmArgs& a, const GemvWork& w, cudaStream_t st) {
   }
   // persistent: enough CTAs for the live items (empty problems are skipped
   // inside), at most 3 per SM
-  const int64_t grid = std::min<int64_t>((int64_t)P.nitems, 3 * (int64_t)sm_count());
+  // at most min(np, rows) problems are live (each holds >= 1 row): size the
+  // grid for those -- at T = 1 a grid for all E problems launched ~3x more
+  // CTAs than there were items, each paying the prologue
+  const int64_t live = std::max<int64_t>(1, std::min<int64_t>(a.np, a.rows));
+  const int64_t grid =
+      std::max<int64_t>(1, std::min<int64_t>(live * P.nft * P.nsplit, 3 * (int64_t)sm_count()));
   MOE_CUDA_TRY(launch_k(0, gv::gemv_kernel<BITS>, dim3((unsigned)grid), dim3(gv::kThreads), smem, st, P));
   note_launch();
   return check_launch("gemv");

@@ -141,17 +141,97 @@ __global__ void __launch_bounds__(1024) plan_scan_kernel(
   if (tid == 0 && active != nullptr) *active = tot[E];
 }
 
+// One CTA per routing key: the key's exclusive prefix over the blocks,
+// blockbase[key][b] = sum of cnt[key][b' < b] (WITHOUT the key's offset), and
+// its total keytot[key].  (E+1) CTAs in parallel instead of one CTA walking
+// the whole (key x block) table: the key offsets are a 1-2 warp scan over
+// keytot that every place CTA redoes (plan_place_kernel with keytot).
+__global__ void __launch_bounds__(256) plan_keyscan_kernel(const uint32_t* __restrict__ blockcnt,
+                                                           int64_t nblk,
+                                                           uint32_t* __restrict__ blockbase,
+                                                           uint32_t* __restrict__ keytot) {
+  __shared__ uint32_t wsum[8];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t* row = blockcnt + (int64_t)blockIdx.x * nblk;
+  uint32_t* brow = blockbase + (int64_t)blockIdx.x * nblk;
+  uint32_t carry = 0;
+  for (int64_t b0 = 0; b0 < nblk; b0 += 256 * 8) {  // thread owns 8 consecutive blocks
+    uint32_t v[8], pre[8], run = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int64_t b = b0 + tid * 8 + j;
+      v[j] = b < nblk ? row[b] : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      pre[j] = run;
+      run += v[j];
+    }
+    uint32_t in = run;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, in, o);
+      if (lane >= o) in += u;
+    }
+    if (lane == 31) wsum[warp] = in;
+    __syncthreads();
+    uint32_t wpre = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      const uint32_t x = wsum[w];
+      wpre += w < warp ? x : 0u;
+      tot += x;
+    }
+    const uint32_t base = carry + wpre + in - run;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int64_t b = b0 + tid * 8 + j;
+      if (b < nblk) brow[b] = base + pre[j];
+    }
+    carry += tot;
+    __syncthreads();  // wsum reused
+  }
+  if (tid == 0) keytot[blockIdx.x] = carry;
+}
+
 __global__ void __launch_bounds__(1024) plan_place_kernel(int spb,
     const uint32_t* __restrict__ expert, const uint8_t* __restrict__ finished, int64_t S, int k,
     int64_t E, const uint32_t* __restrict__ blockbase, uint32_t* __restrict__ perm,
     uint32_t* __restrict__ inv, const uint16_t* __restrict__ src, int64_t cols,
-    uint16_t* __restrict__ dst, uint32_t* bad) {
-  // spb = slots per plan block (blockDim.x >= spb, a multiple of 32)
-  extern __shared__ uint32_t wcnt[];  // [warps][E+1], then pos/slot lists
+    uint16_t* __restrict__ dst, uint32_t* bad, const uint32_t* __restrict__ keytot = nullptr,
+    uint32_t* __restrict__ offsets = nullptr, uint32_t* __restrict__ problems = nullptr,
+    uint32_t* __restrict__ active = nullptr) {
+  // spb = slots per plan block (blockDim.x >= spb, a multiple of 32).
+  // keytot non-null: blockbase holds per-key prefixes only (plan_keyscan);
+  // the key offsets are scanned here and block 0 publishes them.
+  extern __shared__ uint32_t wcnt[];  // [warps][E+1], pos list, [keytot: key offsets]
   const int64_t keys = E + 1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
   for (int64_t i = threadIdx.x; i < nwarp * keys; i += blockDim.x) wcnt[i] = 0;
+  uint32_t* koff = wcnt + nwarp * keys + blockDim.x;
+  if (keytot != nullptr && warp == 0) {
+    uint32_t carry = 0;
+    for (int64_t k0 = 0; k0 < keys; k0 += 32) {
+      const int64_t kk = k0 + lane;
+      const uint32_t v = kk < keys ? keytot[kk] : 0u;
+      uint32_t in = v;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, in, o);
+        if (lane >= o) in += u;
+      }
+      if (kk < keys) koff[kk] = carry + in - v;
+      carry += __shfl_sync(0xffffffffu, in, 31);
+    }
+  }
   __syncthreads();
+  if (keytot != nullptr && blockIdx.x == 0) {
+    for (int64_t kk = threadIdx.x; kk < keys; kk += blockDim.x) offsets[kk] = koff[kk];
+    for (int64_t e = threadIdx.x; e < E; e += blockDim.x) {
+      problems[3 * e] = (uint32_t)e;
+      problems[3 * e + 1] = koff[e];
+      problems[3 * e + 2] = koff[e + 1];
+    }
+    if (threadIdx.x == 0 && active != nullptr) *active = koff[E];
+  }
   const int64_t slot = (int64_t)blockIdx.x * spb + threadIdx.x;
   const bool live = (int)threadIdx.x < spb && slot < S;
   const uint32_t key = live ? slot_key(expert, finished, slot, k, E, bad) : 0xFFFFFFFFu;
@@ -164,7 +244,8 @@ __global__ void __launch_bounds__(1024) plan_place_kernel(int spb,
   if (live) {
     uint32_t before = 0;
     for (int w = 0; w < warp; ++w) before += wcnt[w * keys + key];
-    const uint32_t pos = blockbase[(int64_t)key * gridDim.x + blockIdx.x] + before + rank_w;
+    const uint32_t pos = blockbase[(int64_t)key * gridDim.x + blockIdx.x] + before + rank_w +
+                         (keytot != nullptr ? koff[key] : 0u);
     perm[pos] = (uint32_t)slot;
     inv[slot] = pos;
     pos_l[threadIdx.x] = pos;
@@ -423,14 +504,14 @@ int launch_plan_from_counts(const uint32_t* expert, const uint8_t* finished, int
     }
     return check_launch("plan_place_fused");
   }
-  plan_scan_kernel<<<1, 1024, 0, st>>>(w.blockcnt, nblk, E, w.blockbase, offsets, problems,
-                                       active);
+  if (w.keytot == nullptr) return set_error(MOE_EINVAL, "plan_from_counts: no key-total workspace");
+  plan_keyscan_kernel<<<(unsigned)(E + 1), 256, 0, st>>>(w.blockcnt, nblk, w.blockbase, w.keytot);
   note_launch();
   const int threads = (int)((spb + 31) / 32 * 32);
-  const size_t smem = ((threads / 32) * (E + 1) + threads) * 4;
-  plan_place_kernel<<<(unsigned)nblk, threads, smem, st>>>((int)spb, expert, finished, S, k, E,
-                                                           w.blockbase, perm, inv, nullptr, 0,
-                                                           nullptr, w.bad);
+  const size_t smem = ((threads / 32) * (E + 1) + threads + (E + 1)) * 4;
+  plan_place_kernel<<<(unsigned)nblk, threads, smem, st>>>(
+      (int)spb, expert, finished, S, k, E, w.blockbase, perm, inv, nullptr, 0, nullptr, w.bad,
+      w.keytot, offsets, problems, active);
   note_launch();
   const int s1 = check_launch("plan_from_counts");
   if (s1 != MOE_OK || gather_dst == nullptr) return s1;

@@ -99,6 +99,7 @@ struct PlanWork {
   uint32_t* blockcnt;   // nblk * (E+1)
   uint32_t* blockbase;  // nblk * (E+1)
   uint32_t* bad;        // 1 (expert out of range: lowest slot)
+  uint32_t* keytot = nullptr;  // E+1 per-key totals (plan_keyscan path)
 };
 int64_t plan_blocks(int64_t S);
 int launch_routing_plan(const uint32_t* expert, const uint8_t* finished, int64_t T, int k,
