@@ -283,8 +283,8 @@ __global__ void __launch_bounds__(1024) plan_place_fused_kernel(int spb,
     int64_t E, const uint32_t* __restrict__ blockcnt, uint32_t* __restrict__ perm,
     uint32_t* __restrict__ inv, uint32_t* __restrict__ offsets, uint32_t* __restrict__ problems,
     uint32_t* __restrict__ active, const uint16_t* __restrict__ src, int64_t cols,
-    uint16_t* __restrict__ dst, uint32_t* bad, long long* trace) {
-  extern __shared__ uint32_t sh[];
+    uint16_t* __restrict__ dst, uint32_t* bad, long long* trace, int stage_rows) {
+  extern __shared__ __align__(16) uint32_t sh[];
   const int64_t keys = E + 1, nblk = gridDim.x;
 #define PL_TRACE(i)                                                               \
   do {                                                                            \
@@ -306,6 +306,31 @@ __global__ void __launch_bounds__(1024) plan_place_fused_kernel(int spb,
   griddep_launch();
   griddep_wait();
   PL_TRACE(0);
+  // stage_rows: this block's source rows are bulk-copied into shared memory
+  // now (they do not depend on the placement), overlapping the histogram
+  // and scan phases; the gather at the end is then bulk stores only
+  const int nslots_b = (int)::min((int64_t)spb, S - b * spb);
+  const int64_t ncnt_w = std::max<int64_t>(keys * (nblk + 1), (int64_t)blockDim.x);
+  uint64_t* rbar = reinterpret_cast<uint64_t*>(
+      (reinterpret_cast<uintptr_t>(cnt + ncnt_w) + 15) & ~uintptr_t(15));
+  uint16_t* rows_sm = reinterpret_cast<uint16_t*>(rbar + 2);
+  if (stage_rows && dst != nullptr && warp == 0) {
+    if (elect_one()) {
+      mbar_init(rbar, 1);
+      fence_barrier_init();
+      mbar_arrive_expect_tx(rbar, (uint32_t)(nslots_b * cols * 2));
+      int64_t q = (b * spb) / k;
+      int r = (int)((b * spb) % k);
+      for (int i = 0; i < nslots_b; ++i) {
+        bulk_load(rows_sm + (int64_t)i * cols, src + q * cols, (uint32_t)(cols * 2), rbar);
+        if (++r == k) {
+          r = 0;
+          ++q;
+        }
+      }
+    }
+    __syncwarp();
+  }
   // this thread's slot key, loaded up front (overlaps the histogram loads)
   const int64_t slot = b * spb + threadIdx.x;
   const bool live = (int)threadIdx.x < spb && slot < S;
@@ -398,6 +423,21 @@ __global__ void __launch_bounds__(1024) plan_place_fused_kernel(int spb,
   if (live) srow[threadIdx.x] = (uint32_t)(slot / k);
   __syncthreads();
   PL_TRACE(3);
+  if (stage_rows) {  // rows already in shared memory: bulk stores to their positions
+    if (warp == 0) {
+      mbar_wait_warp(rbar, 0);
+      if (elect_one()) {
+        for (int i = 0; i < nslots_b; ++i)
+          bulk_store(dst + (int64_t)pos_l[i] * cols, rows_sm + (int64_t)i * cols,
+                     (uint32_t)(cols * 2));
+        bulk_commit();
+        bulk_wait_read<0>();  // shared memory stays valid until the stores have read it
+      }
+      __syncwarp();
+    }
+    PL_TRACE(5);
+    return;
+  }
   // 4. gather dst[pos] = src[slot / k]: 16-byte pieces, 8 loads in flight per
   //    thread (32-bit index math: a 64-bit division per piece costs more
   //    than the copy)
@@ -469,8 +509,13 @@ int launch_plan_from_counts(const uint32_t* expert, const uint8_t* finished, int
   if ((E + 1) * nblk <= kFusedScanMax && (cols % 8) == 0 && spb <= 1024) {
     const int threads = (int)std::max<int64_t>(kPlaceThreads, (spb + 31) / 32 * 32);
     // tot | base | wcnt[warps] | pos | staged histogram [(E+1) x nblk]
-    const size_t smem = ((E + 1) * 2 + 1 + (threads / 32) * (E + 1) + threads +
-                         std::max<int64_t>((E + 1) * (nblk + 1), threads)) * 4;
+    const size_t smem0 = ((E + 1) * 2 + 1 + (threads / 32) * (E + 1) + threads +
+                          std::max<int64_t>((E + 1) * (nblk + 1), threads)) * 4;
+    // + the block's source rows, staged by bulk copies (when they fit)
+    const size_t rows_bytes = (size_t)spb * cols * 2;
+    static const bool no_stage = std::getenv("MOE_PLAN_NO_STAGE") != nullptr;  // dev A/B
+    const int stage_rows = !no_stage && gather_dst != nullptr && rows_bytes <= 64 * 1024 ? 1 : 0;
+    const size_t smem = smem0 + (stage_rows ? 16 + 16 + rows_bytes : 0);
     if (smem > 48 * 1024) {
       static size_t attr = 0;
       if (smem > attr) {
@@ -485,7 +530,7 @@ int launch_plan_from_counts(const uint32_t* expert, const uint8_t* finished, int
     MOE_CUDA_TRY(launch_k(0, plan_place_fused_kernel, dim3((unsigned)nblk), dim3(threads), smem, st,
                           (int)spb, expert, finished, S, k, E, (const uint32_t*)w.blockcnt, perm,
                           inv, offsets, problems, active, gather_src, cols, gather_dst, w.bad,
-                          tr ? dtr : nullptr));
+                          tr ? dtr : nullptr, stage_rows));
     note_launch();
     if (tr) {
       std::vector<long long> h(16 + 2 * nblk);
