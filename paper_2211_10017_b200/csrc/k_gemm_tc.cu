@@ -665,9 +665,10 @@ static int run_tc_bits(const GemmArgs& a, cudaStream_t st) {
   // (scripts/gpu_g52.sh / g53.sh; C2 and C4 routed and uniform):
   //   * at most one wave of 256-token tiles: TS-256 with a single
   //     accumulator (A in TMEM, MMA-bound k-blocks; nothing to overlap);
-  //   * big experts (>= 3 tiles of 256 rows): SS-256 (fewest tiles);
   //   * otherwise TS-192 (4 A stages; the evenly split tiles of ~128-190
-  //     rows absorb the spread of routed expert sizes).
+  //     rows absorb the spread of routed expert sizes; at C2's 1024-row
+  //     experts it edges out SS-256, whose k-blocks are bound by the
+  //     shared-memory traffic of A).
   // Single CTAs below that (MOE_TC_PAIR=0 forces them; MOE_TC_BN forces a
   // width: 128/160/192/224 TS, 256 SS, 257 TS single-accumulator).
   const int64_t nft = (a.n + 127) / 128;
@@ -678,7 +679,7 @@ static int run_tc_bits(const GemmArgs& a, cudaStream_t st) {
       const int64_t pairs = sm_count() / 2;
       const int64_t tiles256 = a.np * ((a.rows_hint + 255) / 256) * (nft / 2);
       int bn = force;
-      if (bn == 0) bn = tiles256 <= pairs ? 257 : a.rows_hint >= 768 ? 256 : 192;
+      if (bn == 0) bn = tiles256 <= pairs ? 257 : 192;
       switch (bn) {
         case 128: return run_tc<BITS, 128, true, 2>(a, st);
         case 160: return run_tc<BITS, 160, true, 2>(a, st);
