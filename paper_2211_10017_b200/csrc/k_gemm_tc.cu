@@ -679,7 +679,8 @@ static int run_tc_bits(const GemmArgs& a, cudaStream_t st) {
       const int64_t pairs = sm_count() / 2;
       const int64_t tiles256 = a.np * ((a.rows_hint + 255) / 256) * (nft / 2);
       int bn = force;
-      if (bn == 0) bn = tiles256 <= pairs ? 257 : 192;
+      static const int multi = std::getenv("MOE_TC_BNM") ? std::atoi(std::getenv("MOE_TC_BNM")) : 192;
+      if (bn == 0) bn = tiles256 <= pairs ? 257 : multi;  // MOE_TC_BNM: dev A/B of the multi-wave width
       switch (bn) {
         case 128: return run_tc<BITS, 128, true, 2>(a, st);
         case 160: return run_tc<BITS, 160, true, 2>(a, st);
