@@ -662,7 +662,7 @@ template <int BITS>
 static int run_tc_bits(const GemmArgs& a, cudaStream_t st) {
   // Large problems run on CTA pairs (cta_group::2, M = 256 features) when
   // the feature tiles pair up.  Token-tile width, from B200 measurements
-  // (scripts/gpu_g52.sh / g53.sh; C2 and C4 routed and uniform):
+  // (bench.py sweeps with MOE_TC_BN / MOE_TC_BNM, C2 and C4, routed and uniform):
   //   * at most one wave of 256-token tiles: TS-256 with a single
   //     accumulator (A in TMEM, MMA-bound k-blocks; nothing to overlap);
   //   * otherwise TS-192 (4 A stages; the evenly split tiles of ~128-190
