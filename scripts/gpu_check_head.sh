@@ -1,0 +1,4 @@
+timeout 1200 python -m pytest tests -m gpu -q 2>&1 | tail -1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+python bench.py 2>&1 | tail -1 > gpurun_out/bench_c2_head.json; python3 -c "
+import json; j=json.load(open('gpurun_out/bench_c2_head.json')); print('C2', 'us=%.1f'%(1e3*j['ms_per_step']), 'tok/s=%.4g'%j['value'], 'e2e=%.4g'%j['e2e']['value'], 'frac=%.3f'%j['roofline']['frac'], j['clocks'])"
