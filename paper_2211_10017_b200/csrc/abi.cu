@@ -46,13 +46,15 @@ int check_launch(const char* what) {
   return MOE_OK;
 }
 
-// Opt-in (MOE_PDL=1 all layer kernels, MOE_PDL=2 the GEMMs only): with
-// every kernel triggering its dependents at entry, the parked dependent
-// CTAs crowd the SMs -- measured 2-5% slower at C2/C3 on B200 for "all", so
-// plain stream order is the default.
+// Programmatic dependent launch: by default only on the second GEMM of an
+// FFN pair (MOE_PDL=3): its prologue (barriers, TMEM, descriptor prefetch)
+// runs as the first GEMM's CTAs retire -- C2 -0.4 us, C4 -1 us.  MOE_PDL=1
+// (every layer kernel, each triggering its dependents at entry) and 2 (both
+// GEMMs) measured 1-5% slower: the parked dependent CTAs crowd the SMs.
+// MOE_PDL=0: plain stream order.
 bool pdl_enabled(int kind) {
-  static const int mode = std::getenv("MOE_PDL") ? std::atoi(std::getenv("MOE_PDL")) : 0;
-  return mode == 1 || (mode == 2 && kind == 1);
+  static const int mode = std::getenv("MOE_PDL") ? std::atoi(std::getenv("MOE_PDL")) : 3;
+  return mode == 1 || (mode == 2 && kind >= 1) || (mode == 3 && kind == 2);
 }
 
 int sm_count() {
@@ -614,6 +616,7 @@ static int layer_ffn(moe_layer* L, const uint16_t* xin, int64_t rows, const uint
   const int64_t hint = rows / std::max<int64_t>(1, std::min<int64_t>(El, rows));
   GemmArgs g1{xin, rows, d, problems, np, L->w1t, L->s1, L->bits, El, f, L->b1, 1, h, db, hint};
   GemmArgs g2{h, rows, f, problems, np, L->w2t, L->s2, L->bits, El, d, L->b2, 0, out, db, hint};
+  g2.second = 1;
   if (comb != nullptr && mode == MOE_MODE_FAST) {
     g2.cx = comb->cx;
     g2.cperm = comb->cperm;

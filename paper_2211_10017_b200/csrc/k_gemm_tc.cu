@@ -630,7 +630,7 @@ static int run_tc(const GemmArgs& a, cudaStream_t st) {
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = pdl_enabled(1) ? 2 : 1;
+    cfg.numAttrs = pdl_enabled(a.second ? 2 : 1) ? 2 : 1;
     if (trace_path) {
       int nc = 0;
       cudaOccupancyMaxActiveClusters(&nc, tc::gemm_tc_kernel<BITS, BN, TS, CL>, &cfg);
@@ -638,7 +638,7 @@ static int run_tc(const GemmArgs& a, cudaStream_t st) {
     }
     MOE_CUDA_TRY(cudaLaunchKernelEx(&cfg, tc::gemm_tc_kernel<BITS, BN, TS, CL>, tmap, O, P));
   } else {
-    MOE_CUDA_TRY(launch_k(1, tc::gemm_tc_kernel<BITS, BN, TS, CL>, dim3(sm_count()), dim3(tc::kThreads),
+    MOE_CUDA_TRY(launch_k(a.second ? 2 : 1, tc::gemm_tc_kernel<BITS, BN, TS, CL>, dim3(sm_count()), dim3(tc::kThreads),
                           C::SMEM, st, tmap, O, P));
   }
   note_launch();

@@ -26,8 +26,8 @@ int sm_count();
 // griddep_wait() before it reads anything the previous kernel wrote.  In a
 // CUDA graph the edges become programmatic, so each kernel's launch latency
 // overlaps its predecessor.  Opt-in: MOE_PDL=1 (abi.cu pdl_enabled).
-// kind 0: routing/combine kernels, 1: the grouped GEMMs (MOE_PDL=1: all,
-// MOE_PDL=2: GEMMs only)
+// kind 0: routing/combine kernels, 1: the grouped GEMMs, 2: the second GEMM
+// of an FFN pair (MOE_PDL=1: all, 2: GEMMs, 3: the second GEMM only)
 bool pdl_enabled(int kind = 0);
 template <typename... KArgs, typename... Args>
 cudaError_t launch_k(int pdl_kind, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
@@ -138,6 +138,7 @@ struct GemmArgs {
   uint16_t* out;
   uint16_t debias;  // 0x6408 (W4) / 0x6480 (W8), MOE_FAULT_INJECT aware
   int64_t rows_hint;  // expected rows per problem (tile-size choice)
+  int second = 0;     // the second GEMM of an FFN pair (MOE_PDL=3: PDL on this launch only)
   // k = 1 combine fused into the epilogue (tcgen05 kernel only): output row r
   // (slot position) goes to token t = cperm[r] as
   //   cout[t] = cx[t] (+) (y_r (*) cscale[t])   (fp16 RN each, = combine_kernel)
