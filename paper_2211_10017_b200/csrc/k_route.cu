@@ -676,7 +676,7 @@ int launch_combine(const uint16_t* x, const uint16_t* y, const uint32_t* inv,
   const int64_t work = d % 8 == 0 ? T * d / 8 : T * d;
   const unsigned blocks = (unsigned)std::min<int64_t>((work + 255) / 256, 148 * 16);
   if (d % 8 == 0)
-    MOE_CUDA_TRY(launch_k(0, combine_kernel, dim3(blocks), dim3(256), 0, st, x, y, inv, scale, finished,
+    MOE_CUDA_TRY(launch_k(3, combine_kernel, dim3(blocks), dim3(256), 0, st, x, y, inv, scale, finished,
                           T, d, k, out));
   else
     combine_scalar_kernel<<<blocks, 256, 0, st>>>(x, y, inv, scale, finished, T, d, k, out);
