@@ -55,7 +55,7 @@ int check_launch(const char* what) {
 bool pdl_enabled(int kind) {
   static const int mode = std::getenv("MOE_PDL") ? std::atoi(std::getenv("MOE_PDL")) : 4;
   return mode == 1 || (mode == 2 && (kind == 1 || kind == 2)) || (mode == 3 && kind == 2) ||
-         (mode == 4 && (kind == 2 || kind == 3));
+         (mode == 4 && (kind == 2 || kind == 3)) || (mode == 5 && kind >= 2);
 }
 
 int sm_count() {

@@ -454,7 +454,7 @@ static int run_gemv(const GemmArgs& a, const GemvWork& w, cudaStream_t st) {
   const int64_t live = std::max<int64_t>(1, std::min<int64_t>(a.np, a.rows));
   const int64_t grid =
       std::max<int64_t>(1, std::min<int64_t>(live * P.nft * P.nsplit, 3 * (int64_t)sm_count()));
-  MOE_CUDA_TRY(launch_k(0, gv::gemv_kernel<BITS>, dim3((unsigned)grid), dim3(gv::kThreads), smem, st, P));
+  MOE_CUDA_TRY(launch_k(4, gv::gemv_kernel<BITS>, dim3((unsigned)grid), dim3(gv::kThreads), smem, st, P));
   note_launch();
   return check_launch("gemv");
 }

@@ -27,8 +27,8 @@ int sm_count();
 // CUDA graph the edges become programmatic, so each kernel's launch latency
 // overlaps its predecessor.  Opt-in: MOE_PDL=1 (abi.cu pdl_enabled).
 // kind 0: routing kernels, 1: the grouped GEMMs, 2: the second GEMM of an
-// FFN pair, 3: the combine (MOE_PDL=1: all, 2: GEMMs, 3: the second GEMM,
-// 4: the second GEMM and the combine)
+// FFN pair, 3: the combine, 4: the decode GEMVs (MOE_PDL=1: all, 2: GEMMs,
+// 3: the second GEMM, 4: the second GEMM and the combine, 5: 4 + GEMVs)
 bool pdl_enabled(int kind = 0);
 template <typename... KArgs, typename... Args>
 cudaError_t launch_k(int pdl_kind, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
