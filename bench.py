@@ -132,30 +132,71 @@ def dist_env():
 
 
 # ------------------------------------------------------------ CPU baseline
-def cpu_reference_rate(E, d, f, k, sample_T, seconds=10.0, max_runs=3, seed=11):
-    """Tokens/s of the reference CPU layer (oracle/_ref) on sample_T tokens,
-    all host threads; falls back to the C oracle port (1 thread)."""
+class _Shape:
+    def __init__(self, shape):
+        self.shape = shape
+
+
+def reference_cpu_layer(E, d, f, seed, cores):
+    """(run(x, threads, k), kind, threads used) for the reference CPU layer:
+    oracle/_ref (the reference engine compiled from its sources) when built,
+    else the C oracle port.  Small layers: random_model-style fp16 masters
+    quantized by the reference's own quantize.  Large layers (C4/C5, up to
+    4.3 G weights): synthetic int4 payloads drawn directly (uniform codes,
+    per-channel scales of the same magnitude) -- the CPU cost of the layer
+    does not depend on the weight values, and drawing + quantizing 4 G
+    normals in numpy would dominate the run."""
     import numpy as np
-    from oracle.oracle import Oracle, Reference, random_layer, reference_available
-    lw = random_layer(d, f, E, seed=seed)
+    from oracle.oracle import LayerWeights, Oracle, Reference, random_layer, reference_available
+    rng = np.random.default_rng(seed)
+    if E * d * f <= 2 ** 27:
+        lw = random_layer(d, f, E, seed=seed)
+        q = None
+    else:
+        n = lambda shape, s: (rng.standard_normal(shape) * s).astype(np.float16)  # noqa
+        lw = LayerWeights((1 + 0.1 * rng.standard_normal(d)).astype(np.float16), n((d,), 0.05),
+                          n((d, E), 1 / math.sqrt(d)), n((E,), 0.02), _Shape((E, d, f)),
+                          n((E, f), 0.02), _Shape((E, f, d)), n((E, d), 0.02))
+        sc = lambda m, n_: (np.abs(rng.standard_normal((E, n_))) * 3 / math.sqrt(m) / 7 + 1e-3
+                            ).astype(np.float16)
+        q = (np.frombuffer(rng.bytes(E * d * f // 2), np.uint8), sc(d, f),
+             np.frombuffer(rng.bytes(E * f * d // 2), np.uint8), sc(f, d))
+    if reference_available():
+        R = Reference().layer(lw, 4, threads=cores, q=q)
+        return (lambda x, threads, k: R.forward(x, None, threads=threads, k=k)), "reference"
+    orc = Oracle()
+    if q is None:
+        q = (*orc.quantize(lw.w1, 4), *orc.quantize(lw.w2, 4))
+    return (lambda x, threads, k: orc.moe_forward(lw, x, None, k=k, bits=4, q=q)), "port"
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_reference_rate(E, d, f, k, sample_T, seconds=10.0, max_runs=3, seed=11):
+    """Tokens/s of the reference CPU layer on sample_T tokens at all host
+    threads and at 1 thread."""
+    import numpy as np
     x = np.random.default_rng(seed + 1).standard_normal((sample_T, d)).astype(np.float16)
     cores = os.cpu_count() or 1
-    if reference_available():
-        R = Reference().layer(lw, 4, threads=cores)
-        run = lambda: R.forward(x, None, threads=cores, k=k)  # noqa: E731
-        kind, used = "reference", cores
-    else:
-        orc = Oracle()
-        q = (*orc.quantize(lw.w1, 4), *orc.quantize(lw.w2, 4))
-        run = lambda: orc.moe_forward(lw, x, None, k=k, bits=4, q=q)  # noqa: E731
-        kind, used = "port", 1
-    times, t_end = [], time.perf_counter() + seconds
-    while len(times) < max_runs and (not times or time.perf_counter() < t_end):
-        t0 = time.perf_counter()
-        run()
-        times.append(time.perf_counter() - t0)
-    med = statistics.median(times)
-    return sample_T / med, kind, used, med, len(times)
+    run, kind = reference_cpu_layer(E, d, f, seed, cores)
+    res = {}
+    for threads in ((cores, 1) if kind == "reference" else (1,)):
+        times, t_end = [], time.perf_counter() + seconds
+        while len(times) < max_runs and (not times or time.perf_counter() < t_end):
+            t0 = time.perf_counter()
+            run(x, threads, k)
+            times.append(time.perf_counter() - t0)
+        med = statistics.median(times)
+        res[threads] = (sample_T / med, med, len(times))
+    return res, kind, cores
 
 
 def run_reference_arm(args, wl):
@@ -163,27 +204,21 @@ def run_reference_arm(args, wl):
     if rank != 0:
         return
     import numpy as np
-    from oracle.oracle import Oracle, Reference, random_layer, reference_available
     E, d, f, T, k, label = wl
     cores = os.cpu_count() or 1
-    # bounded sample per step: ~1 s of reference CPU work (config C2 at 8 cores)
-    sample_T = int(os.environ.get("MOE_REF_SAMPLE_T", max(1, min(T, 1024 if d * f <= 2 ** 21 else 16))))
-    lw = random_layer(d, f, E, seed=11)
+    # bounded sample per step: ~0.3-1 s of reference CPU work
+    # (C2: 1024 tokens; C3/C4: 16; C5: 2 -- the int4 reference re-dequantizes
+    # every touched expert per call, ~1.3 s per token-pair at C5 on 8 cores)
+    cap = 1024 if d * f <= 2 ** 21 else (16 if d * f <= 2 ** 23 else 2)
+    sample_T = int(os.environ.get("MOE_REF_SAMPLE_T", max(1, min(T, cap))))
+    run, kind = reference_cpu_layer(E, d, f, 11, cores)
+    used = cores if kind == "reference" else 1
     x = np.random.default_rng(12).standard_normal((sample_T, d)).astype(np.float16)
-    if reference_available():
-        R = Reference().layer(lw, 4, threads=cores)
-        run = lambda: R.forward(x, None, threads=cores, k=k)  # noqa: E731
-        kind, used = "reference", cores
-    else:
-        orc = Oracle()
-        q = (*orc.quantize(lw.w1, 4), *orc.quantize(lw.w2, 4))
-        run = lambda: orc.moe_forward(lw, x, None, k=k, bits=4, q=q)  # noqa: E731
-        kind, used = "port", 1
     for _ in range(args.warmup):
-        run()
+        run(x, used, k)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        run()
+        run(x, used, k)
     dt = time.perf_counter() - t0
     value = args.steps * sample_T / dt
     line = {
@@ -195,6 +230,7 @@ def run_reference_arm(args, wl):
         "config": {"workload": label, "E": E, "d_model": d, "d_ff": f, "tokens": T,
                    "top_k": k, "bits": 4},
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": used, "kind": kind,
+                         "cpu_model": cpu_model(),
                          "sample": f"{sample_T} of {T} tokens per step, moe_ffn_forward "
                                    f"(top-{k} via reference functions), threads={used}"},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
@@ -226,43 +262,45 @@ def make_layers(E, d, f, T, k, R, device, seed):
 
 
 def make_ep_layers(E, d, f, T, k, R, dev, rank, G):
-    """R expert-parallel layer copies: identical full weights on every rank
-    (same seeds), each rank keeping the full gate and its E/G experts."""
+    """R expert-parallel layer copies for this rank: the full gate (same seed
+    on every rank) and only this rank's E/G experts (seeded per global
+    expert block, so the union over ranks is one well-defined layer)."""
     import torch
-    from paper_2211_10017_b200.ep import CudaRank, owner_range
-    from paper_2211_10017_b200.ops import MoELayer
+    from paper_2211_10017_b200.ep import EPMoELayer, owner_range
     e0, el = owner_range(E, G, rank)
-    sl = slice(e0, e0 + el)
-    g = torch.Generator(device=dev)
-    ranks, xs = [], []
+    layers, xs = [], []
     for r in range(R):
+        g = torch.Generator(device=dev)
         g.manual_seed(7000 + r)
         n = lambda shape, s: (torch.randn(shape, generator=g, device=dev) * s).half()  # noqa
         ln_g = (1 + 0.1 * torch.randn(d, generator=g, device=dev)).half()
         ln_b, gw, gb = n((d,), 0.05), n((d, E), 1 / math.sqrt(d)), n((E,), 0.02)
-        w1, b1 = n((E, d, f), 1 / math.sqrt(d)), n((E, f), 0.02)
-        w2, b2 = n((E, f, d), 1 / math.sqrt(f)), n((E, d), 0.02)
-        L = MoELayer(ln_g, ln_b, gw, gb, w1[sl], b1[sl], w2[sl], b2[sl], bits=4, device=dev,
-                     expert_range=(e0, el))
-        L.quant = None
-        L.reserve(T, k)
-        ranks.append(CudaRank(L))
+        g.manual_seed(7000 + 1000 * r + 1 + e0)
+        w1, b1 = n((el, d, f), 1 / math.sqrt(d)), n((el, f), 0.02)
+        w2, b2 = n((el, f, d), 1 / math.sqrt(f)), n((el, d), 0.02)
+        L = EPMoELayer(ln_g, ln_b, gw, gb, w1, b1, w2, b2, bits=4, device=dev, sliced=True)
+        del w1, w2
+        L.layer.quant = None
+        L.layer.reserve(T, k)
+        layers.append(L)
         gx = torch.Generator(device=dev)
         gx.manual_seed(9000 + 97 * rank + r)
         xs.append(torch.randn((T, d), generator=gx, device=dev).half())
+    torch.cuda.empty_cache()
     torch.cuda.synchronize()
-    return ranks, xs
+    return layers, xs
 
 
 def run_native_ep(args, wl):
-    """N > 1: expert parallelism (ep.py) -- each rank owns E/N experts and
-    T tokens; NCCL all-to-all-v dispatch/combine every step (weak scaling)."""
-    import numpy as np
+    """N > 1: expert parallelism through the C-ABI (moe_ep_forward, csrc/ep.cu):
+    each rank owns E/N experts and T tokens; every step routes locally,
+    exchanges counts on the device, dispatches rows per (peer, expert) with
+    NCCL send/recv over NVLink, runs its experts and returns the rows (weak
+    scaling: T tokens per GPU at every N)."""
     import torch
     import torch.distributed as dist
 
     from paper_2211_10017_b200 import abi
-    from paper_2211_10017_b200.ep import DistComm, ep_forward
 
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
@@ -274,18 +312,22 @@ def run_native_ep(args, wl):
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(sk.getsockname()[1]),
                           RANK="0", WORLD_SIZE="1")
         sk.close()
+    # NCCL init logging (rank count, NVLink/NVLS topology) to stderr, not the JSON stream
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     dist.init_process_group("nccl", device_id=dev)
     E, d, f, T, k, label = wl
     if E % ws != 0:
         raise SystemExit(f"ep: {E} experts not divisible by {ws} GPUs")
     per_copy = E // ws * d * f + 2 * T * d * 2 + 2 * T * k * (d + f) * 2
     R = max(2, min(32, math.ceil(2 * L2_BYTES / per_copy)))
-    ranks, xs = make_ep_layers(E, d, f, T, k, R, dev, rank, ws)
-    comm = DistComm()
+    layers, xs = make_ep_layers(E, d, f, T, k, R, dev, rank, ws)
+    outs = [torch.empty_like(x) for x in xs]
     stream = torch.cuda.current_stream()
 
     def step(i):
-        return ep_forward([ranks[i % R]], comm, [xs[i % R]], [None], k=k, mode=1)[0]
+        layers[i % R].forward(xs[i % R], None, k=k, mode=1, out=outs[i % R])
 
     for i in range(args.warmup + R):
         step(i)
@@ -306,20 +348,28 @@ def run_native_ep(args, wl):
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     value = ws * args.steps * T / (ms / 1e3)
-    # e2e: pinned host tokens in, EP forward, host result out, every step
+    # exchange bookkeeping of the last step: rows this rank received / sent
+    sent, recv, rows = layers[(args.steps - 1) % R].counts()
+    cnt = torch.tensor([float(rows), float(sent.sum()), float(sent.sum() - sent[rank].sum())],
+                       device=dev, dtype=torch.float64)
+    mx = cnt.clone()
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    dist.all_reduce(cnt, op=dist.ReduceOp.SUM)
+    # e2e: pinned host tokens in, EP forward (public API), host result out, every step
     xh = torch.empty((T, d), dtype=torch.float16, pin_memory=True)
     oh = torch.empty((T, d), dtype=torch.float16, pin_memory=True)
     xh.copy_(xs[0])
     xd = torch.empty_like(xs[0])
+    od = torch.empty_like(xs[0])
 
     def e2e_step(i):
         xd.copy_(xh, non_blocking=True)
-        out = ep_forward([ranks[i % R]], comm, [xd], [None], k=k, mode=1)[0]
-        oh.copy_(out, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
+        layers[i % R].forward(xd, None, k=k, mode=1, out=od)
+        oh.copy_(od, non_blocking=True)
 
     for i in range(args.warmup):
         e2e_step(i)
+    torch.cuda.synchronize()
     dist.barrier()
     e0_, e1_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0_.record(stream)
@@ -331,9 +381,9 @@ def run_native_ep(args, wl):
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_value = ws * args.steps * T / (float(t.item()) / 1e3)
     hbm, tc_burst, tc_sus, peak_src = load_peaks()
-    S = T * k
-    flops = 4.0 * S * d * f  # per rank per step (balanced routing)
+    flops = 4.0 * T * k * d * f  # per rank per step (balanced routing)
     achieved = flops / (ms / args.steps * 1e-3) / 1e12
+    nvl = 2.0 * (ws - 1) / ws * T * k * d * 2  # dispatch + combine bytes per rank per step
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
@@ -343,14 +393,20 @@ def run_native_ep(args, wl):
         "config": {"workload": label, "E": E, "d_model": d, "d_ff": f, "tokens_per_gpu": T,
                    "top_k": k, "bits": 4, "mode": "fast", "parallelism": f"ep{ws}",
                    "experts_per_gpu": E // ws,
-                   "transport": "NCCL all_to_all_single (counts, dispatch, combine)",
+                   "transport": "moe_ep_forward (C++): device count exchange, NCCL "
+                                "ncclSend/ncclRecv per (peer, expert) segment into expert-major "
+                                "order, one host sync per layer",
                    "l2": f"inputs larger than L2: {R} distinct layer copies rotated"},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": tc_burst,
                      "unit": "TFLOP/s", "frac": achieved / tc_burst, "traffic": None,
                      "kernel": "whole EP layer step (layer-level: 4*T*k*d*f per rank / step time)",
-                     "peak_source": peak_src},
+                     "peak_source": peak_src,
+                     "nvlink_bytes_per_rank_step": nvl},
+        "exchange": {"rows_received_max": mx[0].item(), "rows_received_mean": cnt[0].item() / ws,
+                     "rows_sent_to_peers_mean": cnt[2].item() / ws},
         "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": T * d * 2,
-                "d2h_bytes_per_step": T * d * 2, "path": "EPMoELayer-equivalent ep_forward"},
+                "d2h_bytes_per_step": T * d * 2,
+                "path": "EPMoELayer.forward (moe_ep_forward C-ABI) + pinned H2D/D2H"},
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
@@ -539,11 +595,18 @@ def run_native(args, wl):
         "clocks": clk.summary(),
     }
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        sample_T = min(T, 512 if d * f <= 2 ** 21 else 8)
-        rate, kind, cores, med, nrun = cpu_reference_rate(E, d, f, k, sample_T)
-        line["cpu_baseline"] = {"value": rate, "unit": "tokens/s", "cores": cores, "kind": kind,
+        sample_T = min(T, 512 if d * f <= 2 ** 21 else (8 if d * f <= 2 ** 23 else 2))
+        res, kind, cores = cpu_reference_rate(E, d, f, k, sample_T)
+        top = max(res)
+        rate, med, nrun = res[top]
+        line["cpu_baseline"] = {"value": rate, "unit": "tokens/s", "cores": top, "kind": kind,
+                                "cpu_model": cpu_model(), "nproc": cores,
                                 "sample": f"{sample_T} tokens x {nrun} runs (median "
                                           f"{med:.2f} s), same E/d/f/top-{k}, int4"}
+        if 1 in res and top != 1:
+            line["cpu_baseline"]["threads1"] = {"value": res[1][0], "unit": "tokens/s",
+                                                "cores": 1, "sample": f"{sample_T} tokens x "
+                                                f"{res[1][2]} runs (median {res[1][1]:.2f} s)"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:
@@ -558,17 +621,38 @@ def load_traffic(workload):
         return None
 
 
+def relaunch(n):
+    """`bench.py --gpus N` outside torchrun: re-run this command under
+    torch.distributed.run with N processes (one per GPU) on 127.0.0.1."""
+    import socket
+    import subprocess
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)]
+    cmd += sys.argv[1:]
+    raise SystemExit(subprocess.call(cmd))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
-    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS),
+                    help="default: c2 on one GPU, c5 (the EP config) for --gpus > 1")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--force-ep", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch(args.gpus)  # one process per GPU (does not return)
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.workload is None:
+        args.workload = "c5" if ws > 1 else "c2"
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":
         run_reference_arm(args, wl)

@@ -241,6 +241,62 @@ int moe_layer_traffic(moe_layer* L, uint64_t* out6, moe_stream_t stream);
 int moe_ep_rank_counts(const uint32_t* offsets, int64_t E, int G, int64_t* counts,
                        moe_stream_t stream);
 
+/* ---- expert parallelism (new; csrc/ep.cu) ----
+ * The layer of proj/src/model.cpp:299-349 with its experts sharded over G
+ * ranks: rank g's layer holds experts [g*E/G, (g+1)*E/G) (moe_layer_desc
+ * e_begin / e_count) and the full gate; each rank brings its own tokens.
+ * Transport: NCCL point-to-point (ncclGroupStart + ncclSend/ncclRecv per
+ * (peer, local expert) segment), one process per GPU; or an in-process
+ * loopback of G ranks on one device (tests).  NCCL is resolved at run time
+ * from the process's libnccl.so.2 (status MOE_ENCCL if absent). */
+typedef struct moe_ep moe_ep;
+#define MOE_EP_ID_BYTES 128
+/* ncclGetUniqueId on the root rank; broadcast the bytes to every rank */
+int moe_ep_unique_id(uint8_t* id);
+/* ncclCommInitRank: a communicator of nranks processes, this one = rank
+ * (call with the CUDA device of this rank current) */
+int moe_ep_create(const uint8_t* id, int nranks, int rank, moe_ep** out);
+/* all nranks ranks held by this process (device-to-device copies) */
+int moe_ep_create_loopback(int nranks, moe_ep** out);
+int moe_ep_destroy(moe_ep* ep);
+int moe_ep_world(const moe_ep* ep, int* nranks, int* rank, int* local_ranks);
+/* One EP layer forward.  Arrays hold one entry per LOCAL rank (1 for an
+ * NCCL communicator, nranks for loopback): that rank's layer, its T[i]
+ * tokens x[i] (device, T x d fp16), finished flags (finished may be NULL, or
+ * entries NULL) and its output rows out[i].  One host synchronisation per
+ * call (the exchanged counts size the NCCL transfers); routing status
+ * (non-finite logits) is reported after the collective sequence completes. */
+int moe_ep_forward(moe_ep* ep, moe_layer* const* layers, const uint16_t* const* x,
+                   const uint8_t* const* finished, const int64_t* T, int k, int mode,
+                   uint16_t* const* out, moe_stream_t stream);
+/* Counts of the last forward on local rank `local`: rows sent to (peer p,
+ * local expert j) at [p*el + j], rows received from (source s, j), total
+ * received rows (expert-capacity bookkeeping across ranks). */
+int moe_ep_counts(const moe_ep* ep, int local, uint32_t* send_cnt, uint32_t* recv_cnt,
+                  int64_t* recv_rows);
+/* Pure host arithmetic of the exchange (no device needed): from the sent and
+ * received counts [G*el], the sorted-buffer offset of each sent segment,
+ * the expert-major destination row of each received segment, the local
+ * grouped-GEMM problems (el x {expert, row_begin, row_end}) and the rows
+ * received. */
+int moe_ep_segments(int G, int64_t el, const uint32_t* send_cnt, const uint32_t* recv_cnt,
+                    int64_t* send_off, int64_t* recv_dst, uint32_t* problems, int64_t* rows);
+
+/* ---- expert-capacity bookkeeping (north_star item 1; new) ----
+ * Load report of the layer's last routed forward, computed on the device
+ * (no host sync, graph-capturable) into `report` (device, E + 8 u32):
+ *   report[0..E)  rows routed to each expert (live slots; finished excluded)
+ *   report[E+0]   capacity  = ceil(capacity_factor * live_slots / E)
+ *   report[E+1]   max expert load
+ *   report[E+2]   live slots (T*k minus finished)
+ *   report[E+3]   experts over capacity
+ *   report[E+4]   overflow rows = sum max(0, load - capacity)
+ *   report[E+5]   active (non-empty) experts
+ * Nothing is dropped: the reference routes every live slot (routing.cpp:55-71);
+ * the report states what a capacity-bounded dispatch would have to drop. */
+int moe_layer_load_report(moe_layer* L, float capacity_factor, uint32_t* report,
+                          moe_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -399,8 +399,9 @@ class RefLayer:
     def __init__(self, ref: Reference, lw: LayerWeights, bits, threads, q=None):
         self.ref, self.lw, self.bits = ref, lw, bits
         P = lambda a: _u16(a).ctypes.data
-        self._keep = [_u16(a) for a in (lw.ln_g, lw.ln_b, lw.gw, lw.gb, lw.w1, lw.b1, lw.w2,
-                                        lw.b2)]
+        # fp16 expert masters only when the reference quantizes them itself
+        masters = (lw.w1, lw.w2) if q is None else ()
+        self._keep = [_u16(a) for a in (lw.ln_g, lw.ln_b, lw.gw, lw.gb, lw.b1, lw.b2) + masters]
         if q is not None:
             q1, s1, q2, s2 = [np.ascontiguousarray(a) for a in q]
             self._keep += [q1, _u16(s1), q2, _u16(s2)]

@@ -64,6 +64,15 @@ _SIGS = {
     "moe_layer_ffn": (_int, [_vp, _int, _vp]),
     "moe_layer_experts": (_int, [_vp, _vp, _i64, _vp, _i64, _int, _vp, _vp]),
     "moe_layer_combine": (_int, [_vp, _vp, _vp, _vp, _i64, _int, _vp, _vp]),
+    "moe_layer_load_report": (_int, [_vp, C.c_float, _vp, _vp]),
+    "moe_ep_unique_id": (_int, [_vp]),
+    "moe_ep_create": (_int, [_vp, _int, _int, _vp]),
+    "moe_ep_create_loopback": (_int, [_int, _vp]),
+    "moe_ep_destroy": (_int, [_vp]),
+    "moe_ep_world": (_int, [_vp, _vp, _vp, _vp]),
+    "moe_ep_forward": (_int, [_vp, _vp, _vp, _vp, _vp, _int, _int, _vp, _vp]),
+    "moe_ep_counts": (_int, [_vp, _int, _vp, _vp, _vp]),
+    "moe_ep_segments": (_int, [_int, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
 }
 
 

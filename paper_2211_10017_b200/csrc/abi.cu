@@ -328,98 +328,8 @@ int moe_ep_rank_counts(const uint32_t* offsets, int64_t E, int G, int64_t* count
 
 }  // extern "C"
 
-// ======================================================================= layer
-struct moe_layer {
-  int64_t d = 0, f = 0, E = 0;
-  int64_t El = 0, e0 = 0;  // experts whose FFN weights live here: [e0, e0 + El)
-  int bits = 16;
-  // weights (device)
-  uint16_t *ln_g = nullptr, *ln_b = nullptr, *gw = nullptr, *gb = nullptr;
-  uint16_t *b1 = nullptr, *b2 = nullptr, *s1 = nullptr, *s2 = nullptr;
-  void *w1t = nullptr, *w2t = nullptr;
-  float* gw32 = nullptr;  // gate weights widened to f32, (d, gwp) (fused gate kernel)
-  int64_t gwp = 0;
-  // workspace, sized for (cap_S slots, cap_T rows)
-  int64_t cap_T = 0, cap_S = 0;
-  uint16_t *xn = nullptr, *xp = nullptr, *h = nullptr, *y = nullptr;
-  float* logits = nullptr;
-  uint32_t *expert = nullptr, *perm = nullptr, *inv = nullptr, *offsets = nullptr,
-           *problems = nullptr, *active = nullptr, *bad_row = nullptr;
-  uint16_t* scale = nullptr;
-  uint32_t *blockcnt = nullptr, *blockbase = nullptr, *bad_expert = nullptr, *keytot = nullptr;
-  // EP: hidden activations of rows received from peers
-  uint16_t* ep_h = nullptr;
-  int64_t ep_cap = 0;
-  // decode GEMV split-K workspace (routed rows <= kGemvMaxRows)
-  float* gv_part = nullptr;
-  uint32_t* gv_ticket = nullptr;
-  // host-path staging
-  uint16_t *dx = nullptr, *dout = nullptr;
-  uint8_t* dfin = nullptr;
-  int64_t last_T = 0;
-  int last_k = 1;
-  std::vector<void*> allocs;
-  // stage profiling (moe_layer_profile): kStages+1 events per forward
-  static constexpr int kStages = 7, kProfCap = 512;
-  bool prof = false;
-  int prof_level = 0;
-  int prof_n = 0;
-  std::vector<cudaEvent_t> ev;
-  // CUDA-graph cache (moe_layer_forward_graph / pinned-buffer host path):
-  // the launch sequence of one argument set, captured once, replayed after.
-  struct GraphKey {
-    const void *x = nullptr, *fin = nullptr, *out = nullptr;
-    int64_t T = 0;
-    int k = 0, mode = -1, host = 0, prof = 0;
-    bool operator==(const GraphKey& o) const {
-      return x == o.x && fin == o.fin && out == o.out && T == o.T && k == o.k && mode == o.mode &&
-             host == o.host && prof == o.prof;
-    }
-  };
-  struct Graph {
-    GraphKey key;
-    cudaGraphExec_t exec = nullptr;
-    uint64_t nlaunch = 0;  // kernels in the graph (moe_cuda_launch_count on replay)
-  };
-  std::vector<Graph> graphs;  // small LRU-less cache
-  cudaStream_t cap_stream = nullptr;
-  uint32_t* hstatus = nullptr;  // pinned: bad_row, bad_expert of the last host-path forward
+#include "layer.cuh"
 
-  void drop_graphs() {
-    for (auto& g : graphs)
-      if (g.exec) cudaGraphExecDestroy(g.exec);
-    graphs.clear();
-  }
-  ~moe_layer() {
-    drop_graphs();
-    if (cap_stream) cudaStreamDestroy(cap_stream);
-    if (hstatus) cudaFreeHost(hstatus);
-    for (void* p : allocs) cudaFree(p);
-    for (cudaEvent_t e : ev) cudaEventDestroy(e);
-  }
-  template <class T>
-  int alloc(T** p, size_t bytes) {
-    void* q = nullptr;
-    const cudaError_t e = cudaMalloc(&q, bytes ? bytes : 16);
-    if (e != cudaSuccess) return set_cuda_error(e, "layer alloc");
-    allocs.push_back(q);
-    *p = static_cast<T*>(q);
-    return MOE_OK;
-  }
-  void release(void* p) {
-    for (auto& q : allocs)
-      if (q == p) {
-        cudaFree(q);
-        q = nullptr;
-      }
-  }
-};
-
-#define TRY(x)                \
-  do {                        \
-    const int s__ = (x);      \
-    if (s__ != MOE_OK) return s__; \
-  } while (0)
 
 static int layer_create_impl(const moe_layer_desc* D, moe_layer** out, bool device_src) {
   if (D == nullptr || out == nullptr) return set_error(MOE_EINVAL, "layer: null argument");
@@ -488,7 +398,7 @@ static int layer_create_impl(const moe_layer_desc* D, moe_layer** out, bool devi
   return MOE_OK;
 }
 
-static int layer_reserve(moe_layer* L, int64_t T, int k) {
+int moecu::layer_reserve(moe_layer* L, int64_t T, int k) {
   const int64_t S_ = T * k;
   if (T <= L->cap_T && S_ <= L->cap_S) return MOE_OK;
   const int64_t cT = std::max(T, L->cap_T), cS = std::max(S_, L->cap_S);
@@ -536,35 +446,6 @@ static int layer_reserve(moe_layer* L, int64_t T, int k) {
   return MOE_OK;
 }
 
-// Stage-event recorder of one forward (profiling only): ev[slot*(kStages+1)+i]
-// before stage i.  Inside a graph capture only an *external* record becomes a
-// real event-record node (readable after each replay).  Level 1 records only
-// the GEMM boundaries (marks 4..6): every event node costs ~2-3 us of pipeline
-// drain, so the cheap level is the one used for kernel timing.
-struct Marks {
-  moe_layer* L;
-  cudaStream_t st;
-  cudaEvent_t* evs = nullptr;
-  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  int stage = 0;
-  Marks(moe_layer* l, cudaStream_t s, bool on) : L(l), st(s) {
-    if (on && L->prof && L->prof_n < moe_layer::kProfCap) {
-      evs = &L->ev[(size_t)L->prof_n * (moe_layer::kStages + 1)];
-      cudaStreamIsCapturing(st, &cap);
-    }
-  }
-  int operator()() {
-    if (evs && (L->prof_level >= 2 || (stage >= 4 && stage <= 6)))
-      MOE_CUDA_TRY(cudaEventRecordWithFlags(
-          evs[stage], st, cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0));
-    ++stage;
-    return MOE_OK;
-  }
-  void done() {
-    if (evs) ++L->prof_n;
-  }
-};
-
 // LN -> gate -> top-k -> plan -> gather into L->xp (stages 0..3)
 // the one-kernel gate path applies (and with it the fused k = 1 combine)
 static bool fused_gate_ok(const moe_layer* L, const uint16_t* x, int64_t T, int k) {
@@ -573,8 +454,8 @@ static bool fused_gate_ok(const moe_layer* L, const uint16_t* x, int64_t T, int 
 }
 
 // out_fin non-null (fused k = 1 combine): finished tokens are written there
-static int layer_route(moe_layer* L, const uint16_t* x, const uint8_t* fin, int64_t T, int k,
-                       cudaStream_t st, Marks& mark, uint16_t* out_fin = nullptr) {
+int moecu::layer_route(moe_layer* L, const uint16_t* x, const uint8_t* fin, int64_t T, int k,
+                       cudaStream_t st, Marks& mark, uint16_t* out_fin) {
   const int64_t d = L->d, E = L->E;
   L->last_T = T;
   L->last_k = k;
@@ -609,9 +490,9 @@ static int layer_route(moe_layer* L, const uint16_t* x, const uint8_t* fin, int6
 // FFN1 (ReLU) -> FFN2 over `rows` expert-sorted rows of the LOCAL experts
 // (problems: np device triples, expert ids in [0, El)); stages 4..5
 // comb (FAST, k = 1): FFN2's epilogue applies the combine into comb->cout
-static int layer_ffn(moe_layer* L, const uint16_t* xin, int64_t rows, const uint32_t* problems,
+int moecu::layer_ffn(moe_layer* L, const uint16_t* xin, int64_t rows, const uint32_t* problems,
                      int64_t np, int mode, uint16_t* h, uint16_t* out, cudaStream_t st,
-                     Marks& mark, const GemmArgs* comb = nullptr) {
+                     Marks& mark, const GemmArgs* comb) {
   const int64_t d = L->d, f = L->f, El = L->El;
   const uint16_t db = debias_for(L->bits);
   const int64_t hint = rows / std::max<int64_t>(1, std::min<int64_t>(El, rows));
@@ -735,6 +616,15 @@ static bool is_pinned(const void* p) {
   return a.type == cudaMemoryTypeHost;
 }
 
+int moecu::layer_grow_hidden(moe_layer* L, int64_t rows) {
+  if (rows <= L->ep_cap) return MOE_OK;  // hidden-activation workspace for received rows
+  if (L->ep_h) L->release(L->ep_h);
+  L->drop_graphs();
+  TRY(L->alloc(&L->ep_h, rows * L->f * 2));
+  L->ep_cap = rows;
+  return MOE_OK;
+}
+
 extern "C" {
 
 int moe_layer_forward_graph(moe_layer* L, const uint16_t* x, const uint8_t* finished, int64_t T,
@@ -784,12 +674,7 @@ int moe_layer_experts(moe_layer* L, const uint16_t* xin, int64_t rows, const uin
   if (!L) return set_error(MOE_EINVAL, "layer: null");
   if (rows < 0 || np < 0 || np > L->El) return set_error(MOE_EINVAL, "moe_ffn: bad problem list");
   if (rows == 0 || np == 0) return MOE_OK;
-  if (rows > L->ep_cap) {  // hidden-activation workspace for received rows
-    if (L->ep_h) L->release(L->ep_h);
-    L->drop_graphs();
-    TRY(L->alloc(&L->ep_h, rows * L->f * 2));
-    L->ep_cap = rows;
-  }
+  TRY(layer_grow_hidden(L, rows));
   TRY(layer_reserve(L, 1, 1));  // GEMV split-K workspace
   Marks mark(L, S(stream), false);
   return layer_ffn(L, xin, rows, problems, np, mode, L->ep_h, out, S(stream), mark);
@@ -937,3 +822,63 @@ int moe_layer_traffic(moe_layer* L, uint64_t* t6, moe_stream_t stream) {
 }
 
 }  // extern "C"
+
+// ------------------------------------------------- expert-capacity report
+namespace moecu {
+__global__ void load_report_kernel(const uint32_t* __restrict__ offsets, int64_t E, float cf,
+                                   uint32_t* __restrict__ rep) {
+  __shared__ uint32_t red[4][32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const uint32_t live = offsets[E] - offsets[0];
+  // capacity = ceil(cf * live / E), in f64 so that cf = 1.0 gives the exact ceiling
+  const uint32_t cap = (uint32_t)ceil((double)cf * (double)live / (double)E);
+  uint32_t mx = 0, over = 0, orows = 0, act = 0;
+  for (int64_t e = tid; e < E; e += blockDim.x) {
+    const uint32_t c = offsets[e + 1] - offsets[e];
+    rep[e] = c;
+    mx = max(mx, c);
+    over += c > cap;
+    orows += c > cap ? c - cap : 0u;
+    act += c > 0;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    over += __shfl_xor_sync(0xffffffffu, over, o);
+    orows += __shfl_xor_sync(0xffffffffu, orows, o);
+    act += __shfl_xor_sync(0xffffffffu, act, o);
+  }
+  if (lane == 0) {
+    red[0][warp] = mx;
+    red[1][warp] = over;
+    red[2][warp] = orows;
+    red[3][warp] = act;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int w = 1; w < nw; ++w) {
+      mx = max(mx, red[0][w]);
+      over += red[1][w];
+      orows += red[2][w];
+      act += red[3][w];
+    }
+    rep[E + 0] = cap;
+    rep[E + 1] = mx;
+    rep[E + 2] = live;
+    rep[E + 3] = over;
+    rep[E + 4] = orows;
+    rep[E + 5] = act;
+    rep[E + 6] = 0;
+    rep[E + 7] = 0;
+  }
+}
+}  // namespace moecu
+
+extern "C" int moe_layer_load_report(moe_layer* L, float capacity_factor, uint32_t* report,
+                                     moe_stream_t stream) {
+  if (!L || !report) return set_error(MOE_EINVAL, "layer: null");
+  if (!(capacity_factor > 0.f)) return set_error(MOE_EINVAL, "capacity factor must be > 0");
+  if (!L->offsets) return set_error(MOE_EINVAL, "moe_ffn: no routed forward yet");
+  load_report_kernel<<<1, 256, 0, S(stream)>>>(L->offsets, L->E, capacity_factor, report);
+  note_launch();
+  return check_launch("load_report");
+}

@@ -134,11 +134,6 @@ __device__ __forceinline__ int tile_n(const Tile& T) {
   return live >= BN ? BN : (int)((live + 15) / 16 * 16);
 }
 
-// Output tensor maps: box {32 features, 32 >> i rows}, i = 0..5.
-struct OutMaps {
-  CUtensorMap map[6];
-};
-
 struct Params {
   const uint8_t* tiled;
   const uint16_t* scales;
@@ -176,8 +171,7 @@ constexpr int kTraceN = 1024;  // events per role slot
 // peer's dequant / epilogue arrivals remotely; commits multicast to both.
 template <int BITS, int BN, bool TS, int CL>
 __global__ void __launch_bounds__(kThreads, 1)
-    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ OutMaps O,
-                   const Params P) {
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const Params P) {
   using C = Cfg<BITS, BN, TS, CL>;
   constexpr bool PAIR = CL == 2;
   const int rank = CL > 1 ? (int)cluster_ctarank() : 0;
@@ -430,10 +424,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ----------------------------------------------------------- epilogue
     // kEpiGroups groups of 4 warps take alternate 32-token chunks of a tile.
     // Every warp works alone: it drains its 32 features x 32 tokens from TMEM,
-    // stages them as [token][32 features] fp16 (one 64-byte row per token),
-    // and lane 0 TMA-stores the block -- one box per power-of-two run of
-    // valid rows, so a problem's last chunk never writes the next expert's
-    // rows.  Staging is double-buffered per warp; no cross-warp barriers.
+    // stages them as [token][32 features] fp16 (one 64-byte row per token) in
+    // its private staging buffer, and reads them back as 16-byte row chunks
+    // (8 features) that it stores directly.  Each chunk is guarded by its
+    // row (a problem's last chunk never writes the next expert's rows) and by
+    // its column (n % 8 == 0, so a chunk is entirely inside or outside the
+    // row when n % 32 != 0).  No cross-warp barriers.
     const int q = warp & 3, ew = warp - 4 - 4 * kDqGroups, eg = ew >> 2;
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
     uint16_t* stage0 = reinterpret_cast<uint16_t*>(smem + C::OFF_EPI + ew * C::EPI_WBUF);
@@ -454,7 +450,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       // only the columns holding this tile's rows need draining
       const int64_t live = T.row1 - T.row0;
       const int ncols = (int)(live < BN ? (live + 31) / 32 * 32 : BN);
-      const bool slice_live = T.ft * 128 + q * 32 < P.n;
 #pragma unroll 1
       for (int c0 = eg * 32; c0 < ((P.dbg & 1) ? 0 : ncols); c0 += 32 * kEpiGroups, ++cc) {
         uint16_t* stg = stage0;  // read back before the next chunk overwrites it
@@ -484,12 +479,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         // read back as 16-byte vectors: lane -> (row lane/4 + 8i, 8 features)
         const int nrow = (int)::min((int64_t)32, T.row1 - (T.row0 + c0));
         const int64_t col = T.ft * 128 + q * 32 + (lane & 3) * 8;
+        const bool col_live = col < P.n;  // whole 8-feature chunk (n % 8 == 0)
         if (P.cout == nullptr) {
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const int row = i * 8 + (lane >> 2);
             const uint4 val = *reinterpret_cast<const uint4*>(stg + row * 32 + (lane & 3) * 8);
-            if (row < nrow && slice_live)
+            if (row < nrow && col_live)
               *reinterpret_cast<uint4*>(P.out + (T.row0 + c0 + row) * P.n + col) = val;
           }
         } else {
@@ -499,7 +495,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const int row = i * 8 + (lane >> 2);
-            tok[i] = row < nrow && slice_live ? P.cperm[T.row0 + c0 + row] : 0xFFFFFFFFu;
+            tok[i] = row < nrow && col_live ? P.cperm[T.row0 + c0 + row] : 0xFFFFFFFFu;
           }
           uint4 xv[4];
           uint16_t sv[4];
@@ -529,7 +525,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (lane == 0 && ew == 0) TC_TRACE(7, local);
     }
-    if (lane == 0) bulk_wait<0>();  // all output rows written before the CTA retires
   }
   tc_fence_before();
   __syncthreads();
@@ -571,17 +566,6 @@ static int run_tc(const GemmArgs& a, cudaStream_t st) {
                       CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(MOE_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
-  tc::OutMaps O;
-  for (int i = 0; i < 6; ++i) {
-    const cuuint64_t odims[2] = {(cuuint64_t)a.n, (cuuint64_t)a.rows};
-    const cuuint64_t ostr[1] = {(cuuint64_t)a.n * 2};
-    const cuuint32_t obox[2] = {32, (cuuint32_t)(32 >> i)};
-    r = encode(&O.map[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a.out, odims, ostr, obox, estr,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-               CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS)
-      return set_error(MOE_ECUDA, "cuTensorMapEncodeTiled(out) failed (%d)", (int)r);
-  }
   tc::Params P;
   P.tiled = static_cast<const uint8_t*>(a.tiled);
   P.scales = a.scales;
@@ -636,10 +620,10 @@ static int run_tc(const GemmArgs& a, cudaStream_t st) {
       cudaOccupancyMaxActiveClusters(&nc, tc::gemm_tc_kernel<BITS, BN, TS, CL>, &cfg);
       std::fprintf(stderr, "gemm_tc pair BN=%d TS=%d: max active clusters %d\n", BN, (int)TS, nc);
     }
-    MOE_CUDA_TRY(cudaLaunchKernelEx(&cfg, tc::gemm_tc_kernel<BITS, BN, TS, CL>, tmap, O, P));
+    MOE_CUDA_TRY(cudaLaunchKernelEx(&cfg, tc::gemm_tc_kernel<BITS, BN, TS, CL>, tmap, P));
   } else {
     MOE_CUDA_TRY(launch_k(a.second ? 2 : 1, tc::gemm_tc_kernel<BITS, BN, TS, CL>, dim3(sm_count()), dim3(tc::kThreads),
-                          C::SMEM, st, tmap, O, P));
+                          C::SMEM, st, tmap, P));
   }
   note_launch();
   const int rc = check_launch("gemm_tc");

@@ -673,9 +673,12 @@ int launch_combine(const uint16_t* x, const uint16_t* y, const uint32_t* inv,
                    const uint16_t* scale, const uint8_t* finished, int64_t T, int64_t d, int k,
                    uint16_t* out, cudaStream_t st) {
   if (T == 0) return MOE_OK;
-  const int64_t work = d % 8 == 0 ? T * d / 8 : T * d;
+  // 16-byte vector path only when every row start is 16-byte aligned
+  const bool vec = d % 8 == 0 && ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y) |
+                                   reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+  const int64_t work = vec ? T * d / 8 : T * d;
   const unsigned blocks = (unsigned)std::min<int64_t>((work + 255) / 256, 148 * 16);
-  if (d % 8 == 0)
+  if (vec)
     MOE_CUDA_TRY(launch_k(3, combine_kernel, dim3(blocks), dim3(256), 0, st, x, y, inv, scale, finished,
                           T, d, k, out));
   else

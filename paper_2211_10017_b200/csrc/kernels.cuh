@@ -25,7 +25,9 @@ int sm_count();
 // independent prologue -- barrier init, TMEM alloc, weight prefetch) and
 // griddep_wait() before it reads anything the previous kernel wrote.  In a
 // CUDA graph the edges become programmatic, so each kernel's launch latency
-// overlaps its predecessor.  Opt-in: MOE_PDL=1 (abi.cu pdl_enabled).
+// overlaps its predecessor.  Default MOE_PDL=4 (the second GEMM of an FFN
+// pair and the combine); the other modes are A/B switches (abi.cu
+// pdl_enabled).
 // kind 0: routing kernels, 1: the grouped GEMMs, 2: the second GEMM of an
 // FFN pair, 3: the combine, 4: the decode GEMVs (MOE_PDL=1: all, 2: GEMMs,
 // 3: the second GEMM, 4: the second GEMM and the combine, 5: 4 + GEMVs)

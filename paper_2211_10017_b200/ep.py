@@ -1,33 +1,29 @@
 """Expert parallelism for the MoE layer.
 
-G ranks (one process per GPU); rank g owns experts [g*E/G, (g+1)*E/G) and a
-contiguous range of tokens.  One forward:
+A thin wrapper over the C-ABI (include/moe_cuda.h `moe_ep_*`,
+csrc/ep.cu): G ranks, one process per GPU; rank g owns experts
+[g*E/G, (g+1)*E/G) and brings its own tokens.  The whole forward -- route,
+device-side count exchange, per-(peer, expert) NCCL send/recv dispatch into
+expert-major order, local grouped GEMMs, reverse exchange, combine -- runs
+in C++/CUDA; Python only creates the communicator (the NCCL unique id is
+broadcast over torch.distributed) and passes pointers.
 
-  1. route     -- local LN -> gate -> top-k -> plan -> gather (moe_layer_route);
-                  the plan is sorted by expert, hence by owner rank
-  2. counts    -- per (destination rank, local expert) row counts from the
-                  plan offsets; all-to-all of G x E/G counts
-  3. dispatch  -- all-to-all-v of the expert-sorted rows (NCCL over NVLink)
-  4. regroup   -- received rows are (source, expert)-major; one gather puts
-                  them expert-major for the grouped GEMMs
-  5. experts   -- FFN1 + FFN2 of the local experts (moe_layer_experts)
-  6. combine   -- inverse gather, reverse all-to-all-v, then the local
-                  residual + gate-scaled un-permute (moe_layer_combine)
-
-Every compute step is a libmoe_cuda.so kernel; torch.distributed (NCCL) is
-the transport.  Rows are independent in every kernel, so in EXACT numerics
-an EP forward is bit-identical to the single-GPU layer on the same tokens
-(tests/test_ep_*.py).  The orchestration is written over a list of rank
-states and a `Comm`, so the same code runs (a) distributed, one state per
-process, and (b) as an in-process loopback of G ranks on one device (tests;
-and the gloo CPU tests drive it with the oracle as the local compute).
+`LoopbackEP` holds all G ranks in one process on one device (the same
+orchestration with device-to-device copies as the transport): the G > 1
+test path on a single GPU.  `segments` is the pure host arithmetic of the
+exchange (moe_ep_segments), callable without a GPU.
 """
 from __future__ import annotations
 
+import ctypes as C
+
 import numpy as np
 
+from . import abi
 
-# ----------------------------------------------------------- host bookkeeping
+ID_BYTES = 128
+
+
 def owner_range(E: int, G: int, g: int):
     """(first expert, count) owned by rank g (E % G == 0)."""
     if E % G != 0:
@@ -36,196 +32,132 @@ def owner_range(E: int, G: int, g: int):
     return g * el, el
 
 
-def send_counts(offsets, E: int, G: int) -> np.ndarray:
-    """(G, E/G) rows this rank sends to each (owner rank, local expert);
-    offsets = the plan's expert_offsets (E+1), finished rows excluded."""
-    off = np.asarray(offsets, np.int64)
-    return np.diff(off[: E + 1]).reshape(G, E // G)
+def segments(G: int, el: int, send_cnt, recv_cnt):
+    """moe_ep_segments: (send_off [G*el], recv_dst [G*el], problems (el, 3),
+    rows received) from the per-(peer, local expert) sent / received counts."""
+    sc = np.ascontiguousarray(send_cnt, np.uint32).reshape(-1)
+    rc = np.ascontiguousarray(recv_cnt, np.uint32).reshape(-1)
+    so = np.zeros(G * el, np.int64)
+    rd = np.zeros(G * el, np.int64)
+    pr = np.zeros((el, 3), np.uint32)
+    rows = C.c_int64()
+    abi.call("moe_ep_segments", G, el, C.c_void_p(sc.ctypes.data), C.c_void_p(rc.ctypes.data),
+             C.c_void_p(so.ctypes.data), C.c_void_p(rd.ctypes.data), C.c_void_p(pr.ctypes.data),
+             C.byref(rows))
+    return so, rd, pr, rows.value
 
 
-def regroup(recv_counts: np.ndarray):
-    """Received rows arrive (source rank, local expert)-major.  Returns
-    perm (gather: expert-major position -> received position) and the
-    grouped-GEMM problems (local expert, row_begin, row_end)."""
-    rc = np.asarray(recv_counts, np.int64)
-    G, el = rc.shape
-    base = np.concatenate([[0], np.cumsum(rc.reshape(-1))])[:-1].reshape(G, el)
-    perm = np.empty(int(rc.sum()), np.int64)
-    problems = np.zeros((el, 3), np.int64)
-    pos = 0
-    for e in range(el):
-        start = pos
-        for src in range(G):
-            c = int(rc[src, e])
-            perm[pos:pos + c] = np.arange(base[src, e], base[src, e] + c)
-            pos += c
-        problems[e] = (e, start, pos)
-    return perm, problems
+def _ptrs(ts, ctype=C.c_void_p):
+    arr = (ctype * len(ts))()
+    for i, t in enumerate(ts):
+        arr[i] = None if t is None else t.data_ptr()
+    return arr
 
 
-def inverse(perm: np.ndarray) -> np.ndarray:
-    inv = np.empty_like(perm)
-    inv[perm] = np.arange(len(perm), dtype=perm.dtype)
-    return inv
+class _EP:
+    """Owner of a moe_ep handle."""
 
+    def __init__(self, handle):
+        self._h = handle
 
-# ------------------------------------------------------------------ transports
-class DistComm:
-    """torch.distributed all-to-all-v (NCCL on GPUs, gloo on CPU); one local
-    rank state per process."""
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                abi.lib().moe_ep_destroy(h)
+            except Exception:  # interpreter shutdown
+                pass
+            self._h = None
 
-    def __init__(self, group=None):
-        import torch.distributed as dist
-        self.dist, self.group = dist, group
-        self.world = dist.get_world_size(group)
+    def world(self):
+        g, r, n = C.c_int(), C.c_int(), C.c_int()
+        abi.call("moe_ep_world", self._h, C.byref(g), C.byref(r), C.byref(n))
+        return g.value, r.value, n.value
 
-    def all_to_all(self, sends, send_splits, recv_splits, outs=None):
-        """sends: [tensor (sum(send_splits), ...)] for the one local rank;
-        outs (optional): [preallocated receive tensor] (e.g. a layer buffer)."""
+    def _forward(self, layers, xs, fins, k, mode, outs, stream):
         import torch
-        (x,), (ss,), (rs,) = sends, send_splits, recv_splits
-        out = outs[0] if outs is not None else torch.empty(
-            (int(sum(rs)),) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
-        self.dist.all_to_all_single(out, x.contiguous(), [int(v) for v in rs],
-                                    [int(v) for v in ss], group=self.group)
-        return [out]
+        n = len(layers)
+        Ls = (C.c_void_p * n)(*[L._h.value for L in layers])
+        Ts = (C.c_int64 * n)(*[x.shape[0] for x in xs])
+        s = stream if stream is not None else torch.cuda.current_stream()
+        fin_arr = None if all(f is None for f in fins) else _ptrs(fins)
+        abi.call("moe_ep_forward", self._h, Ls, _ptrs(xs), fin_arr, Ts, k, mode, _ptrs(outs),
+                 C.c_void_p(s.cuda_stream))
+        return outs
+
+    def counts(self, local=0):
+        """(sent (G, el), received (G, el), rows received) of the last forward."""
+        G, _, _ = self.world()
+        E = self._E
+        sc = np.zeros(E, np.uint32)
+        rc = np.zeros(E, np.uint32)
+        rows = C.c_int64()
+        abi.call("moe_ep_counts", self._h, local, C.c_void_p(sc.ctypes.data),
+                 C.c_void_p(rc.ctypes.data), C.byref(rows))
+        return sc.reshape(G, -1), rc.reshape(G, -1), rows.value
 
 
-class LoopbackComm:
-    """All G ranks in this process (one device): the all-to-all is a
-    reshuffle of row segments between the rank states."""
-
-    def __init__(self, world):
-        self.world = world
-
-    def all_to_all(self, sends, send_splits, recv_splits, outs=None):
-        import torch
-        G = self.world
-        seg = []
-        for g in range(G):
-            cuts = np.concatenate([[0], np.cumsum(send_splits[g])]).astype(np.int64)
-            seg.append([sends[g][int(cuts[j]):int(cuts[j + 1])] for j in range(G)])
-        res = [torch.cat([seg[src][dst] for src in range(G)], 0) for dst in range(G)]
-        if outs is not None:
-            for o, r in zip(outs, res):
-                if o is not None and r.shape[0]:
-                    o.copy_(r)
-            return outs
-        return res
-
-
-# ------------------------------------------------------------------ compute
-class CudaRank:
-    """Local compute of one rank over libmoe_cuda.so (a MoELayer holding the
-    full gate and only this rank's experts)."""
-
-    def __init__(self, layer):
-        self.L = layer
-        self.E = layer.E
-
-    def route(self, x, fin, k):
-        self.L.route(x, fin, k)
-        import torch
-        off = torch.empty(self.L.E + 1, dtype=torch.int32)
-        from . import abi
-        import ctypes as C
-        abi.call("moe_cuda_memcpy", C.c_void_p(off.data_ptr()), C.c_void_p(self.L.offsets_device()),
-                 (self.L.E + 1) * 4, 1, None)
-        return off.numpy().view(np.uint32).astype(np.int64)
-
-    def sorted_rows(self, n):
-        return _dev_view(self.L.buffers()[0], n, self.L.d)
-
-    def y_rows(self, n):
-        return _dev_view(self.L.buffers()[1], n, self.L.d)
-
-    def gather(self, x, idx):
-        from . import ops
-        import torch
-        if x.shape[0] == 0:
-            return x.clone()
-        p = torch.as_tensor(idx.astype(np.int32), device=x.device)
-        return ops.permute_rows(x, p)
-
-    def experts(self, xe, problems, mode):
-        import torch
-        if xe.shape[0] == 0:
-            return torch.empty_like(xe)
-        pr = torch.as_tensor(problems.astype(np.int32), device=xe.device)
-        return self.L.experts(xe, pr, mode=mode)
-
-    def combine(self, x, fin, k, y_sorted):
-        return self.L.combine(x, self.L.buffers()[1], fin, k)
-
-
-class _CAI:
-    def __init__(self, ptr, shape):
-        self.__cuda_array_interface__ = {"shape": shape, "typestr": "<f2", "data": (ptr, False),
-                                         "version": 3, "strides": None}
-
-
-def _dev_view(ptr, rows, cols):
-    """torch view (no copy) of rows x cols fp16 at a device pointer."""
-    import torch
-    if rows == 0:
-        return torch.empty((0, cols), dtype=torch.float16, device="cuda")
-    return torch.as_tensor(_CAI(ptr, (rows, cols)), device="cuda")
-
-
-# ------------------------------------------------------------------ forward
-def ep_forward(ranks, comm, xs, fins, k=1, mode=1):
-    """One expert-parallel MoE layer forward.
-
-    ranks: local compute per rank state (CudaRank or a test double);
-    xs / fins: per-state input rows / finished flags (None = none finished).
-    Returns the per-state outputs (same shapes as xs)."""
-    n = len(ranks)
-    G = comm.world
-    E = ranks[0].E
-    el = E // G
-    offs = [ranks[i].route(xs[i], fins[i], k) for i in range(n)]
-    # 2. counts (G, el) -> exchanged
-    sc = [send_counts(o, E, G) for o in offs]
-    import torch
-    cnt_dev = "cpu" if not xs[0].is_cuda else xs[0].device
-    sends = [torch.as_tensor(c.reshape(-1), dtype=torch.int64, device=cnt_dev) for c in sc]
-    recv = comm.all_to_all(sends, [[el] * G] * n, [[el] * G] * n)
-    rc = [r.cpu().numpy().reshape(G, el) for r in recv]
-    send_rows = [c.sum(1) for c in sc]
-    recv_rows = [c.sum(1) for c in rc]
-    active = [int(o[E]) for o in offs]
-    # 3. dispatch
-    xsend = [ranks[i].sorted_rows(active[i]) for i in range(n)]
-    xrecv = comm.all_to_all(xsend, send_rows, recv_rows)
-    # 4./5. regroup + experts
-    yrecv = []
-    for i in range(n):
-        perm, probs = regroup(rc[i])
-        xe = ranks[i].gather(xrecv[i], perm)
-        ye = ranks[i].experts(xe, probs, mode)
-        yrecv.append(ranks[i].gather(ye, inverse(perm)))
-    # 6. reverse all-to-all straight into each rank's sorted y, then local combine
-    ys = [ranks[i].y_rows(active[i]) for i in range(n)]
-    comm.all_to_all(yrecv, recv_rows, send_rows, outs=ys)
-    return [ranks[i].combine(xs[i], fins[i], k, ys[i]) for i in range(n)]
-
-
-class EPMoELayer:
-    """Distributed EP layer for this process's rank: the full gate plus the
-    owned experts on this GPU, NCCL transport."""
+class EPMoELayer(_EP):
+    """This process's rank of an EP layer: the full gate plus the owned
+    experts on the current GPU, NCCL transport.  torch.distributed must be
+    initialised (any backend: it only carries the 128-byte NCCL id)."""
 
     def __init__(self, ln_g, ln_b, gate_w, gate_b, w1, b1, w2, b2, bits=4, group=None,
-                 device="cuda"):
+                 device="cuda", q=None, sliced=False):
+        """w1/b1/w2/b2 (and q): all E experts, or (sliced=True) only this
+        rank's E/G experts."""
+        import torch
         import torch.distributed as dist
         from .ops import MoELayer
-        self.comm = DistComm(group)
-        G, g = self.comm.world, dist.get_rank(group)
+        G, g = dist.get_world_size(group), dist.get_rank(group)
         E = gate_w.shape[1]
         e0, el = owner_range(E, G, g)
-        sl = slice(e0, e0 + el)
-        layer = MoELayer(ln_g, ln_b, gate_w, gate_b, w1[sl], b1[sl], w2[sl], b2[sl], bits=bits,
-                         device=device, expert_range=(e0, el))
-        self.rank = CudaRank(layer)
+        sl = slice(0, el) if sliced else slice(e0, e0 + el)
+        if q is not None and not sliced:
+            raise ValueError("EPMoELayer: pass q payloads already sliced to this rank (sliced=True)")
+        self.layer = MoELayer(ln_g, ln_b, gate_w, gate_b, None if w1 is None else w1[sl], b1[sl],
+                              None if w2 is None else w2[sl], b2[sl], bits=bits, device=device,
+                              expert_range=(e0, el), q=q)
+        idb = torch.zeros(ID_BYTES, dtype=torch.uint8)
+        if g == 0:
+            raw = (C.c_uint8 * ID_BYTES)()
+            abi.call("moe_ep_unique_id", raw)
+            idb = torch.tensor(list(bytes(raw)), dtype=torch.uint8)
+        if dist.get_backend(group) == "nccl":
+            idb = idb.to(device)
+        dist.broadcast(idb, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                       group=group)
+        raw = (C.c_uint8 * ID_BYTES)(*idb.cpu().tolist())
+        h = C.c_void_p()
+        abi.call("moe_ep_create", raw, G, g, C.byref(h))
+        super().__init__(h)
+        self._E = E
+        self.E, self.rank, self.world_size = E, g, G
 
-    def forward(self, x, finished=None, k=1, mode=1):
-        return ep_forward([self.rank], self.comm, [x], [finished], k=k, mode=mode)[0]
+    def forward(self, x, finished=None, k=1, mode=abi.MODE_FAST, out=None, stream=None):
+        import torch
+        if out is None:
+            out = torch.empty_like(x)
+        self._forward([self.layer], [x], [finished], k, mode, [out], stream)
+        return out
+
+
+class LoopbackEP(_EP):
+    """All G ranks of an EP layer in this process on one device (test path):
+    layers[g] holds rank g's experts (MoELayer(..., expert_range=(g*el, el)))."""
+
+    def __init__(self, layers):
+        G = len(layers)
+        h = C.c_void_p()
+        abi.call("moe_ep_create_loopback", G, C.byref(h))
+        super().__init__(h)
+        self.layers = layers
+        self._E = layers[0].E
+
+    def forward(self, xs, fins=None, k=1, mode=abi.MODE_FAST, outs=None, stream=None):
+        import torch
+        if fins is None:
+            fins = [None] * len(xs)
+        if outs is None:
+            outs = [torch.empty_like(x) for x in xs]
+        return self._forward(self.layers, xs, fins, k, mode, outs, stream)

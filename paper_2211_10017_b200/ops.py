@@ -316,3 +316,22 @@ class MoELayer:
         t = np.zeros(6, np.uint64)
         abi.call("moe_layer_traffic", self._h, C.c_void_p(t.ctypes.data), _stream(stream))
         return dict(expert=tuple(int(v) for v in t[:3]), other=tuple(int(v) for v in t[3:]))
+
+    def load_report(self, capacity_factor=1.0, stream=None):
+        """Expert-capacity bookkeeping of the last routed forward
+        (moe_layer_load_report): per-expert live rows, the capacity
+        ceil(cf * live / E), max load, experts / rows over capacity.  Nothing
+        is dropped (the reference routes every live slot)."""
+        import numpy as np
+        E = self.E
+        rep = torch.empty(E + 8, dtype=torch.int32, device="cuda")
+        abi.call("moe_layer_load_report", self._h, C.c_float(capacity_factor), _p(rep),
+                 _stream(stream))
+        r = rep.cpu().numpy().view(np.uint32)
+        load = r[:E].astype(np.int64)
+        live = int(r[E + 2])
+        return dict(load=load, capacity=int(r[E]), max_load=int(r[E + 1]), live_slots=live,
+                    experts_over=int(r[E + 3]), overflow_rows=int(r[E + 4]),
+                    active_experts=int(r[E + 5]),
+                    imbalance=float(r[E + 1]) / (live / E) if live else 0.0,
+                    capacity_factor=capacity_factor)
