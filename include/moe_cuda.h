@@ -297,6 +297,19 @@ int moe_ep_segments(int G, int64_t el, const uint32_t* send_cnt, const uint32_t*
 int moe_layer_load_report(moe_layer* L, float capacity_factor, uint32_t* report,
                           moe_stream_t stream);
 
+/* ---- decode with batch pruning (new; csrc/decode.cu) ----
+ * The MoE blocks of beam-search decoding (proj/src/decode.cpp:104-345): for
+ * every step s < steps and every block l < n_layers, one layer forward over
+ * the step's rows (x_steps[s], steps x rows x d device), block l's output
+ * feeding block l+1, the last block's output written to out_steps[s]; the
+ * finished mask of step s (finished_steps[s], steps x rows, may be NULL) is
+ * routed iff prune (decode.cpp:167-169, 216): finished rows leave the expert
+ * workload and pass through bit for bit.  work: rows x d device scratch.  One
+ * stream, no host synchronisation (graph-capturable). */
+int moe_decode_run(moe_layer* const* layers, int n_layers, const uint16_t* x_steps,
+                   const uint8_t* finished_steps, int steps, int64_t rows, int k, int mode,
+                   int prune, uint16_t* out_steps, uint16_t* work, moe_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -73,6 +73,7 @@ _SIGS = {
     "moe_ep_forward": (_int, [_vp, _vp, _vp, _vp, _vp, _int, _int, _vp, _vp]),
     "moe_ep_counts": (_int, [_vp, _int, _vp, _vp, _vp]),
     "moe_ep_segments": (_int, [_int, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "moe_decode_run": (_int, [_vp, _int, _vp, _vp, _int, _i64, _int, _int, _int, _vp, _vp, _vp]),
 }
 
 

@@ -525,7 +525,7 @@ int moecu::layer_ffn(moe_layer* L, const uint16_t* xin, int64_t rows, const uint
   return mark();
 }
 
-static int layer_forward(moe_layer* L, const uint16_t* x, const uint8_t* fin, int64_t T, int k,
+int moecu::layer_forward(moe_layer* L, const uint16_t* x, const uint8_t* fin, int64_t T, int k,
                          int mode, uint16_t* out, cudaStream_t st) {
   if (T <= 0) return set_error(MOE_EINVAL, "moe_ffn: no rows");
   if (k < 1 || k > L->E) return set_error(MOE_EINVAL, "moe_ffn: k must be in [1, n_experts]");
@@ -705,6 +705,34 @@ int moe_layer_forward(moe_layer* L, const uint16_t* x, const uint8_t* finished, 
   if (!L) return set_error(MOE_EINVAL, "layer: null");
   return layer_forward(L, x, finished, T, k, mode, out, S(stream));
 }
+// Chunks of the pinned host-buffer path: the layer splits its tokens into c
+// chunks and pipelines copy-in (chunk i+1), compute (chunk i) and copy-out
+// (chunk i-1) on three streams -- PCIe is full duplex, and both directions
+// overlap the kernels.  Rows are independent in every kernel, so chunking
+// never changes a result.  Cost model per c (B = 50 GB/s pinned PCIe, each
+// direction): t(c) = (t_in + t_out) / c + max(t_in, t_out, t_comp(c)),
+// where t_comp(c) re-streams the expert weights c times (each chunk routes
+// to every expert); c = 1 unless a larger c is predicted >= 10 % faster.
+static int host_chunks(const moe_layer* L, int64_t T, int k) {
+  if (T * k < 1024) return 1;  // decode-sized: one launch sequence
+  const double pcie = 50e9, hbm = 6.5e12, tc = 0.9e15;
+  const double io = (double)T * L->d * 2 / pcie;
+  const double wb = (double)L->El * L->d * L->f * (L->bits == 16 ? 4.0 : L->bits == 8 ? 2.0 : 1.0);
+  const double flops = 4.0 * T * k * L->d * L->f;
+  int best = 1;
+  double tbest = 2 * io + std::max(flops / tc, wb / hbm) + 20e-6;
+  for (int c = 2; c <= moe_layer::kMaxChunks; c *= 2) {
+    if (T / c < 256) break;
+    const double comp = std::max(flops / tc, c * wb / hbm) + c * 12e-6;
+    const double t = 2 * io / c + std::max(io, comp);
+    if (t < 0.9 * tbest) {
+      best = c;
+      tbest = t;
+    }
+  }
+  return best;
+}
+
 int moe_layer_forward_host(moe_layer* L, const uint16_t* x_host, const uint8_t* fin_host,
                            int64_t T, int k, int mode, uint16_t* out_host, moe_stream_t stream) {
   if (!L) return set_error(MOE_EINVAL, "layer: null");
@@ -712,33 +740,93 @@ int moe_layer_forward_host(moe_layer* L, const uint16_t* x_host, const uint8_t* 
   if (k < 1 || k > L->E) return set_error(MOE_EINVAL, "moe_ffn: k must be in [1, n_experts]");
   TRY(layer_reserve(L, T, k));
   cudaStream_t st = S(stream);
-  auto body = [&](cudaStream_t s2, uint32_t* status_dst) -> int {
-    MOE_CUDA_TRY(cudaMemcpyAsync(L->dx, x_host, T * L->d * 2, cudaMemcpyHostToDevice, s2));
+  const int64_t d = L->d;
+  const bool pinned = is_pinned(x_host) && is_pinned(out_host) && is_pinned(fin_host);
+  const int nc = pinned ? host_chunks(L, T, k) : 1;
+  static const int force = std::getenv("MOE_HOST_CHUNKS") ? std::atoi(std::getenv("MOE_HOST_CHUNKS")) : 0;
+  const int c = pinned && force > 0 ? std::min(force, moe_layer::kMaxChunks) : nc;
+  if (!L->hstatus) MOE_CUDA_TRY(cudaMallocHost(&L->hstatus, 2 * 4 * moe_layer::kMaxChunks));
+  if (!L->dstatus) TRY(L->alloc(&L->dstatus, 2 * 4 * moe_layer::kMaxChunks));
+  auto chunk_rows = [&](int i, int64_t* t0, int64_t* t1) {
+    *t0 = T * i / c;
+    *t1 = T * (i + 1) / c;
+  };
+  // serial: copy in, forward, copy out, status -- on one stream
+  auto serial = [&](cudaStream_t s2) -> int {
+    MOE_CUDA_TRY(cudaMemcpyAsync(L->dx, x_host, T * d * 2, cudaMemcpyHostToDevice, s2));
     if (fin_host) MOE_CUDA_TRY(cudaMemcpyAsync(L->dfin, fin_host, T, cudaMemcpyHostToDevice, s2));
     TRY(layer_forward(L, L->dx, fin_host ? L->dfin : nullptr, T, k, mode, L->dout, s2));
-    MOE_CUDA_TRY(cudaMemcpyAsync(out_host, L->dout, T * L->d * 2, cudaMemcpyDeviceToHost, s2));
-    MOE_CUDA_TRY(cudaMemcpyAsync(status_dst, L->bad_row, 8, cudaMemcpyDeviceToHost, s2));
+    MOE_CUDA_TRY(cudaMemcpyAsync(out_host, L->dout, T * d * 2, cudaMemcpyDeviceToHost, s2));
+    MOE_CUDA_TRY(cudaMemcpyAsync(L->hstatus, L->bad_row, 8, cudaMemcpyDeviceToHost, s2));
     return MOE_OK;
   };
-  uint32_t hs[2];
-  if (is_pinned(x_host) && is_pinned(out_host) && is_pinned(fin_host)) {
+  // pipelined: fork copy-in / copy-out streams off the capture stream
+  auto piped = [&](cudaStream_t cs) -> int {
+    if (!L->io_in) MOE_CUDA_TRY(cudaStreamCreateWithFlags(&L->io_in, cudaStreamNonBlocking));
+    if (!L->io_out) MOE_CUDA_TRY(cudaStreamCreateWithFlags(&L->io_out, cudaStreamNonBlocking));
+    if (L->io_ev.empty()) {
+      L->io_ev.resize(2 * moe_layer::kMaxChunks + 3);
+      for (auto& e : L->io_ev) MOE_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    cudaEvent_t* in_done = &L->io_ev[0];
+    cudaEvent_t* comp_done = &L->io_ev[moe_layer::kMaxChunks];
+    cudaEvent_t fork = L->io_ev[2 * moe_layer::kMaxChunks], jin = L->io_ev[2 * moe_layer::kMaxChunks + 1],
+                jout = L->io_ev[2 * moe_layer::kMaxChunks + 2];
+    MOE_CUDA_TRY(cudaEventRecord(fork, cs));
+    MOE_CUDA_TRY(cudaStreamWaitEvent(L->io_in, fork, 0));
+    MOE_CUDA_TRY(cudaStreamWaitEvent(L->io_out, fork, 0));
+    for (int i = 0; i < c; ++i) {  // all copy-ins queued back to back
+      int64_t t0, t1;
+      chunk_rows(i, &t0, &t1);
+      MOE_CUDA_TRY(cudaMemcpyAsync(L->dx + t0 * d, x_host + t0 * d, (t1 - t0) * d * 2,
+                                   cudaMemcpyHostToDevice, L->io_in));
+      if (fin_host)
+        MOE_CUDA_TRY(cudaMemcpyAsync(L->dfin + t0, fin_host + t0, t1 - t0, cudaMemcpyHostToDevice,
+                                     L->io_in));
+      MOE_CUDA_TRY(cudaEventRecord(in_done[i], L->io_in));
+    }
+    for (int i = 0; i < c; ++i) {
+      int64_t t0, t1;
+      chunk_rows(i, &t0, &t1);
+      MOE_CUDA_TRY(cudaStreamWaitEvent(cs, in_done[i], 0));
+      TRY(layer_forward(L, L->dx + t0 * d, fin_host ? L->dfin + t0 : nullptr, t1 - t0, k, mode,
+                        L->dout + t0 * d, cs));
+      MOE_CUDA_TRY(cudaMemcpyAsync(L->dstatus + 2 * i, L->bad_row, 8, cudaMemcpyDeviceToDevice, cs));
+      MOE_CUDA_TRY(cudaEventRecord(comp_done[i], cs));
+      MOE_CUDA_TRY(cudaStreamWaitEvent(L->io_out, comp_done[i], 0));
+      MOE_CUDA_TRY(cudaMemcpyAsync(out_host + t0 * d, L->dout + t0 * d, (t1 - t0) * d * 2,
+                                   cudaMemcpyDeviceToHost, L->io_out));
+    }
+    MOE_CUDA_TRY(cudaMemcpyAsync(L->hstatus, L->dstatus, 8 * c, cudaMemcpyDeviceToHost, L->io_out));
+    MOE_CUDA_TRY(cudaEventRecord(jin, L->io_in));
+    MOE_CUDA_TRY(cudaEventRecord(jout, L->io_out));
+    MOE_CUDA_TRY(cudaStreamWaitEvent(cs, jin, 0));
+    MOE_CUDA_TRY(cudaStreamWaitEvent(cs, jout, 0));
+    return MOE_OK;
+  };
+  if (pinned) {
     // pinned buffers: one captured graph (copies + kernels + status readback)
-    if (!L->hstatus) MOE_CUDA_TRY(cudaMallocHost(&L->hstatus, 8));
-    moe_layer::GraphKey key{x_host, fin_host, out_host, T, k, mode, 1, L->prof_level};
+    moe_layer::GraphKey key{x_host, fin_host, out_host, T, k, mode, 1 + c, L->prof_level};
     cudaGraphExec_t exec = nullptr;
     uint64_t nl = 0;
-    TRY(layer_graph(L, key, [&](cudaStream_t cs) { return body(cs, L->hstatus); }, &exec, &nl));
+    TRY(layer_graph(L, key, [&](cudaStream_t cs) { return c > 1 ? piped(cs) : serial(cs); },
+                    &exec, &nl));
     MOE_CUDA_TRY(cudaGraphLaunch(exec, st));
     g_launches.fetch_add(nl);
     MOE_CUDA_TRY(cudaStreamSynchronize(st));
-    hs[0] = L->hstatus[0];
-    hs[1] = L->hstatus[1];
   } else {
-    TRY(body(st, hs));
+    TRY(serial(st));
     MOE_CUDA_TRY(cudaStreamSynchronize(st));
   }
-  if (hs[0] != 0xFFFFFFFFu) return set_error(MOE_EINVAL, "gate_top1: non-finite logit at row %u", hs[0]);
-  if (hs[1] != 0xFFFFFFFFu) return set_error(MOE_EINVAL, "build_routing_plan: expert out of range");
+  for (int i = 0; i < (pinned ? c : 1); ++i) {
+    int64_t t0, t1;
+    chunk_rows(i, &t0, &t1);
+    if (c == 1 || !pinned) t0 = 0;
+    const uint32_t* hs = L->hstatus + 2 * i;
+    if (hs[0] != 0xFFFFFFFFu)
+      return set_error(MOE_EINVAL, "gate_top1: non-finite logit at row %u", (unsigned)(hs[0] + t0));
+    if (hs[1] != 0xFFFFFFFFu) return set_error(MOE_EINVAL, "build_routing_plan: expert out of range");
+  }
   return MOE_OK;
 }
 int moe_layer_status(moe_layer* L, moe_stream_t stream) {

@@ -73,9 +73,127 @@ __global__ void __launch_bounds__(256) quantize_kernel(const uint16_t* __restric
   }
 }
 
+// Vector form (n % 8 == 0, 16-byte aligned rows).  A CTA owns 128 columns
+// of one expert: 16 column groups of 8 (one 16-byte load per row; a
+// half-warp reads 256 contiguous bytes of a row) x 16 row slices.  Pass 1:
+// per-thread channel max |w| and first non-finite weight (lowest flat index,
+// no early exit) over its slice, reduced over the slices in shared memory;
+// pass 2 (same rows, mostly L2): codes with an f32 division and
+// round-half-away -- identical to the reference's llround(f64 w / f64 s) for
+// every fp16 pair (exhaustive proof: tests/native/quant_div_check.c) --
+// packed in registers: one 32-bit word (int4) or 8 bytes (int8) per row.
+constexpr int kQCols = 16, kQSlices = 16;
+template <int BITS>
+__global__ void __launch_bounds__(256) quantize8_kernel(const uint16_t* __restrict__ w, int64_t e,
+                                                        int64_t m, int64_t n,
+                                                        uint8_t* __restrict__ packed,
+                                                        uint16_t* __restrict__ scales,
+                                                        unsigned long long* bad) {
+  __shared__ float smx[kQSlices][kQCols * 8];
+  const int64_t cpb = (n + 8 * kQCols - 1) / (8 * kQCols);  // CTAs per expert
+  const int64_t ei = blockIdx.x / cpb;
+  const int cg = threadIdx.x % kQCols, sl = threadIdx.x / kQCols;
+  const int64_t c0 = (blockIdx.x % cpb) * 8 * kQCols + cg * 8;
+  const bool live = c0 < n;
+  constexpr int qmax = BITS == 8 ? 127 : 7;
+  constexpr int offset = BITS == 8 ? 128 : 8;
+  const uint4* col = reinterpret_cast<const uint4*>(w + ei * m * n + (live ? c0 : 0));
+  const int64_t rs = n / 8;  // row stride in uint4
+  const int64_t r0 = m * sl / kQSlices, r1 = m * (sl + 1) / kQSlices;
+  float mx[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) mx[j] = 0.f;
+  unsigned long long first_bad = ~0ull;
+  auto scan = [&](const uint4& v, int64_t mi) {
+    const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint16_t h = (uint16_t)(wd[j >> 1] >> ((j & 1) * 16));
+      if ((h & 0x7C00) == 0x7C00)
+        first_bad = ::min(first_bad, (unsigned long long)((ei * m + mi) * n + c0 + j));
+      mx[j] = fmaxf(mx[j], fabsf(h2f(h)));
+    }
+  };
+  if (live) {
+    int64_t mi = r0;
+    for (; mi + 4 <= r1; mi += 4) {
+      uint4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = __ldg(col + (mi + u) * rs);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) scan(v[u], mi + u);
+    }
+    for (; mi < r1; ++mi) scan(__ldg(col + mi * rs), mi);
+    if (first_bad != ~0ull) atomicMin(bad, first_bad);
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) smx[sl][cg * 8 + j] = mx[j];
+  __syncthreads();
+  // quant_scale_from_maxabs (quantize.cpp:14-24), max over the slices
+  float sf[8];
+  uint16_t sh[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    float v = 0.f;
+    for (int q = 0; q < kQSlices; ++q) v = fmaxf(v, smx[q][cg * 8 + j]);
+    uint16_t s = 0x3C00;
+    if (v != 0.0f) {
+      s = f2h(__fdiv_rn(v, (float)qmax));
+      if ((s & 0x7FFF) == 0) s = 0x0001;
+    }
+    sh[j] = s;
+    sf[j] = h2f(s);
+  }
+  if (!live) return;
+  if (sl == 0)
+    *reinterpret_cast<uint4*>(scales + ei * n + c0) =
+        make_uint4(sh[0] | (uint32_t)sh[1] << 16, sh[2] | (uint32_t)sh[3] << 16,
+                   sh[4] | (uint32_t)sh[5] << 16, sh[6] | (uint32_t)sh[7] << 16);
+  auto emit = [&](const uint4& v, int64_t mi) {
+    const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
+    uint32_t code[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float q = roundf(__fdiv_rn(h2f((uint16_t)(wd[j >> 1] >> ((j & 1) * 16))), sf[j]));
+      code[j] = (uint32_t)((int)fminf(fmaxf(q, (float)-qmax), (float)qmax) + offset);
+    }
+    const int64_t flat = (ei * m + mi) * n + c0;
+    if constexpr (BITS == 8) {
+      *reinterpret_cast<uint2*>(packed + flat) =
+          make_uint2(code[0] | code[1] << 8 | code[2] << 16 | code[3] << 24,
+                     code[4] | code[5] << 8 | code[6] << 16 | code[7] << 24);
+    } else {
+      // quantize.cpp:44-47: v0|v2<<4, v4|v6<<4, v1|v3<<4, v5|v7<<4
+      *reinterpret_cast<uint32_t*>(packed + flat / 2) =
+          code[0] | code[2] << 4 | code[4] << 8 | code[6] << 12 | code[1] << 16 |
+          code[3] << 20 | code[5] << 24 | code[7] << 28;
+    }
+  };
+  int64_t mi = r0;
+  for (; mi + 4 <= r1; mi += 4) {
+    uint4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = __ldg(col + (mi + u) * rs);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) emit(v[u], mi + u);
+  }
+  for (; mi < r1; ++mi) emit(__ldg(col + mi * rs), mi);
+}
+
 int launch_quantize(const uint16_t* w, int64_t e, int64_t m, int64_t n, int bits,
                     uint8_t* packed, uint16_t* scales, unsigned long long* bad,
                     cudaStream_t st) {
+  const bool vec = n % 8 == 0 && ((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(scales) |
+                                   reinterpret_cast<uintptr_t>(packed)) & 15) == 0;
+  if (vec) {
+    const unsigned blocks = (unsigned)(e * ((n + 8 * kQCols - 1) / (8 * kQCols)));
+    if (bits == 8)
+      quantize8_kernel<8><<<blocks, 256, 0, st>>>(w, e, m, n, packed, scales, bad);
+    else
+      quantize8_kernel<4><<<blocks, 256, 0, st>>>(w, e, m, n, packed, scales, bad);
+    note_launch();
+    return check_launch("quantize");
+  }
   const int64_t cols_per_e = (n + 255) / 256 * 256;
   const int64_t blocks = e * cols_per_e / 256;
   if (bits == 8)

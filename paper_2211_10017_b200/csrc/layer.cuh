@@ -60,7 +60,13 @@ struct moe_layer {
   };
   std::vector<Graph> graphs;  // small LRU-less cache
   cudaStream_t cap_stream = nullptr;
-  uint32_t* hstatus = nullptr;  // pinned: bad_row, bad_expert of the last host-path forward
+  uint32_t* hstatus = nullptr;  // pinned: (bad_row, bad_expert) per chunk of the last host-path forward
+  // chunked host path: copy-in / copy-out streams forked from the capture
+  // stream, fork/join events, per-chunk status words (device)
+  cudaStream_t io_in = nullptr, io_out = nullptr;
+  std::vector<cudaEvent_t> io_ev;
+  uint32_t* dstatus = nullptr;
+  static constexpr int kMaxChunks = 8;
 
   void drop_graphs() {
     for (auto& g : graphs)
@@ -70,6 +76,9 @@ struct moe_layer {
   ~moe_layer() {
     drop_graphs();
     if (cap_stream) cudaStreamDestroy(cap_stream);
+    if (io_in) cudaStreamDestroy(io_in);
+    if (io_out) cudaStreamDestroy(io_out);
+    for (cudaEvent_t e : io_ev) cudaEventDestroy(e);
     if (hstatus) cudaFreeHost(hstatus);
     for (void* p : allocs) cudaFree(p);
     for (cudaEvent_t e : ev) cudaEventDestroy(e);
@@ -130,6 +139,9 @@ int layer_ffn(moe_layer* L, const uint16_t* xin, int64_t rows, const uint32_t* p
               int64_t np, int mode, uint16_t* h, uint16_t* out, cudaStream_t st, Marks& mark,
               const GemmArgs* comb = nullptr);
 int layer_grow_hidden(moe_layer* L, int64_t rows);  // EP: L->ep_h holds >= rows x f
+// the whole layer (moe_ffn_forward) on one stream, no host synchronisation
+int layer_forward(moe_layer* L, const uint16_t* x, const uint8_t* fin, int64_t T, int k, int mode,
+                  uint16_t* out, cudaStream_t st);
 }  // namespace moecu
 
 #define TRY(x)                     \

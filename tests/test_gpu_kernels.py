@@ -20,7 +20,8 @@ def _ops():
 
 # --------------------------------------------------------------------- quantize
 @pytest.mark.parametrize("bits", [8, 4])
-@pytest.mark.parametrize("shape", [(1, 3, 8), (2, 16, 8), (8, 64, 16), (3, 7, 24), (4, 33, 136)])
+@pytest.mark.parametrize("shape", [(1, 3, 8), (2, 16, 8), (8, 64, 16), (3, 7, 24), (4, 33, 136),
+                                   (3, 301, 264), (2, 1024, 520)])
 def test_quantize_matches_oracle(cuda, oracle, bits, shape):
     rng = np.random.default_rng(hash((bits,) + shape) % 2**32)
     w = rng.uniform(-4, 4, shape).astype(np.float16)
@@ -31,6 +32,37 @@ def test_quantize_matches_oracle(cuda, oracle, bits, shape):
 
 
 @pytest.mark.parametrize("bits", [8, 4])
+def test_quantize_int8_ragged_columns(cuda, oracle):
+    """int8 with n % 8 != 0 (the scalar per-column kernel)."""
+    rng = np.random.default_rng(12)
+    for shape in [(2, 17, 12), (1, 5, 3), (3, 40, 100)]:
+        w = rng.uniform(-3, 3, shape).astype(np.float16)
+        p_ref, s_ref = oracle.quantize(w, 8)
+        p, s = _ops().quantize(to_dev(w), 8)
+        assert np.array_equal(to_np(p), p_ref)
+        assert np.array_equal(bits16(to_np(s)), bits16(s_ref))
+
+
+def test_quantize_half_integer_quotients(cuda, oracle):
+    """Weights placed exactly on and one ulp around code boundaries (w = (j +
+    0.5) * s): round-half-away must match llround(f64 w / f64 s)."""
+    rng = np.random.default_rng(5)
+    for bits, qmax in ((4, 7), (8, 127)):
+        s = np.float16(2.0 ** -6)  # qmax * s and (j + 0.5) * s are exact in fp16
+        m, n = 64, 16
+        w = np.zeros((1, m, n), np.float16)
+        w[0, 0, :] = np.float16(qmax) * s  # pins maxabs -> the scale s
+        j = rng.integers(-qmax, qmax, (m - 1, n)).astype(np.float64) + 0.5
+        v = (j * np.float64(s)).astype(np.float16)
+        bump = rng.integers(-1, 2, v.shape).astype(np.int16)
+        v = (v.view(np.int16) + bump).view(np.float16)
+        w[0, 1:, :] = v
+        p_ref, s_ref = oracle.quantize(w, bits)
+        p, sc = _ops().quantize(to_dev(w), bits)
+        assert np.array_equal(to_np(p), p_ref)
+        assert np.array_equal(bits16(to_np(sc)), bits16(s_ref))
+
+
 def test_quantize_degenerate_and_subnormal(cuda, oracle, bits):
     w = np.zeros((2, 24, 8), np.float16)
     w[0, :, 1] = np.float16(2.0**-24)            # smallest subnormals

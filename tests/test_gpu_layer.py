@@ -191,3 +191,41 @@ def test_layer_fast_repeat_bitwise_deterministic(cuda, bits, f):
         got = to_np(L.forward(x, fin, k=1, mode=1))
         assert np.array_equal(bits16(got), bits16(ref))
 
+
+
+def _pinned_like(a):
+    import torch
+    t = torch.empty(a.shape, dtype=torch.int16 if a.dtype == np.float16 else torch.uint8,
+                    pin_memory=True)
+    v = t.numpy().view(a.dtype)
+    v[...] = a
+    return t, v
+
+
+@pytest.mark.parametrize("k", [1, 2])
+def test_layer_host_pinned_chunked_pipeline(cuda, oracle, k):
+    """Pinned host buffers: moe_layer_forward_host pipelines copy-in / compute
+    / copy-out over token chunks on three streams (C2 shape, 4 chunks).
+    EXACT: bit-identical to the device path and the per-token oracle; FAST:
+    identical to the device path (rows are independent), finished rows pass
+    through; a non-finite token in a late chunk is reported by its global row."""
+    lw, x, fin = _case(512, 2048, 8, 4096, seed=77 + k, fin_frac=0.1)
+    L = _layer(lw, 4)
+    q = tuple(to_np(t) for t in L.quant)
+    xt, xh = _pinned_like(x)
+    ft, fh = _pinned_like(fin)
+    ot, oh = _pinned_like(np.zeros_like(x))
+    for mode in (0, 1):
+        L.forward_host(xh, fh, k=k, mode=mode, out_host=oh)
+        dev = to_np(L.forward(to_dev(x), to_dev(fin), k=k, mode=mode))
+        if mode == 0:
+            assert np.array_equal(bits16(oh), bits16(dev))
+            rows = np.arange(0, 4096, 97)
+            want = oracle.moe_per_token(lw, x[rows], fin[rows], k=k, bits=4, q=q)
+            assert np.array_equal(bits16(oh[rows]), bits16(want))
+        else:
+            assert layer_err(oh, dev, x) <= TOL_FAST
+        assert np.array_equal(bits16(oh)[fin == 1], bits16(x)[fin == 1])
+    xh[3500, 7] = np.inf
+    with pytest.raises(ValueError, match="non-finite logit at row 3500"):
+        L.forward_host(xh, fh, k=k, mode=1, out_host=oh)
