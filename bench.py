@@ -445,8 +445,10 @@ def run_decode(args, wl):
     stream = torch.cuda.current_stream()
     res = {}
     for prune in (False, True):
+        n_cap = abi.launch_count()
         decode_run(layers, xs, fin, k=k, mode=1, prune=prune, out=out, work=work)
         torch.cuda.synchronize()
+        per_decode = abi.launch_count() - n_cap  # kernels in one decode (= one graph replay)
         gr = torch.cuda.CUDAGraph()
         with torch.cuda.graph(gr):
             decode_run(layers, xs, fin, k=k, mode=1, prune=prune, out=out, work=work)
@@ -454,15 +456,13 @@ def run_decode(args, wl):
             gr.replay()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        n0 = abi.launch_count()
         with ClockSampler(0) as clk:
             e0.record(stream)
             for _ in range(args.steps):
                 gr.replay()
             e1.record(stream)
             torch.cuda.synchronize()
-        res[prune] = (e0.elapsed_time(e1) / args.steps, clk.summary(),
-                      abi.launch_count() - n0)
+        res[prune] = (e0.elapsed_time(e1) / args.steps, clk.summary(), per_decode * args.steps)
     ms_on, clk, launches = res[True]
     ms_off = res[False][0]
     line = {
@@ -618,8 +618,13 @@ def run_native(args, wl):
     S = T * k
     gemm_ms = gemm_stage["ffn_pair"]
     flops = 4.0 * S * d * f
-    # decode-shaped workloads are bounded by streaming the active experts' weights
-    active = E * (1 - (1 - 1 / E) ** S)
+    # decode-shaped workloads are bounded by streaming the active experts'
+    # weights: the active-expert count of each copy's own routing plan
+    # (moe_layer_load_report), averaged over the copies
+    reps_ = [L.load_report(1.0) for L in layers]
+    active = sum(r["active_experts"] for r in reps_) / len(reps_)
+    load = reps_[0]
+    load125 = layers[0].load_report(1.25)
     wbytes = active * (d * f + 4 * (f + d)) + S * (d + f) * 2 * 2
     t_tc, t_hbm = flops / (tc_burst * 1e12), wbytes / (hbm * 1e9)
     if t_tc >= t_hbm:
@@ -630,7 +635,7 @@ def run_native(args, wl):
         roof = {"bound": "hbm", "achieved": wbytes / (gemm_ms * 1e-3) / 1e9, "peak": hbm,
                 "unit": "GB/s"}
         alg = (f"active*(d*f + 4(f+d)) + S*(d+f)*4 = {wbytes:.4g} B per step over 2 launches "
-               f"(expected active experts {active:.1f})")
+               f"(active experts {active:.1f}, from the runs' own routing plans)")
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["traffic"] = load_traffic(args.workload)
     kname = ("gemv_kernel<4> (K5 FFN1 + FFN2, mma.sync over the tcgen05 weight tiles)"
@@ -655,6 +660,17 @@ def run_native(args, wl):
                          f"({R * per_copy / 2**20:.0f} MiB > 2x L2)"},
         "roofline": roof,
         "layer_roofline_frac": layer_roof_t / (ms / args.steps * 1e-3),
+        "expert_load": {"note": "moe_layer_load_report of layer copy 0's last forward; nothing "
+                                "is dropped (reference routes every live slot)",
+                        "live_slots": load["live_slots"], "active_experts": load["active_experts"],
+                        "max_load": load["max_load"], "mean_load": load["live_slots"] / E,
+                        "max_over_mean": load["imbalance"],
+                        "capacity_1.0": {"capacity": load["capacity"],
+                                         "experts_over": load["experts_over"],
+                                         "overflow_rows": load["overflow_rows"]},
+                        "capacity_1.25": {"capacity": load125["capacity"],
+                                          "experts_over": load125["experts_over"],
+                                          "overflow_rows": load125["overflow_rows"]}},
         "stage_ms": stage_ms,
         "stage_ms_note": "per-stage CUDA events inside the layer graph (each event node adds "
                          "~2-3 us; shares, not a sum to ms_per_step). roofline.kernel_ms_per_step "

@@ -804,7 +804,12 @@ int moe_layer_forward_host(moe_layer* L, const uint16_t* x_host, const uint8_t* 
     MOE_CUDA_TRY(cudaStreamWaitEvent(cs, jout, 0));
     return MOE_OK;
   };
-  if (pinned) {
+  static const bool use_graph = !(std::getenv("MOE_HOST_GRAPH") && std::atoi(std::getenv("MOE_HOST_GRAPH")) == 0);
+  if (pinned && c > 1 && !use_graph) {
+    // dev A/B: the pipelined streams launched directly (no graph)
+    TRY(piped(st));
+    MOE_CUDA_TRY(cudaStreamSynchronize(st));
+  } else if (pinned) {
     // pinned buffers: one captured graph (copies + kernels + status readback)
     moe_layer::GraphKey key{x_host, fin_host, out_host, T, k, mode, 1 + c, L->prof_level};
     cudaGraphExec_t exec = nullptr;

@@ -12,14 +12,19 @@
 //               plan offsets; exchanged device-to-device (G x E/G u32 each way)
 //   3. one D2H of the sent + received counts (the only host synchronisation:
 //               NCCL point-to-point sizes are host arguments)
-//   4. dispatch per (peer, local expert) segment: ncclSend of the sorted rows,
-//               ncclRecv straight into EXPERT-MAJOR position -- the regroup
-//               of the received rows happens in the transport, no gather
+//   4. dispatch ONE ncclSend per peer (the sorted rows owned by that peer are
+//               contiguous) and one ncclRecv per source into a staging buffer
+//               ((source, local expert)-major); a segment-copy kernel regroups
+//               the rows EXPERT-major for the grouped GEMMs (one message per
+//               peer: NCCL point-to-point costs ~5 us per operation, so
+//               per-(peer, expert) messages -- E of them -- cost more than the
+//               extra on-device copy)
 //   5. experts  FFN1 + FFN2 of the local experts over the received rows
 //               (layer_ffn: tcgen05 grouped GEMM, or the decode GEMV)
-//   6. combine  the reverse segment exchange lands every row back at its
-//               sorted position in the sender's y; then the local residual +
-//               gate-scaled un-permute (combine_kernel)
+//   6. combine  the inverse segment copy puts the results back in
+//               (source, expert) order, one ncclSend per source returns them
+//               straight to their sorted positions in the sender's y; then the
+//               local residual + gate-scaled un-permute (combine_kernel)
 //
 // Rows are independent in every kernel, so with the same kernel choices an
 // EP forward is bit-identical to the single-GPU layer on the same tokens
@@ -98,11 +103,15 @@ int nccl_error(ncclResult_t r, const char* what) {
 // ------------------------------------------------------------------- state
 // Per local rank: device + pinned-host exchange state of the last forward.
 struct EpRank {
-  uint32_t* dcnt = nullptr;   // device: send counts [G*el] | recv counts [G*el] | problems [el*3]
-  uint32_t* hcnt = nullptr;   // pinned: send | recv | bad_row, bad_expert | problems [el*3]
+  // device: send counts [G*el] | recv counts [G*el] | problems [el*3] | segments [G*el*3]
+  uint32_t* dcnt = nullptr;
+  // pinned: send | recv | bad_row, bad_expert | problems [el*3] | segments [G*el*3]
+  uint32_t* hcnt = nullptr;
+  uint16_t *xr = nullptr;     // received rows, (source, expert)-major; reused for the results
   uint16_t *xe = nullptr, *ye = nullptr;  // received rows (expert-major) and their FFN output
-  int64_t cap = 0;            // rows xe / ye hold
+  int64_t cap = 0;            // rows xr / xe / ye hold
   int64_t rows = 0;           // rows received in the last forward
+  int nseg = 0;               // non-empty (source, expert) segments of the last forward
   std::vector<int64_t> send_off, recv_dst;
 };
 
@@ -116,6 +125,7 @@ struct moe_ep {
     for (auto& x : r) {
       if (x.dcnt) cudaFree(x.dcnt);
       if (x.hcnt) cudaFreeHost(x.hcnt);
+      if (x.xr) cudaFree(x.xr);
       if (x.xe) cudaFree(x.xe);
       if (x.ye) cudaFree(x.ye);
     }
@@ -131,6 +141,27 @@ namespace moecu {
 __global__ void ep_counts_kernel(const uint32_t* __restrict__ offsets, int64_t E,
                                  uint32_t* __restrict__ cnt) {
   for (int64_t e = threadIdx.x; e < E; e += blockDim.x) cnt[e] = offsets[e + 1] - offsets[e];
+}
+
+// Row moves between the staging order ((source, expert)-major) and the
+// expert-major GEMM order: one CTA per segment {staging row, expert-major
+// row, rows}; inverse swaps source and destination.
+__global__ void ep_regroup_kernel(const uint32_t* __restrict__ seg, const uint16_t* __restrict__ src,
+                                  uint16_t* __restrict__ dst, int64_t d, int inverse) {
+  const uint32_t a = seg[3 * blockIdx.x], b = seg[3 * blockIdx.x + 1], nr = seg[3 * blockIdx.x + 2];
+  // blockIdx.y splits the segment's rows (large segments over several CTAs)
+  const uint32_t r0 = (uint32_t)((uint64_t)nr * blockIdx.y / gridDim.y);
+  const uint32_t n = (uint32_t)((uint64_t)nr * (blockIdx.y + 1) / gridDim.y) - r0;
+  const int64_t from = (int64_t)(inverse ? b : a) + r0, to = (int64_t)(inverse ? a : b) + r0;
+  if (d % 8 == 0) {
+    const int64_t q = d / 8, total = (int64_t)n * q;
+    const uint4* s4 = reinterpret_cast<const uint4*>(src + from * d);
+    uint4* d4 = reinterpret_cast<uint4*>(dst + to * d);
+    for (int64_t i = threadIdx.x; i < total; i += blockDim.x) d4[i] = s4[i];
+  } else {
+    const int64_t total = (int64_t)n * d;
+    for (int64_t i = threadIdx.x; i < total; i += blockDim.x) dst[to * d + i] = src[from * d + i];
+  }
 }
 
 // Sends issued by local rank i and receives posted by local rank i, in
@@ -195,8 +226,8 @@ static int ep_bind(moe_ep* ep, moe_layer* const* layers) {
     ep->r.resize(n);
     const int64_t G = ep->G, el = ep->el;
     for (auto& x : ep->r) {
-      MOE_CUDA_TRY(cudaMalloc(&x.dcnt, (2 * G * el + 3 * el) * 4));
-      MOE_CUDA_TRY(cudaMallocHost(&x.hcnt, (2 * G * el + 2 + 3 * el) * 4));
+      MOE_CUDA_TRY(cudaMalloc(&x.dcnt, (2 * G * el + 3 * el + 3 * G * el) * 4));
+      MOE_CUDA_TRY(cudaMallocHost(&x.hcnt, (2 * G * el + 2 + 3 * el + 3 * G * el) * 4));
       x.send_off.resize(G * el);
       x.recv_dst.resize(G * el);
     }
@@ -329,48 +360,79 @@ int moe_ep_forward(moe_ep* ep, moe_layer* const* layers, const uint16_t* const* 
   for (int i = 0; i < n; ++i) {
     EpRank& R = ep->r[i];
     uint32_t* prob = R.hcnt + 2 * G * el + 2;
+    uint32_t* segt = prob + 3 * el;
     TRY(moe_ep_segments(G, el, R.hcnt, R.hcnt + G * el, R.send_off.data(), R.recv_dst.data(),
                         prob, &R.rows));
+    // staging order: source-major, experts in order inside a source
+    const uint32_t* rc = R.hcnt + G * el;
+    int64_t pos = 0;
+    R.nseg = 0;
+    for (int s2 = 0; s2 < G; ++s2)
+      for (int64_t j = 0; j < el; ++j) {
+        const uint32_t c = rc[s2 * el + j];
+        if (c == 0) continue;
+        segt[3 * R.nseg] = (uint32_t)pos;
+        segt[3 * R.nseg + 1] = (uint32_t)R.recv_dst[s2 * el + j];
+        segt[3 * R.nseg + 2] = c;
+        ++R.nseg;
+        pos += c;
+      }
     if (R.rows > R.cap) {  // grow the receive buffers (rows of the exchange)
-      if (R.xe) cudaFree(R.xe);
-      if (R.ye) cudaFree(R.ye);
-      R.xe = R.ye = nullptr;
+      for (uint16_t** b : {&R.xr, &R.xe, &R.ye})
+        if (*b) {
+          cudaFree(*b);
+          *b = nullptr;
+        }
       const int64_t cap = R.rows + R.rows / 4 + 64;
+      MOE_CUDA_TRY(cudaMalloc(&R.xr, cap * d * 2));
       MOE_CUDA_TRY(cudaMalloc(&R.xe, cap * d * 2));
       MOE_CUDA_TRY(cudaMalloc(&R.ye, cap * d * 2));
       R.cap = cap;
     }
     TRY(layer_grow_hidden(layers[i], std::max<int64_t>(R.rows, 1)));
-    MOE_CUDA_TRY(cudaMemcpyAsync(R.dcnt + 2 * G * el, prob, 3 * el * 4, cudaMemcpyHostToDevice, st));
+    MOE_CUDA_TRY(cudaMemcpyAsync(R.dcnt + 2 * G * el, prob, (3 * el + 3 * (int64_t)R.nseg) * 4,
+                                 cudaMemcpyHostToDevice, st));
   }
-  // 4. dispatch: sorted rows -> expert-major receive buffer
+  // one message per (rank pair): rows [send_off[p*el], +sum_j sent[p][j]) of
+  // the sorted buffer <-> staging rows [base_s, +sum_j recv[s][j])
   const size_t rb = (size_t)d * 2;
-  auto segments = [&](bool forward) {
+  auto pairs = [&](bool forward) {
     Xfer xd(n);
     for (int i = 0; i < n; ++i) {
       EpRank& R = ep->r[i];
       const uint32_t *sc = R.hcnt, *rc = R.hcnt + G * el;
-      for (int p = 0; p < G; ++p)
-        for (int64_t j = 0; j < el; ++j) {
-          const int64_t c = sc[p * el + j];
-          if (c == 0) continue;
-          uint16_t* base = forward ? layers[i]->xp : layers[i]->y;
-          (forward ? xd.send : xd.recv)[i].push_back({p, base + R.send_off[p * el + j] * d, c * rb});
-        }
-      for (int s = 0; s < G; ++s)
-        for (int64_t j = 0; j < el; ++j) {
-          const int64_t c = rc[s * el + j];
-          if (c == 0) continue;
-          uint16_t* base = forward ? R.xe : R.ye;
-          (forward ? xd.recv : xd.send)[i].push_back({s, base + R.recv_dst[s * el + j] * d, c * rb});
-        }
+      uint16_t* sorted = forward ? layers[i]->xp : layers[i]->y;
+      for (int p = 0; p < G; ++p) {
+        int64_t c = 0;
+        for (int64_t j = 0; j < el; ++j) c += sc[p * el + j];
+        if (c) (forward ? xd.send : xd.recv)[i].push_back({p, sorted + R.send_off[p * el] * d, c * rb});
+      }
+      int64_t base = 0;
+      for (int s2 = 0; s2 < G; ++s2) {
+        int64_t c = 0;
+        for (int64_t j = 0; j < el; ++j) c += rc[s2 * el + j];
+        if (c) (forward ? xd.recv : xd.send)[i].push_back({s2, R.xr + base * d, c * rb});
+        base += c;
+      }
     }
     return xd;
   };
+  auto regroup = [&](int i, int inverse) -> int {
+    EpRank& R = ep->r[i];
+    if (R.nseg == 0) return MOE_OK;
+    // ~2 CTAs per SM over all segments
+    const int ys = (int)std::max<int64_t>(1, std::min<int64_t>(32, (2 * sm_count() + R.nseg - 1) / R.nseg));
+    ep_regroup_kernel<<<dim3(R.nseg, ys), 256, 0, st>>>(R.dcnt + 2 * G * el + 3 * el, inverse ? R.ye : R.xr,
+                                              inverse ? R.xr : R.xe, d, inverse);
+    note_launch();
+    return check_launch("ep_regroup");
+  };
+  // 4. dispatch + regroup
   {
-    Xfer xd = segments(true);
+    Xfer xd = pairs(true);
     TRY(run_xfer(ep, xd, st));
   }
+  for (int i = 0; i < n; ++i) TRY(regroup(i, 0));
   // 5. local experts
   for (int i = 0; i < n; ++i) {
     EpRank& R = ep->r[i];
@@ -379,9 +441,10 @@ int moe_ep_forward(moe_ep* ep, moe_layer* const* layers, const uint16_t* const* 
     Marks mark(L, st, false);
     TRY(layer_ffn(L, R.xe, R.rows, R.dcnt + 2 * G * el, el, mode, L->ep_h, R.ye, st, mark));
   }
-  // 6. combine: results back to the senders' sorted positions, then residual
+  // 6. results back in staging order, one message per rank pair, then residual
+  for (int i = 0; i < n; ++i) TRY(regroup(i, 1));
   {
-    Xfer xb = segments(false);
+    Xfer xb = pairs(false);
     TRY(run_xfer(ep, xb, st));
   }
   for (int i = 0; i < n; ++i) {

@@ -657,6 +657,14 @@ static int run_tc_bits(const GemmArgs& a, cudaStream_t st) {
   // width: 128/160/192/224 TS, 256 SS, 257 TS single-accumulator).
   const int64_t nft = (a.n + 127) / 128;
   static const int force = std::getenv("MOE_TC_BN") ? std::atoi(std::getenv("MOE_TC_BN")) : 0;
+  static const bool small_pairs =
+      !(std::getenv("MOE_TC_SMALL_PAIR") && std::atoi(std::getenv("MOE_TC_SMALL_PAIR")) == 0);
+  if (a.rows_hint >= 32 && a.rows_hint < 96 && small_pairs && nft % 2 == 0 && force == 0) {
+    // few rows per expert (C5's 64): every weight tile serves one short token
+    // tile, and a single CTA re-reads 2 B of activations from L2 per weight
+    // byte; the pair halves that stream and the MMA issues per SM
+    return run_tc<BITS, 96, true, 2>(a, st);
+  }
   if (a.rows_hint >= 96) {
     static const bool pair_ok = !(std::getenv("MOE_TC_PAIR") && std::atoi(std::getenv("MOE_TC_PAIR")) == 0);
     if (pair_ok && nft % 2 == 0) {

@@ -17,7 +17,10 @@
 // Loads run U k-blocks ahead (double-buffered registers) so every warp keeps
 // 2-4 KB in flight.  Split-K partials (f32) are reduced in a fixed order by
 // the last CTA of each (problem, feature tile) -- deterministic.
+#include <cstdio>
+#include <cstdlib>
 #include <type_traits>
+#include <vector>
 
 #include "kernels.cuh"
 
@@ -111,7 +114,14 @@ struct Params {
   uint32_t db2;           // debias constant in both halves
   uint32_t hb2;           // -(64 + debias - 1024) in both halves (i2f_u4_fast)
   int nitems;             // np * nft * nsplit work items, strided over persistent CTAs
+  long long* trace;       // dev-only (MOE_GEMV_TRACE): per CTA [start, prologue, items, k-loop ns, x-stage ns, epi ns, end]
 };
+
+__device__ __forceinline__ long long gv_time() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 // Weight blocks stream through a ring of NST stages (TMA bulk copies issued
 // by a producer warp, mbarrier full/empty handshake); the 8 compute warps read
@@ -203,6 +213,9 @@ __global__ void __launch_bounds__(kThreads, 3) gemv_kernel(const Params P) {
   __shared__ int s_nlive;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int kp = P.kbs_per_split * 64 + 8;  // row pitch of xs (conflict-free fragments)
+  const long long t_start = P.trace ? gv_time() : 0;
+  long long t_k = 0, t_x = 0, t_e = 0;
+  int n_it = 0;
   if (threadIdx.x == 0) {
     for (int i = 0; i < RG::NST; ++i) {
       mbar_init(&full[i], 1);
@@ -225,6 +238,7 @@ __global__ void __launch_bounds__(kThreads, 3) gemv_kernel(const Params P) {
   }
   __syncthreads();
   const int nitems = s_nlive * P.nsplit * (int)P.nft;
+  const long long t_pro = P.trace ? gv_time() : 0;
 
   if (warp == kWarps) {
     // ------------------------------------------------------------- producer
@@ -282,6 +296,7 @@ __global__ void __launch_bounds__(kThreads, 3) gemv_kernel(const Params P) {
       const int kq = nkbl * 8;  // 16-byte pieces per staged row
       for (int64_t rb = it.r0; rb < it.r1; rb += NT) {
         const int nrow = (int)(it.r1 - rb < (int64_t)NT ? it.r1 - rb : (int64_t)NT);
+        long long tt0 = P.trace ? gv_time() : 0;
         if (rb != staged_r || it.kb0 != staged_kb) {  // same rows as the last item: reuse
           named_bar_sync(1, kCompute);  // everyone done with xs
           for (int q = threadIdx.x; q < nrow * kq; q += kCompute) {
@@ -297,6 +312,9 @@ __global__ void __launch_bounds__(kThreads, 3) gemv_kernel(const Params P) {
           staged_kb = it.kb0;
         }
 
+        long long tt1 = P.trace ? gv_time() : 0;
+        t_x += tt1 - tt0;
+        ++n_it;
         float acc[2][2][4];
 #pragma unroll
         for (int j = 0; j < 2; ++j)
@@ -339,6 +357,9 @@ __global__ void __launch_bounds__(kThreads, 3) gemv_kernel(const Params P) {
           kloop(std::integral_constant<int, 2>{});
         else
           kloop(std::integral_constant<int, 1>{});
+        long long tt2 = P.trace ? gv_time() : 0;
+        t_k += tt2 - tt1;
+        tt0 = tt2;
 #pragma unroll
         for (int j = 0; j < 2; ++j)
 #pragma unroll
@@ -361,6 +382,7 @@ __global__ void __launch_bounds__(kThreads, 3) gemv_kernel(const Params P) {
             }
           }
       }
+      const long long te0 = P.trace ? gv_time() : 0;
       if (P.nsplit > 1) {
         // last CTA of this (expert, feature tile) reduces the splits in order
         __threadfence();
@@ -388,6 +410,17 @@ __global__ void __launch_bounds__(kThreads, 3) gemv_kernel(const Params P) {
           if (threadIdx.x == 0) P.ticket[it.e * P.nft + it.ft] = 0;
         }
       }
+      if (P.trace) t_e += gv_time() - te0;
+    }
+    if (P.trace && threadIdx.x == 0) {
+      long long* tr = P.trace + 8 * blockIdx.x;
+      tr[0] = t_start;
+      tr[1] = t_pro - t_start;
+      tr[2] = n_it;
+      tr[3] = t_k;
+      tr[4] = t_x;
+      tr[5] = t_e;
+      tr[6] = gv_time();
     }
   }
 }
@@ -454,8 +487,35 @@ static int run_gemv(const GemmArgs& a, const GemvWork& w, cudaStream_t st) {
   const int64_t live = std::max<int64_t>(1, std::min<int64_t>(a.np, a.rows));
   const int64_t grid =
       std::max<int64_t>(1, std::min<int64_t>(live * P.nft * P.nsplit, 3 * (int64_t)sm_count()));
+  static long long* dtrace = nullptr;
+  const bool tr = std::getenv("MOE_GEMV_TRACE") != nullptr;
+  if (tr && !dtrace) MOE_CUDA_TRY(cudaMalloc(&dtrace, 8 * 8 * 4096));
+  P.trace = tr ? dtrace : nullptr;
+  if (tr) MOE_CUDA_TRY(cudaMemsetAsync(dtrace, 0, 8 * 8 * grid, st));
   MOE_CUDA_TRY(launch_k(4, gv::gemv_kernel<BITS>, dim3((unsigned)grid), dim3(gv::kThreads), smem, st, P));
   note_launch();
+  if (tr) {  // dev instrumentation: per-CTA phase times (ns)
+    std::vector<long long> h(8 * grid);
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h.data(), dtrace, h.size() * 8, cudaMemcpyDeviceToHost);
+    long long lo = h[0], hi = h[6];
+    double pro = 0, items = 0, tk = 0, tx = 0, te = 0, span = 0;
+    for (int64_t b = 0; b < grid; ++b) {
+      lo = std::min(lo, h[8 * b]);
+      hi = std::max(hi, h[8 * b + 6]);
+      pro += h[8 * b + 1];
+      items += h[8 * b + 2];
+      tk += h[8 * b + 3];
+      tx += h[8 * b + 4];
+      te += h[8 * b + 5];
+      span += h[8 * b + 6] - h[8 * b];
+    }
+    std::fprintf(stderr,
+                 "gemv m=%lld n=%lld rows=%lld nsplit=%d grid=%lld: kernel span %lld ns; per CTA mean: "
+                 "life %.0f ns, prologue %.0f, items %.2f, x-stage %.0f, k-loop %.0f, epilogue %.0f\n",
+                 (long long)a.m, (long long)a.n, (long long)a.rows, P.nsplit, (long long)grid,
+                 hi - lo, span / grid, pro / grid, items / grid, tx / grid, tk / grid, te / grid);
+  }
   return check_launch("gemv");
 }
 

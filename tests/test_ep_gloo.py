@@ -1,9 +1,11 @@
 """Expert-parallel host logic on CPU, world_size 2 and 4 over gloo.
 
 The exchange protocol of csrc/ep.cu (moe_ep_forward) is replayed with gloo
-point-to-point transfers in the same issue order as its NCCL transport, and
-the product's C++ segment arithmetic (moe_ep_segments, called through the
-C-ABI -- pure host code, no GPU) places every row.  The local compute (LN,
+point-to-point transfers -- one message per rank pair in the same issue
+order as its NCCL transport, the staging -> expert-major segment copies of
+its regroup kernel -- and the product's C++ segment arithmetic
+(moe_ep_segments, called through the C-ABI -- pure host code, no GPU)
+places every row.  The local compute (LN,
 gate, plan, expert FFNs, combine) is the C oracle.  Every rank's output must
 equal the single-process oracle layer on its tokens bit for bit (rows are
 independent), for top-1/top-2, int4/int8/fp16 experts, ragged and empty
@@ -80,13 +82,23 @@ def _worker(rank, world, port, cfg, results):
     # 3. the product's segment arithmetic (C++)
     so, rd, probs, rows = segments(G, el, send_cnt, recv_cnt)
     so, rd = so.reshape(G, el), rd.reshape(G, el)
-    # 4. dispatch, same issue order as ep.cu
-    xe = np.zeros((rows, d), np.int16)
-    sends = [(p, xp[so[p, j]:so[p, j] + send_cnt[p, j]]) for p in range(G) for j in range(el)
-             if send_cnt[p, j]]
-    recvs = [(s, xe[rd[s, j]:rd[s, j] + recv_cnt[s, j]]) for s in range(G) for j in range(el)
-             if recv_cnt[s, j]]
+    # 4. dispatch, same messages as ep.cu: one per rank pair into the
+    # (source, expert)-major staging buffer, then the regroup segment copies
+    base = np.concatenate([[0], np.cumsum(recv_cnt.sum(1))]).astype(np.int64)
+    segs = []  # (staging row, expert-major row, rows)
+    for s in range(G):
+        pos = base[s]
+        for j in range(el):
+            if recv_cnt[s, j]:
+                segs.append((pos, rd[s, j], recv_cnt[s, j]))
+                pos += recv_cnt[s, j]
+    xr = np.zeros((rows, d), np.int16)
+    sends = [(p, xp[so[p, 0]:so[p, 0] + send_cnt[p].sum()]) for p in range(G) if send_cnt[p].sum()]
+    recvs = [(s, xr[base[s]:base[s + 1]]) for s in range(G) if base[s + 1] > base[s]]
     _exchange(dist, torch, sends, recvs, rank)
+    xe = np.zeros((rows, d), np.int16)
+    for a, b, c in segs:
+        xe[b:b + c] = xr[a:a + c]
     # 5. local experts (oracle grouped GEMMs over the expert-major rows)
     sl = slice(e0, e0 + el)
     ye = np.zeros((rows, d), np.int16)
@@ -105,12 +117,13 @@ def _worker(rank, world, port, cfg, results):
             y, _ = orc.grouped_gemm(h, probs, bits=bits, packed=per(q[2], f, d), scales=q[3][sl],
                                     E=el, n=d, bias=lw.b2[sl], relu=False)
         ye[...] = y.view(np.int16)
-    # 6. reverse exchange into the sorted y, then the residual combine
+    # 6. inverse regroup, one message per rank pair back into the sorted y,
+    # then the residual combine
+    for a, b, c in segs:
+        xr[a:a + c] = ye[b:b + c]
     ys = np.zeros((int(offs[E]) if T else 0, d), np.int16)
-    sends = [(s, ye[rd[s, j]:rd[s, j] + recv_cnt[s, j]]) for s in range(G) for j in range(el)
-             if recv_cnt[s, j]]
-    recvs = [(p, ys[so[p, j]:so[p, j] + send_cnt[p, j]]) for p in range(G) for j in range(el)
-             if send_cnt[p, j]]
+    sends = [(s, xr[base[s]:base[s + 1]]) for s in range(G) if base[s + 1] > base[s]]
+    recvs = [(p, ys[so[p, 0]:so[p, 0] + send_cnt[p].sum()]) for p in range(G) if send_cnt[p].sum()]
     _exchange(dist, torch, sends, recvs, rank)
     if T:
         out = x.copy()

@@ -31,7 +31,6 @@ def test_quantize_matches_oracle(cuda, oracle, bits, shape):
     assert np.array_equal(bits16(to_np(s)), bits16(s_ref))
 
 
-@pytest.mark.parametrize("bits", [8, 4])
 def test_quantize_int8_ragged_columns(cuda, oracle):
     """int8 with n % 8 != 0 (the scalar per-column kernel)."""
     rng = np.random.default_rng(12)
@@ -63,6 +62,7 @@ def test_quantize_half_integer_quotients(cuda, oracle):
         assert np.array_equal(bits16(to_np(sc)), bits16(s_ref))
 
 
+@pytest.mark.parametrize("bits", [8, 4])
 def test_quantize_degenerate_and_subnormal(cuda, oracle, bits):
     w = np.zeros((2, 24, 8), np.float16)
     w[0, :, 1] = np.float16(2.0**-24)            # smallest subnormals
@@ -346,6 +346,8 @@ def test_gemm_fast_equals_exact_semantics_large(cuda, oracle):
     ([1000, 17, 1, 1500, 257, 999, 2048, 2182], 512, 2048),   # CTA pairs, 256-token SS tiles
     ([672] * 8, 512, 2048),                                   # CTA pairs, 224-token TS tiles
     ([300, 15, 33, 224, 225, 480, 600, 0, 431], 520, 1024),   # pairs, ragged + K tail
+    ([64, 70, 33, 95, 1, 0, 80, 50, 96, 17], 512, 1024),      # pairs, 96-token tiles (C5-like)
+    ([64] * 16, 1024, 2048),                                  # pairs, 96-token tiles, 64 rows
 ])
 def test_gemm_fast_cta_pair_ragged(cuda, sizes, m, n, bits):
     """cta_group::2 tiles (M = 256 over two SMs, each CTA holding half of the
