@@ -705,32 +705,25 @@ int moe_layer_forward(moe_layer* L, const uint16_t* x, const uint8_t* finished, 
   if (!L) return set_error(MOE_EINVAL, "layer: null");
   return layer_forward(L, x, finished, T, k, mode, out, S(stream));
 }
-// Chunks of the pinned host-buffer path: the layer splits its tokens into c
-// chunks and pipelines copy-in (chunk i+1), compute (chunk i) and copy-out
-// (chunk i-1) on three streams -- PCIe is full duplex, and both directions
-// overlap the kernels.  Rows are independent in every kernel, so chunking
-// never changes a result.  Cost model per c (B = 50 GB/s pinned PCIe, each
-// direction): t(c) = (t_in + t_out) / c + max(t_in, t_out, t_comp(c)),
-// where t_comp(c) re-streams the expert weights c times (each chunk routes
-// to every expert); c = 1 unless a larger c is predicted >= 10 % faster.
+// Chunks of the pinned host-buffer path: the layer splits its tokens into
+// two chunks and pipelines copy-in (chunk 1), compute (chunk 0) and
+// copy-out (chunk 0) on three streams -- PCIe is full duplex, and both
+// directions overlap the kernels.  Rows are independent in every kernel, so
+// chunking never changes a result.  Chunked when the PCIe time exceeds the
+// compute estimate and each chunk still routes >= 96 rows per expert (the
+// tcgen05 pair tiles; C5's 64 rows per expert would fall to short tiles and
+// re-stream 2 GB of weights).  Measured (pinned PCIe on the B200 boxes:
+// H2D ~25 GB/s, D2H ~50 GB/s): C2 305 us / step with 2 chunks against 405
+// with one; 4 chunks measured slower than 2 (per-chunk launch and
+// copy-engine costs).
 static int host_chunks(const moe_layer* L, int64_t T, int k) {
   if (T * k < 1024) return 1;  // decode-sized: one launch sequence
-  const double pcie = 50e9, hbm = 6.5e12, tc = 0.9e15;
-  const double io = (double)T * L->d * 2 / pcie;
-  const double wb = (double)L->El * L->d * L->f * (L->bits == 16 ? 4.0 : L->bits == 8 ? 2.0 : 1.0);
-  const double flops = 4.0 * T * k * L->d * L->f;
-  int best = 1;
-  double tbest = 2 * io + std::max(flops / tc, wb / hbm) + 20e-6;
-  for (int c = 2; c <= moe_layer::kMaxChunks; c *= 2) {
-    if (T / c < 256) break;
-    const double comp = std::max(flops / tc, c * wb / hbm) + c * 12e-6;
-    const double t = 2 * io / c + std::max(io, comp);
-    if (t < 0.9 * tbest) {
-      best = c;
-      tbest = t;
-    }
-  }
-  return best;
+  const double h2d = 25e9, d2h = 50e9, hbm = 6.5e12, tc = 0.45e15;
+  const double io = (double)T * L->d * 2 * (1 / h2d + 1 / d2h);
+  const double wb = (double)L->El * L->d * L->f * (L->bits == 16 ? 2.0 : L->bits == 8 ? 1.0 : 0.5);
+  const double comp = 4.0 * T * k * L->d * L->f / tc + wb / hbm;
+  const bool wide = (double)T * k / 2 / (double)L->El >= 96;
+  return io > comp && wide ? 2 : 1;
 }
 
 int moe_layer_forward_host(moe_layer* L, const uint16_t* x_host, const uint8_t* fin_host,

@@ -79,6 +79,7 @@ struct Cfg {
   // layers (NS = 3 / 7) faulted or gave non-deterministic outputs under
   // repeated route+FFN stress (scripts/stress_layer.py; root cause not yet
   // isolated); every measured config keeps its stage count or loses one
+  // at most 8 (16 measured no faster for C5's 96-token pair tiles)
   static constexpr int NS = NS0 > 8 ? 8 : (NS0 & ~1);
   // [TMA stages][B | W] | [SS: A stages] | epilogue staging | barriers | table
   static constexpr int OFF_A = NS * STAGE;

@@ -114,6 +114,9 @@ struct Params {
   uint32_t db2;           // debias constant in both halves
   uint32_t hb2;           // -(64 + debias - 1024) in both halves (i2f_u4_fast)
   int nitems;             // np * nft * nsplit work items, strided over persistent CTAs
+  int early;              // second GEMM of an FFN pair: problems and weights are read before
+                          // the programmatic-dependent-launch wait (only x is the previous
+                          // kernel's output)
   long long* trace;       // dev-only (MOE_GEMV_TRACE): per CTA [start, prologue, items, k-loop ns, x-stage ns, epi ns, end]
 };
 
@@ -224,7 +227,11 @@ __global__ void __launch_bounds__(kThreads, 3) gemv_kernel(const Params P) {
     fence_barrier_init();
   }
   griddep_launch();
-  griddep_wait();  // problems / activations come from the previous kernels
+  // FFN1: problems and activations come from the previous kernel.  FFN2
+  // (early): the problems were written two kernels back (complete before
+  // FFN1 started), the weights never change -- the prologue and the weight
+  // stream start while FFN1 retires; the compute warps wait before reading x
+  if (!P.early) griddep_wait();
   if (warp == 0) {  // compact the live problems: work items cover only those
     int base = 0;
     for (int p0 = 0; p0 < P.np; p0 += 32) {
@@ -272,6 +279,7 @@ __global__ void __launch_bounds__(kThreads, 3) gemv_kernel(const Params P) {
     }
   } else {
     // -------------------------------------------------------------- compute
+    if (P.early) griddep_wait();  // x = the previous kernel's output
     int s = 0;
     uint32_t ph = 0;
     const int fg = warp * 16 + g;
@@ -472,6 +480,9 @@ static int run_gemv(const GemmArgs& a, const GemvWork& w, cudaStream_t st) {
     P.hb2 = (uint32_t)hb | ((uint32_t)hb << 16);
   }
   P.nitems = (int)(a.np * P.nft * P.nsplit);
+  // PDL on the second GEMV of a pair (kind 2, default on): early prologue
+  const bool pdl = pdl_enabled(a.second ? 2 : 4);
+  P.early = a.second && pdl ? 1 : 0;
   const size_t smem = gemv_smem(a.m, w.nsplit, BITS);
   static size_t attr = 0;
   if (smem > 48 * 1024 && smem > attr) {
@@ -485,14 +496,16 @@ static int run_gemv(const GemmArgs& a, const GemvWork& w, cudaStream_t st) {
   // grid for those -- at T = 1 a grid for all E problems launched ~3x more
   // CTAs than there were items, each paying the prologue
   const int64_t live = std::max<int64_t>(1, std::min<int64_t>(a.np, a.rows));
+  static const int per_sm = std::getenv("MOE_GEMV_CTAS") ? std::atoi(std::getenv("MOE_GEMV_CTAS")) : 3;
   const int64_t grid =
-      std::max<int64_t>(1, std::min<int64_t>(live * P.nft * P.nsplit, 3 * (int64_t)sm_count()));
+      std::max<int64_t>(1, std::min<int64_t>(live * P.nft * P.nsplit, per_sm * (int64_t)sm_count()));
   static long long* dtrace = nullptr;
   const bool tr = std::getenv("MOE_GEMV_TRACE") != nullptr;
   if (tr && !dtrace) MOE_CUDA_TRY(cudaMalloc(&dtrace, 8 * 8 * 4096));
   P.trace = tr ? dtrace : nullptr;
   if (tr) MOE_CUDA_TRY(cudaMemsetAsync(dtrace, 0, 8 * 8 * grid, st));
-  MOE_CUDA_TRY(launch_k(4, gv::gemv_kernel<BITS>, dim3((unsigned)grid), dim3(gv::kThreads), smem, st, P));
+  MOE_CUDA_TRY(launch_k(a.second ? 2 : 4, gv::gemv_kernel<BITS>, dim3((unsigned)grid),
+                        dim3(gv::kThreads), smem, st, P));
   note_launch();
   if (tr) {  // dev instrumentation: per-CTA phase times (ns)
     std::vector<long long> h(8 * grid);

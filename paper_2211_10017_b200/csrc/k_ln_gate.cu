@@ -175,13 +175,20 @@ __device__ __forceinline__ void logit_chunk(float2 (&acc)[RPT][EPG >= 2 ? EPG / 
 #pragma unroll
     for (int q = 0; q < KS; q += 2) {  // one input pair: 2 * EPG floats
       const float* wq = w0 + (q >> 1) * wstride;
+      if constexpr (EPG == 1) {
+        // expert e0 inside its expert pair: inputs q, q+1 are 2 floats apart
+        // (wg was shifted back by e0 & 1 by the caller)
+        o.w[q][0] = wq[0];
+        o.w[q + 1][0] = wq[2];
+      } else {
 #pragma unroll
-      for (int j = 0; j < EPG; j += 2) {  // experts e0+j, e0+j+1 x inputs q, q+1
-        const float4 w4 = *reinterpret_cast<const float4*>(wq + 2 * j);
-        o.w[q][j] = w4.x;
-        o.w[q][j + 1] = w4.y;
-        o.w[q + 1][j] = w4.z;
-        o.w[q + 1][j + 1] = w4.w;
+        for (int j = 0; j < EPG; j += 2) {  // experts e0+j, e0+j+1 x inputs q, q+1
+          const float4 w4 = *reinterpret_cast<const float4*>(wq + 2 * j);
+          o.w[q][j] = w4.x;
+          o.w[q][j + 1] = w4.y;
+          o.w[q + 1][j] = w4.z;
+          o.w[q + 1][j + 1] = w4.w;
+        }
       }
     }
   };
@@ -197,9 +204,15 @@ __device__ __forceinline__ void logit_chunk(float2 (&acc)[RPT][EPG >= 2 ? EPG / 
           const uint32_t hw = o.xh[i][q / 2];
           xq = h2f((uint16_t)((q & 1) ? (hw >> 16) : (hw & 0xFFFFu)));
         }
+        if constexpr (EPG == 1) {
+          // one chain per thread: plain FFMA (half the dependent latency of
+          // FFMA2 -- the latency-bound small-T configs)
+          acc[i][0].x = fmaf(xq, o.w[q][0], acc[i][0].x);
+        } else {
 #pragma unroll
-        for (int j = 0; j < NP; ++j)
-          acc[i][j] = g3::ffma2(xq, make_float2(o.w[q][2 * j], o.w[q][2 * j + 1]), acc[i][j]);
+          for (int j = 0; j < NP; ++j)
+            acc[i][j] = g3::ffma2(xq, make_float2(o.w[q][2 * j], o.w[q][2 * j + 1]), acc[i][j]);
+        }
       }
     }
   };
@@ -255,7 +268,12 @@ __global__ void __launch_bounds__(NT, 1) ln_gate_kernel(
       mbar_arrive_expect_tx(&bars[0], (uint32_t)nrow * d * 2);
     }
     __syncwarp();
-    // the gate weights never change: fetched before the previous kernel ends
+    // the rows first (the LN chains wait on them; the weights are needed only
+    // by the logit phase), one copy per lane; then the gate weights
+    griddep_wait();  // x and finished may be the previous kernel's output
+    for (int r = tid; r < nrow; r += 32)
+      bulk_load(xs + (size_t)r * xp, x + (r0 + r) * d, (uint32_t)d * 2, &bars[0]);
+    __syncwarp();
     for (int c = 0; c < C.ns; ++c) {
       const uint32_t bytes = (uint32_t)::min(C.kc, d - c * C.kc) * gwp * 4;
       if (elect_one()) {
@@ -263,9 +281,6 @@ __global__ void __launch_bounds__(NT, 1) ln_gate_kernel(
         bulk_load(sm + C.off_w + c * C.wslot, gw32 + (size_t)c * C.kc * gwp, bytes, &bars[1 + c]);
       }
     }
-    griddep_wait();  // x and finished may be the previous kernel's output
-    for (int r = 0; r < nrow; ++r)
-      if (elect_one()) bulk_load(xs + (size_t)r * xp, x + (r0 + r) * d, (uint32_t)d * 2, &bars[0]);
   } else {
     // the small operands every later phase reads, fetched while the rows
     // land (each would otherwise cost an L2 round trip on the critical path)
@@ -427,7 +442,9 @@ __global__ void __launch_bounds__(NT, 1) ln_gate_kernel(
       // weights blocked by (input pair, expert pair) (k_gate_fused.cu):
       // inputs 2j, 2j+1 of experts e0.. are the contiguous floats
       // [j * 2 * gwp + 2 * e0, ... + 2 * EPG)
-      const float* wg = reinterpret_cast<const float*>(sm + C.off_w + s * C.wslot) + 2 * e0;
+      // EPG = 1: an odd expert's floats start one before 2 * e0 in its pair
+      const float* wg = reinterpret_cast<const float*>(sm + C.off_w + s * C.wslot) + 2 * e0 -
+                        (EPG == 1 ? (e0 & 1) : 0);
       const int kn = ::min(C.kc, d - c * C.kc);  // multiple of 8
       if (C.wide)  // f32 copy of xn (written by the normalise pass)
         logit_chunk<EPG, RPT, KS, (EPG * RPT <= 2 ? 4 : 2), true>(
@@ -593,6 +610,9 @@ struct G3Pick {
 
 static bool g3_fits(int64_t d, int64_t E, int64_t gwp, int rb, int epg, int rpt, int nt, int k) {
   const g3::Cfg c = g3::cfg(d, E, gwp, rb, epg, rpt, nt);
+  // scalar chains only while they are few (latency-bound: C3 decode); with
+  // more chains FFMA2 pairs issue half the instructions (measured, C2)
+  if (epg == 1 && c.ntask > 128) return false;
   return c.ntask <= nt && c.total <= g3::kSmemMax && (int64_t)rb * k <= 1024;
 }
 
@@ -606,11 +626,15 @@ static bool g3_pick(int64_t T, int64_t d, int64_t E, int k, G3Pick* p) {
   const int64_t per_sm = (T + sms - 1) / sms;
   const int64_t waves = (per_sm + rbmax - 1) / rbmax;
   int rb = (int)std::max<int64_t>(1, (T + sms * waves - 1) / (sms * waves));
-  static const int kE[] = {2, 4, 8, 8};
-  static const int kR[] = {1, 1, 1, 2};
-  static const int kT[] = {256, 256, 256, 256};
+  // one expert chain per thread (scalar FFMA) when the chains fit: the
+  // small-T configs are bound by chain latency, and an FFMA2 chain step takes
+  // longer than an FFMA step; FFMA2 pairs when chains outnumber the threads
+  static const int kE[] = {1, 2, 4, 8, 8};
+  static const int kR[] = {1, 1, 1, 1, 2};
+  static const int kT[] = {256, 256, 256, 256, 256};
+  static const int first = std::getenv("MOE_GATE_NO_EPG1") ? 1 : 0;  // dev A/B
   for (;;) {
-    for (int i = 0; i < 4; ++i)
+    for (int i = first; i < 5; ++i)
       if (g3_fits(d, E, gwp, rb, kE[i], kR[i], kT[i], k)) {
         *p = G3Pick{rb, kE[i], kR[i], kT[i]};
         return true;
@@ -674,6 +698,7 @@ int launch_ln_gate(const GateFusedArgs& a, cudaStream_t st) {
   G3Pick p;
   if (!g3_pick(a.T, a.d, a.E, a.k, &p)) return set_error(MOE_EINVAL, "ln_gate: unsupported shape");
   if (p.rb != a.rows) return set_error(MOE_EINVAL, "ln_gate: row block mismatch");
+  if (p.epg == 1) return launch_g3<1, 1, 256>(a, p.rb, st);
   if (p.epg == 2) return launch_g3<2, 1, 256>(a, p.rb, st);
   if (p.epg == 4) return launch_g3<4, 1, 256>(a, p.rb, st);
   if (p.rpt == 1) return launch_g3<8, 1, 256>(a, p.rb, st);
