@@ -6,7 +6,8 @@
  * No torch types.  Status codes:
  *   MOE_OK 0, MOE_EINVAL 1 (argument / data validation; message mirrors the
  *   reference's std::invalid_argument text), MOE_ECUDA 2, MOE_ENCCL 3,
- *   MOE_ERANGE 4 (index out of range, reference std::out_of_range).
+ *   MOE_ERANGE 4 (index out of range, reference std::out_of_range),
+ *   MOE_EIO 5 (checkpoint file errors, reference std::runtime_error).
  * moe_cuda_last_error() returns the thread-local message of the last failure.
  *
  * Each entry point names the reference interface it replaces
@@ -38,6 +39,7 @@ extern "C" {
 #define MOE_ECUDA 2
 #define MOE_ENCCL 3
 #define MOE_ERANGE 4
+#define MOE_EIO 5 /* checkpoint file errors (reference std::runtime_error "checkpoint: ...") */
 
 #define MOE_MODE_EXACT 0
 #define MOE_MODE_FAST 1
@@ -309,6 +311,22 @@ int moe_layer_load_report(moe_layer* L, float capacity_factor, uint32_t* report,
 int moe_decode_run(moe_layer* const* layers, int n_layers, const uint16_t* x_steps,
                    const uint8_t* finished_steps, int steps, int64_t rows, int k, int mode,
                    int prune, uint16_t* out_steps, uint16_t* work, moe_stream_t stream);
+
+/* ---- .moec checkpoint -> device layers (new; csrc/moec.cu) ----
+ * Parses the reference checkpoint format (proj/src/checkpoint.cpp:35-446:
+ * magic, version, config, precision, FNV-1a checksum, every record in the
+ * reference's order, same "checkpoint: ..." messages, status MOE_EIO) and,
+ * if create_layers, builds one device layer per MoE block (enc.i.ffn /
+ * dec.i.ffn, i % moe_every == 0) straight from the file's int4 / int8 / fp16
+ * payloads -- no host dequantization; re-tiled on the device. */
+typedef struct moe_moec moe_moec;
+int moe_moec_load(const char* path, int create_layers, moe_moec** out);
+/* cfg9: d_model, d_ffn, n_enc_layers, n_dec_layers, n_experts, n_heads,
+ * vocab_size, moe_every, max_seq_len; precision 0 f16, 1 int8, 2 int4 */
+int moe_moec_info(const moe_moec* m, uint32_t* cfg9, int* precision, int* n_moe_blocks);
+/* i-th MoE block in file order: its layer (NULL unless created) and name */
+int moe_moec_block(const moe_moec* m, int i, moe_layer** layer, char* name, size_t name_len);
+int moe_moec_destroy(moe_moec* m);
 
 #ifdef __cplusplus
 }

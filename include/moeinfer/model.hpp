@@ -55,4 +55,20 @@ HalfMat moe_ffn_forward(const HalfMat& x, const MoeFfn& w, std::span<const uint8
 // quantize both expert tensors of a block (model.cpp:153-173, per block)
 MoeFfn quantize_moe_ffn(const MoeFfn& w, QuantBits bits, int threads = 1);
 
+// Model precision tag (model.hpp:52)
+enum class Precision : uint8_t { f16 = 0, int8 = 1, int4 = 2 };
+
+// The hot-path slice of moe::Model (model.hpp:97-112): its MoE blocks in
+// file order (encoder, then decoder) and the precision tag.
+struct MoeModel {
+  Precision precision = Precision::f16;
+  std::vector<MoeFfn> blocks;
+};
+
+// quantize_model (model.hpp:118, model.cpp:153-173): every MoE block's
+// expert tensors quantized (on the GPU, codes bit-identical to quantize()),
+// everything else -- biases included -- stays FP16; the source must be an
+// fp16 model.
+MoeModel quantize_model(const MoeModel& m, QuantBits bits, int threads = 1);
+
 }  // namespace moe

@@ -20,6 +20,9 @@
 //   moe_ffn_forward          proj/include/moeinfer/model.hpp:154-156
 //   ref::moe_per_token       proj/include/moeinfer/reference.hpp:62-63
 //   ref::quantize            proj/include/moeinfer/reference.hpp:41
+//   random_model / quantize_model / save_model / load_model
+//                            proj/include/moeinfer/model.hpp:114-118,
+//                            proj/include/moeinfer/checkpoint.hpp:41-42
 //
 // The one thing the reference lacks is top-k>1 gating.
 // ref_moe_ffn_forward_topk composes the reference's own primitives
@@ -37,6 +40,7 @@
 #include <string>
 #include <vector>
 
+#include "moeinfer/checkpoint.hpp"
 #include "moeinfer/dequant.hpp"
 #include "moeinfer/grouped_gemm.hpp"
 #include "moeinfer/model.hpp"
@@ -436,6 +440,40 @@ int ref_layer_forward_topk(void* h, const uint16_t* x, size_t T, size_t d,
       }
     }
     out_mat(o, out);
+  });
+}
+
+
+// Write a .moec checkpoint of random_model(cfg, seed), quantized to `bits`
+// (16 = FP16) by quantize_model -- the reference's own writer
+// (checkpoint.cpp:390-415), for the loader fixtures.
+int ref_make_moec(const char* path, const uint32_t* cfg9, int bits, uint64_t seed) {
+  return guarded([&] {
+    ModelConfig c;
+    uint32_t* f[] = {&c.d_model, &c.d_ffn, &c.n_enc_layers, &c.n_dec_layers, &c.n_experts,
+                     &c.n_heads, &c.vocab_size, &c.moe_every, &c.max_seq_len};
+    for (int i = 0; i < 9; ++i) *f[i] = cfg9[i];
+    Model m = random_model(c, seed);
+    if (bits != 16) m = quantize_model(m, bits == 8 ? QuantBits::b8 : QuantBits::b4, 1);
+    save_model(m, path);
+  });
+}
+
+// moe_ffn_forward of the i-th MoE block (file order: encoder, then decoder)
+// of a loaded .moec (load_model, checkpoint.cpp:419-483).
+int ref_moec_block_forward(const char* path, int block, const uint16_t* x, size_t T,
+                           const uint8_t* finished, uint16_t* out) {
+  return guarded([&] {
+    const Model m = load_model(path);
+    std::vector<const MoeFfn*> blocks;
+    for (const auto& l : m.encoder)
+      if (const auto* b = std::get_if<MoeFfn>(&l.ffn)) blocks.push_back(b);
+    for (const auto& l : m.decoder)
+      if (const auto* b = std::get_if<MoeFfn>(&l.ffn)) blocks.push_back(b);
+    if (block < 0 || block >= (int)blocks.size()) throw std::out_of_range("block");
+    const auto y = moe_ffn_forward(mat(x, T, m.config.d_model), *blocks[block],
+                                   std::span<const uint8_t>(finished, T), nullptr, 1);
+    out_mat(y, out);
   });
 }
 

@@ -12,7 +12,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libmoe_cuda.so")
 
-MOE_OK, MOE_EINVAL, MOE_ECUDA, MOE_ENCCL, MOE_ERANGE = 0, 1, 2, 3, 4
+MOE_OK, MOE_EINVAL, MOE_ECUDA, MOE_ENCCL, MOE_ERANGE, MOE_EIO = 0, 1, 2, 3, 4, 5
 MODE_EXACT, MODE_FAST, MODE_GEMV = 0, 1, 2
 
 _vp, _i64, _int, _u16, _sz = C.c_void_p, C.c_int64, C.c_int, C.c_uint16, C.c_size_t
@@ -73,6 +73,10 @@ _SIGS = {
     "moe_ep_forward": (_int, [_vp, _vp, _vp, _vp, _vp, _int, _int, _vp, _vp]),
     "moe_ep_counts": (_int, [_vp, _int, _vp, _vp, _vp]),
     "moe_ep_segments": (_int, [_int, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "moe_moec_load": (_int, [C.c_char_p, _int, _vp]),
+    "moe_moec_info": (_int, [_vp, _vp, _vp, _vp]),
+    "moe_moec_block": (_int, [_vp, _int, _vp, _vp, _sz]),
+    "moe_moec_destroy": (_int, [_vp]),
     "moe_decode_run": (_int, [_vp, _int, _vp, _vp, _int, _i64, _int, _int, _int, _vp, _vp, _vp]),
 }
 

@@ -378,6 +378,15 @@ MoeFfn quantize_moe_ffn(const MoeFfn& w, QuantBits bits, int threads) {
   return q;
 }
 
+MoeModel quantize_model(const MoeModel& m, QuantBits bits, int threads) {
+  require(m.precision == Precision::f16, "quantize_model: source must be an fp16 model");
+  MoeModel out;
+  out.precision = bits == QuantBits::b8 ? Precision::int8 : Precision::int4;
+  out.blocks.reserve(m.blocks.size());
+  for (const MoeFfn& b : m.blocks) out.blocks.push_back(quantize_moe_ffn(b, bits, threads));
+  return out;
+}
+
 // ---------------------------------------------------------------- device API
 namespace cuda {
 

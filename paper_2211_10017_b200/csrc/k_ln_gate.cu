@@ -626,13 +626,13 @@ static bool g3_pick(int64_t T, int64_t d, int64_t E, int k, G3Pick* p) {
   const int64_t per_sm = (T + sms - 1) / sms;
   const int64_t waves = (per_sm + rbmax - 1) / rbmax;
   int rb = (int)std::max<int64_t>(1, (T + sms * waves - 1) / (sms * waves));
-  // one expert chain per thread (scalar FFMA) when the chains fit: the
-  // small-T configs are bound by chain latency, and an FFMA2 chain step takes
-  // longer than an FFMA step; FFMA2 pairs when chains outnumber the threads
+  // EPG = 1 (one scalar-FFMA chain per thread) is kept for A/B only
+  // (MOE_GATE_EPG1=1): measured slower than FFMA2 pairs at C2 (7114 vs 5880
+  // cycles in the logit phase) and at C3 T = 1 (9399 vs 8006)
   static const int kE[] = {1, 2, 4, 8, 8};
   static const int kR[] = {1, 1, 1, 1, 2};
   static const int kT[] = {256, 256, 256, 256, 256};
-  static const int first = std::getenv("MOE_GATE_NO_EPG1") ? 1 : 0;  // dev A/B
+  static const int first = std::getenv("MOE_GATE_EPG1") ? 0 : 1;
   for (;;) {
     for (int i = first; i < 5; ++i)
       if (g3_fits(d, E, gwp, rb, kE[i], kR[i], kT[i], k)) {

@@ -156,11 +156,11 @@ int launch_gemm_exact(const GemmArgs& a, cudaStream_t st);
 // k_gemv.cu: decode-sized FAST path (mma.sync over the same weight tiles)
 constexpr int64_t kGemvMaxRows = 256;  // routed rows (T*k) up to which the layer uses it
 struct GemvWork {
-  float* part;       // split-K partials, nsplit * rows * n
-  uint32_t* ticket;  // E * ceil(n/128), zero-initialised, self-resetting
-  int nsplit;
+  float* part;          // partials of items split across CTAs: [piece][rows][n]
+  uint32_t* ticket;     // E * ceil(n/128), zero-initialised, self-resetting
+  int64_t part_floats;  // capacity of part (>= rows * n)
 };
-int gemv_splits(int64_t m, int64_t n, double active_experts);
+int64_t gemv_part_floats(int64_t m, int64_t n, int64_t rows);  // a good part size
 int launch_gemv(const GemmArgs& a, const GemvWork& w, cudaStream_t st);
 int launch_gemm_tc(const GemmArgs& a, cudaStream_t st);
 

@@ -1,0 +1,270 @@
+// moec.cu -- `.moec` checkpoint -> device MoE layers.
+//
+// Reads the reference's checkpoint format (proj/src/checkpoint.cpp:
+// Writer/Reader :35-240, record walk :242-300, header :390-446): magic
+// "MOEC", version 1, nine u32 config fields, precision tag, record count,
+// length-prefixed records {name u16+bytes, dtype u8 (0 f16, 1 u8, 2 u4),
+// layout u8 (0 dense, 1 interleaved), ndim u8, dims u64...; payload; for
+// quantized records a u64 scale count + fp16 scales}, FNV-1a-64 of
+// everything before the trailing checksum.  Every record is validated in
+// the reference's serialization order with the reference's messages
+// ("checkpoint: ..."); the records of each MoE block (enc.i.ffn /
+// dec.i.ffn with i % moe_every == 0) are handed to moe_layer_create
+// straight from the file image -- int4 / int8 payloads in the reference's
+// packing and fp16 scales go to the device as stored (no host dequant) and
+// are re-tiled on the device into the tcgen05/TMA weight layout.
+// Attention, dense-FFN, embedding and projection records are checked and
+// skipped (outside the hot path).
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "layer.cuh"
+
+namespace {
+
+constexpr uint32_t kVersion = 1;
+
+uint64_t fnv1a(const uint8_t* p, size_t n) {
+  uint64_t h = 0xcbf29ce484222325ull;
+  for (size_t i = 0; i < n; ++i) {
+    h ^= p[i];
+    h *= 0x100000001b3ull;
+  }
+  return h;
+}
+
+struct Fail {
+  std::string what;
+};
+
+struct Rd {
+  const std::vector<uint8_t>& in;
+  size_t pos = 0;
+  size_t end;
+  void need(size_t n) const {
+    if (pos + n > end) throw Fail{"truncated file"};
+  }
+  uint64_t uint(int bytes) {
+    need(bytes);
+    uint64_t v = 0;
+    for (int i = 0; i < bytes; ++i) v |= (uint64_t)in[pos++] << (8 * i);
+    return v;
+  }
+  const uint8_t* take(size_t n) {
+    need(n);
+    const uint8_t* p = in.data() + pos;
+    pos += n;
+    return p;
+  }
+  // one record header; returns a pointer to its payload
+  const uint8_t* record(const std::string& name, uint8_t dtype, uint8_t layout,
+                        std::initializer_list<uint64_t> dims, size_t payload) {
+    const uint64_t len = uint(2);
+    need(len);
+    const std::string got(reinterpret_cast<const char*>(in.data() + pos), len);
+    pos += len;
+    if (got != name) throw Fail{"unexpected record '" + got + "', wanted '" + name + "'"};
+    const uint8_t dt = (uint8_t)uint(1), ly = (uint8_t)uint(1);
+    if (dt != dtype || ly != layout) throw Fail{"record '" + name + "' has wrong dtype"};
+    if (uint(1) != dims.size()) throw Fail{"record rank mismatch"};
+    for (uint64_t w : dims)
+      if (uint(8) != w) throw Fail{"record shape mismatch"};
+    return take(payload);
+  }
+  const uint16_t* f16(const std::string& name, std::initializer_list<uint64_t> dims) {
+    uint64_t n = 1;
+    for (uint64_t v : dims) n *= v;
+    return reinterpret_cast<const uint16_t*>(record(name, 0, 0, dims, n * 2));
+  }
+};
+
+struct Cfg {
+  uint32_t d, f, nenc, ndec, E, heads, vocab, every, maxlen;
+};
+
+}  // namespace
+
+struct moe_moec {
+  Cfg cfg{};
+  int precision = 0;
+  std::vector<std::string> names;
+  std::vector<moe_layer*> layers;
+  ~moe_moec() {
+    for (moe_layer* L : layers) moe_layer_destroy(L);
+  }
+};
+
+using namespace moecu;
+
+namespace {
+
+// Walk the file in the reference's order (checkpoint.cpp:242-300); for each
+// MoE block fill a descriptor and (create) build its device layer.
+int walk(const std::vector<uint8_t>& bytes, moe_moec* M, bool create) {
+  try {
+    if (bytes.size() < 12) throw Fail{"truncated file"};
+    const size_t body = bytes.size() - 8;
+    uint64_t stored = 0;
+    for (int i = 0; i < 8; ++i) stored |= (uint64_t)bytes[body + i] << (8 * i);
+    if (stored != fnv1a(bytes.data(), body)) throw Fail{"checksum mismatch"};
+    Rd r{bytes, 0, body};
+    if (std::memcmp(r.take(4), "MOEC", 4) != 0) throw Fail{"bad magic"};
+    if (r.uint(4) != kVersion) throw Fail{"unsupported version"};
+    Cfg& c = M->cfg;
+    for (uint32_t* f : {&c.d, &c.f, &c.nenc, &c.ndec, &c.E, &c.heads, &c.vocab, &c.every, &c.maxlen})
+      *f = (uint32_t)r.uint(4);
+    // ModelConfig::validate (proj/src/model.cpp:15-27)
+    if (!(c.d > 0 && c.heads > 0 && c.d % c.heads == 0))
+      return set_error(MOE_EINVAL, "config: d_model must be a positive multiple of n_heads");
+    if (!(c.f > 0 && c.f % 8 == 0)) return set_error(MOE_EINVAL, "config: d_ffn must be a positive multiple of 8");
+    if (c.d % 8 != 0) return set_error(MOE_EINVAL, "config: d_model must be a multiple of 8");
+    if (!(c.nenc > 0 && c.ndec > 0)) return set_error(MOE_EINVAL, "config: need layers");
+    if (c.E == 0) return set_error(MOE_EINVAL, "config: need at least one expert");
+    if (c.vocab < 4) return set_error(MOE_EINVAL, "config: vocab must cover BOS, EOS and payload");
+    if (c.every < 1) return set_error(MOE_EINVAL, "config: moe_every must be >= 1");
+    if (c.maxlen < 2) return set_error(MOE_EINVAL, "config: max_seq_len too small");
+    const uint8_t prec = (uint8_t)r.uint(1);
+    if (prec > 2) throw Fail{"bad precision tag"};
+    M->precision = prec;
+    const uint32_t n_records = (uint32_t)r.uint(4);
+    const uint64_t d = c.d, f = c.f, E = c.E;
+    uint64_t count = 0;
+    auto attn = [&](const std::string& p) {
+      r.f16(p + ".ln_g", {d});
+      r.f16(p + ".ln_b", {d});
+      for (const char* w : {"q", "k", "v", "o"}) {
+        r.f16(p + ".w" + w, {d, d});
+        r.f16(p + ".b" + w, {d});
+      }
+      count += 10;
+    };
+    auto quant = [&](const std::string& name, uint64_t m, uint64_t n, const uint8_t** packed,
+                     const uint16_t** scales) {
+      const bool is4 = prec == 2;
+      *packed = r.record(name, is4 ? 2 : 1, is4 ? 1 : 0, {E, m, n}, is4 ? E * m * n / 2 : E * m * n);
+      if (r.uint(8) != E * n) throw Fail{"record '" + name + "' has wrong scale count"};
+      *scales = reinterpret_cast<const uint16_t*>(r.take(E * n * 2));
+    };
+    auto ffn = [&](const std::string& p, uint32_t idx) -> int {
+      if (idx % c.every != 0) {  // dense FFN block
+        r.f16(p + ".ln_g", {d});
+        r.f16(p + ".ln_b", {d});
+        r.f16(p + ".w1", {d, f});
+        r.f16(p + ".b1", {f});
+        r.f16(p + ".w2", {f, d});
+        r.f16(p + ".b2", {d});
+        count += 6;
+        return MOE_OK;
+      }
+      moe_layer_desc D{};
+      D.d = (int64_t)d;
+      D.f = (int64_t)f;
+      D.E = (int64_t)E;
+      D.bits = prec == 0 ? 16 : prec == 1 ? 8 : 4;
+      D.ln_g = r.f16(p + ".ln_g", {d});
+      D.ln_b = r.f16(p + ".ln_b", {d});
+      D.gate_w = r.f16(p + ".gate_w", {d, E});
+      D.gate_b = r.f16(p + ".gate_b", {E});
+      if (prec == 0) {
+        D.w1 = r.f16(p + ".w1", {E, d, f});
+        D.w2 = r.f16(p + ".w2", {E, f, d});
+      } else {
+        quant(p + ".w1", d, f, &D.q1, &D.s1);
+        quant(p + ".w2", f, d, &D.q2, &D.s2);
+      }
+      D.b1 = r.f16(p + ".b1", {E, f});
+      D.b2 = r.f16(p + ".b2", {E, d});
+      count += 8;
+      M->names.push_back(p);
+      if (create) {
+        moe_layer* L = nullptr;
+        const int st = moe_layer_create(&D, &L);
+        if (st != MOE_OK) return st;
+        M->layers.push_back(L);
+      }
+      return MOE_OK;
+    };
+    r.f16("tok_embed", {c.vocab, d});
+    r.f16("pos_embed", {c.maxlen, d});
+    count += 2;
+    for (uint32_t i = 0; i < c.nenc; ++i) {
+      const std::string p = "enc." + std::to_string(i);
+      attn(p + ".attn");
+      TRY(ffn(p + ".ffn", i));
+    }
+    for (uint32_t i = 0; i < c.ndec; ++i) {
+      const std::string p = "dec." + std::to_string(i);
+      attn(p + ".self");
+      attn(p + ".cross");
+      TRY(ffn(p + ".ffn", i));
+    }
+    for (const char* nm : {"enc_ln_g", "enc_ln_b", "dec_ln_g", "dec_ln_b"}) r.f16(nm, {d});
+    r.f16("out_w", {d, c.vocab});
+    r.f16("out_b", {c.vocab});
+    count += 6;
+    if (n_records != count) throw Fail{"record count mismatch"};
+    if (r.pos != body) throw Fail{"trailing bytes"};
+    return MOE_OK;
+  } catch (const Fail& e) {
+    return set_error(MOE_EIO, "checkpoint: %s", e.what.c_str());
+  }
+}
+
+int read_file(const char* path, std::vector<uint8_t>* out) {
+  FILE* fp = std::fopen(path, "rb");
+  if (!fp) return set_error(MOE_EIO, "checkpoint: cannot open '%s'", path);
+  std::fseek(fp, 0, SEEK_END);
+  const long n = std::ftell(fp);
+  std::fseek(fp, 0, SEEK_SET);
+  out->resize(n > 0 ? (size_t)n : 0);
+  const size_t got = n > 0 ? std::fread(out->data(), 1, (size_t)n, fp) : 0;
+  std::fclose(fp);
+  if ((long)got != n) return set_error(MOE_EIO, "checkpoint: read from '%s' failed", path);
+  return MOE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int moe_moec_load(const char* path, int create_layers, moe_moec** out) {
+  if (!path || !out) return set_error(MOE_EINVAL, "checkpoint: null argument");
+  std::vector<uint8_t> bytes;
+  TRY(read_file(path, &bytes));
+  auto M = std::make_unique<moe_moec>();
+  TRY(walk(bytes, M.get(), create_layers != 0));
+  *out = M.release();
+  return MOE_OK;
+}
+
+int moe_moec_info(const moe_moec* M, uint32_t* cfg9, int* precision, int* n_moe_blocks) {
+  if (!M) return set_error(MOE_EINVAL, "checkpoint: null");
+  if (cfg9) {
+    const Cfg& c = M->cfg;
+    const uint32_t v[9] = {c.d, c.f, c.nenc, c.ndec, c.E, c.heads, c.vocab, c.every, c.maxlen};
+    std::memcpy(cfg9, v, sizeof v);
+  }
+  if (precision) *precision = M->precision;
+  if (n_moe_blocks) *n_moe_blocks = (int)M->names.size();
+  return MOE_OK;
+}
+
+int moe_moec_block(const moe_moec* M, int i, moe_layer** layer, char* name, size_t name_len) {
+  if (!M || i < 0 || i >= (int)M->names.size())
+    return set_error(MOE_ERANGE, "checkpoint: MoE block index out of range");
+  if (layer) *layer = i < (int)M->layers.size() ? M->layers[i] : nullptr;
+  if (name && name_len) {
+    std::snprintf(name, name_len, "%s", M->names[i].c_str());
+  }
+  return MOE_OK;
+}
+
+int moe_moec_destroy(moe_moec* M) {
+  delete M;
+  return MOE_OK;
+}
+
+}  // extern "C"

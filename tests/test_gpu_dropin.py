@@ -133,3 +133,19 @@ def test_errors_map_like_the_reference(mi):
     qw = mi.quantize(np.ones((2, 4, 8), np.float16), bits=4)
     with pytest.raises(IndexError):
         qw.unpack_expert(5)
+
+
+def test_cpp_quantize_model(cuda, tmp_path):
+    """C++ drop-in quantize_model (reference model.hpp:118): built with g++
+    against libmoeinfer_b200.so and run (tests/native/dropin_quantize_model.cpp)."""
+    import os
+    import subprocess
+    from conftest import ROOT
+    pkg = os.path.join(ROOT, "paper_2211_10017_b200")
+    exe = str(tmp_path / "dq")
+    subprocess.run(["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"),
+                    "-I", "/usr/local/cuda/include", "-o", exe,
+                    os.path.join(ROOT, "tests", "native", "dropin_quantize_model.cpp"),
+                    "-L", pkg, "-lmoeinfer_b200", "-lmoe_cuda", f"-Wl,-rpath,{pkg}"], check=True)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
