@@ -51,11 +51,14 @@ int check_launch(const char* what) {
 // kernel's CTAs retire -- C2 -0.4 us, C4 -1 us, C3 decode -0.4 us.
 // MOE_PDL=1 (every layer kernel, each triggering its dependents at entry)
 // and 2 (both GEMMs) measured 1-5% slower: the parked dependent CTAs crowd
-// the SMs.  3: the second GEMM only; 0: plain stream order.
+// the SMs.  3: the second GEMM only; 5: 4 + the decode GEMVs; 6: 4 + the
+// gate kernel (kind 5: its weight fetch overlaps the previous layer's
+// tail); 0: plain stream order.
 bool pdl_enabled(int kind) {
   static const int mode = std::getenv("MOE_PDL") ? std::atoi(std::getenv("MOE_PDL")) : 4;
   return mode == 1 || (mode == 2 && (kind == 1 || kind == 2)) || (mode == 3 && kind == 2) ||
-         (mode == 4 && (kind == 2 || kind == 3)) || (mode == 5 && kind >= 2);
+         (mode == 4 && (kind == 2 || kind == 3)) || (mode == 5 && kind >= 2 && kind <= 4) ||
+         (mode == 6 && (kind == 2 || kind == 3 || kind == 5));
 }
 
 int sm_count() {
@@ -307,13 +310,13 @@ int moe_grouped_gemm(const uint16_t* x, int64_t rows, int64_t m, const uint32_t*
   if (mode == MOE_MODE_FAST) return launch_gemm_tc(a, S(stream));
   if (mode == MOE_MODE_GEMV) {
     // decode path with its own split-K workspace (the layer keeps a persistent one)
-    const int64_t pf = gemv_part_floats(m, n, rows);
+    const int ns = gemv_splits(m, n, (double)std::min<int64_t>(np, rows));
     DevBuf part, ticket;
     const int64_t nt = E * ((n + 127) / 128);
-    MOE_CUDA_TRY(cudaMallocAsync(&part.p, std::max<int64_t>(1, pf * 4), S(stream)));
+    MOE_CUDA_TRY(cudaMallocAsync(&part.p, std::max<int64_t>(1, (int64_t)ns * rows * n * 4), S(stream)));
     MOE_CUDA_TRY(cudaMallocAsync(&ticket.p, nt * 4, S(stream)));
     MOE_CUDA_TRY(cudaMemsetAsync(ticket.p, 0, nt * 4, S(stream)));
-    GemvWork w{static_cast<float*>(part.p), static_cast<uint32_t*>(ticket.p), pf};
+    GemvWork w{static_cast<float*>(part.p), static_cast<uint32_t*>(ticket.p), ns};
     const int rc = launch_gemv(a, w, S(stream));
     MOE_CUDA_TRY(cudaStreamSynchronize(S(stream)));
     return rc;
@@ -426,8 +429,8 @@ int moecu::layer_reserve(moe_layer* L, int64_t T, int k) {
   TRY(L->alloc(&L->dfin, cT));
   if (!L->gv_part) {
     const int64_t rmax = kGemvMaxRows;
-    L->gv_part_floats = gemv_part_floats(std::max(d, f), std::max(d, f), rmax);
-    TRY(L->alloc(&L->gv_part, L->gv_part_floats * 4));
+    const int64_t p1 = (int64_t)gemv_splits(d, f, 1.0) * f, p2 = (int64_t)gemv_splits(f, d, 1.0) * d;
+    TRY(L->alloc(&L->gv_part, rmax * std::max(p1, p2) * 4));
     const int64_t nt = E * ((std::max(d, f) + 127) / 128);
     TRY(L->alloc(&L->gv_ticket, nt * 4));
     MOE_CUDA_TRY(cudaMemset(L->gv_ticket, 0, nt * 4));
@@ -507,8 +510,9 @@ int moecu::layer_ffn(moe_layer* L, const uint16_t* xin, int64_t rows, const uint
   }
   if (mode == MOE_MODE_FAST && rows <= kGemvMaxRows) {
     // decode regime: stream the active experts' weights (K5)
-    GemvWork w1{L->gv_part, L->gv_ticket, L->gv_part_floats};
-    GemvWork w2{L->gv_part, L->gv_ticket, L->gv_part_floats};
+    const double act = (double)El * (1.0 - std::pow(1.0 - 1.0 / (double)El, (double)rows));
+    GemvWork w1{L->gv_part, L->gv_ticket, gemv_splits(d, f, act)};
+    GemvWork w2{L->gv_part, L->gv_ticket, gemv_splits(f, d, act)};
     TRY(launch_gemv(g1, w1, st));
     TRY(mark());
     TRY(launch_gemv(g2, w2, st));

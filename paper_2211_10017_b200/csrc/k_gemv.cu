@@ -107,17 +107,17 @@ struct Params {
   const uint16_t* bias;   // (E, n)
   const uint32_t* problems;
   uint16_t* out;          // (rows, n)
-  float* part;            // split-item partials [piece][rows][n]
-  int64_t part_cap;       // floats available in part
+  float* part;            // split-K partials [nsplit][rows][n]
   uint32_t* ticket;       // [E][nft] arrival counters (self-resetting)
   int64_t m, n, rows, nft, nkb;
-  int np, relu;
+  int np, nsplit, kbs_per_split, relu;
   uint32_t db2;           // debias constant in both halves
   uint32_t hb2;           // -(64 + debias - 1024) in both halves (i2f_u4_fast)
+  int nitems;             // np * nft * nsplit work items, strided over persistent CTAs
   int early;              // second GEMM of an FFN pair: problems and weights are read before
                           // the programmatic-dependent-launch wait (only x is the previous
                           // kernel's output)
-  long long* trace;       // dev-only (MOE_GEMV_TRACE): per CTA [start, prologue, passes, k-loop ns, x-stage ns, epi ns, end]
+  long long* trace;       // dev-only (MOE_GEMV_TRACE): per CTA [start, prologue, items, k-loop ns, x-stage ns, epi ns, end]
 };
 
 __device__ __forceinline__ long long gv_time() {
@@ -177,48 +177,31 @@ __device__ __forceinline__ void dequant_fast(const uint32_t (&w)[Frag<BITS>::NW]
   }
 }
 
-constexpr int KCH = 16;  // k-blocks of x staged at once (1024 inputs)
-
-// One CTA's unit range, segment by segment: units are (live problem, feature
-// tile, k-block), k-block fastest; a segment is the CTA's run of k-blocks of
-// one (problem, feature tile) item.
-struct Seg {
+struct Item {
   int64_t e, r0, r1;
-  int ft, kba, kbb;  // k-blocks [kba, kbb)
-  int npieces, piece;  // CTAs sharing this item, this CTA's index among them
+  int ft, split, kb0, kb1;
 };
 
-__device__ __forceinline__ int64_t owner_cta(int64_t unit, int64_t U, int ga) {
-  return ((unit + 1) * ga + U - 1) / U - 1;  // CTA whose range holds `unit`
+// item order: feature tile fastest, then k-split, then problem -- a CTA's
+// consecutive items share the expert rows it has staged
+__device__ __forceinline__ Item item_at(const Params& P, const int* live, int i) {
+  Item it;
+  it.ft = i % (int)P.nft;
+  it.split = (i / (int)P.nft) % P.nsplit;
+  const int p = live[i / (P.nsplit * (int)P.nft)];
+  it.e = P.problems[3 * p];
+  it.r0 = P.problems[3 * p + 1];
+  it.r1 = P.problems[3 * p + 2];
+  it.kb0 = it.split * P.kbs_per_split;
+  const int64_t hi = (int64_t)it.kb0 + P.kbs_per_split;
+  it.kb1 = (int)(P.nkb < hi ? P.nkb : hi);
+  return it;
 }
 
-__device__ __forceinline__ Seg seg_at(const Params& P, const int* live, int64_t u, int64_t q1,
-                                      int64_t U, int ga, int b) {
-  Seg g;
-  const int64_t j = u / P.nkb;
-  g.kba = (int)(u % P.nkb);
-  g.kbb = (int)(P.nkb < g.kba + (q1 - u) ? P.nkb : g.kba + (q1 - u));
-  g.ft = (int)(j % P.nft);
-  const int p = live[j / P.nft];
-  g.e = P.problems[3 * p];
-  g.r0 = P.problems[3 * p + 1];
-  g.r1 = P.problems[3 * p + 2];
-  const int64_t first = owner_cta(j * P.nkb, U, ga), last = owner_cta(j * P.nkb + P.nkb - 1, U, ga);
-  g.npieces = (int)(last - first + 1);
-  g.piece = (int)(b - first);
-  return g;
-}
-
-// Persistent, perfectly balanced: the live units (problem x feature tile x
-// k-block) are split into equal contiguous ranges, one per CTA, so no CTA
-// streams more than ceil(U / grid) weight blocks (item-granular schedules
-// left whole items on a few CTAs: a 2.004-items-per-CTA launch ran as long
-// as 3 items).  An item cut by range boundaries is reduced by the last of
-// its CTAs to arrive, in piece order (deterministic).  The producer warp
-// streams the weight blocks of the whole range back to back through the
-// ring; the compute warps stage each segment's live rows (the MMA's unused
-// B rows only feed discarded columns) and the next segment's problem fields
-// load during the current one.
+// Persistent: CTA b handles work items b, b + grid, ...  The producer warp
+// streams the weight blocks of all of them back to back through the ring
+// (it never drains between items); the compute warps stage only the live
+// rows of each item (the MMA's unused B rows only feed discarded columns).
 template <int BITS>
 __global__ void __launch_bounds__(kThreads, 3) gemv_kernel(const Params P) {
   using F = Frag<BITS>;
@@ -232,7 +215,7 @@ __global__ void __launch_bounds__(kThreads, 3) gemv_kernel(const Params P) {
   __shared__ int s_live[kMaxGemvProblems];  // non-empty problems, in order
   __shared__ int s_nlive;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  constexpr int kp = KCH * 64 + 8;  // row pitch of xs (conflict-free fragments)
+  const int kp = P.kbs_per_split * 64 + 8;  // row pitch of xs (conflict-free fragments)
   const long long t_start = P.trace ? gv_time() : 0;
   long long t_k = 0, t_x = 0, t_e = 0;
   int n_it = 0;
@@ -249,7 +232,7 @@ __global__ void __launch_bounds__(kThreads, 3) gemv_kernel(const Params P) {
   // FFN1 started), the weights never change -- the prologue and the weight
   // stream start while FFN1 retires; the compute warps wait before reading x
   if (!P.early) griddep_wait();
-  if (warp == 0) {  // compact the live problems: units cover only those
+  if (warp == 0) {  // compact the live problems: work items cover only those
     int base = 0;
     for (int p0 = 0; p0 < P.np; p0 += 32) {
       const int p = p0 + lane;
@@ -261,42 +244,41 @@ __global__ void __launch_bounds__(kThreads, 3) gemv_kernel(const Params P) {
     if (lane == 0) s_nlive = base;
   }
   __syncthreads();
-  const int64_t U = (int64_t)s_nlive * P.nft * P.nkb;
-  // active CTAs: all of them unless the split items' partials would not fit
-  // the workspace (pieces per item <= nkb / floor(U / ga) + 2)
-  int ga = (int)gridDim.x;
-  while (ga > 1 && (P.nkb / (U / ga > 1 ? U / ga : (int64_t)1) + 2) * P.rows * P.n > P.part_cap)
-    ga = ga * 3 / 4;
-  const int b = (int)blockIdx.x;
+  const int nitems = s_nlive * P.nsplit * (int)P.nft;
   const long long t_pro = P.trace ? gv_time() : 0;
-  if (U == 0 || b >= ga) return;
-  const int64_t q0 = U * b / ga, q1 = U * (b + 1) / ga;
 
   if (warp == kWarps) {
     // ------------------------------------------------------------- producer
     // converged warp, one elected lane issues: a lane-0-only loop makes
     // ptxas re-uniformise the copy operands per instruction (R2UR waterfall)
-    int s = 0;
-    uint32_t ph = 0;
-    int n = 0;
-    for (int64_t u = q0; u < q1;) {
-      const Seg sg = seg_at(P, s_live, u, q1, U, ga, b);
-      u += sg.kbb - sg.kba;
-      const uint8_t* wb = P.tiled + ((sg.e * P.nft + sg.ft) * P.nkb) * (int64_t)RG::WB;
-      const int npass = (int)((sg.r1 - sg.r0 + NT - 1) / NT);
-      for (int pass = 0; pass < npass; ++pass)
-        for (int kb = sg.kba; kb < sg.kbb; ++kb, ++n) {
-          if (n >= RG::NST) mbar_wait_warp(&empty[s], ph ^ 1u);
-          if (elect_one()) {
-            mbar_arrive_expect_tx(&full[s], RG::WB);
-            bulk_load(ring + s * RG::WB, wb + (int64_t)kb * RG::WB, RG::WB, &full[s]);
+    {
+      int s = 0;
+      uint32_t ph = 0;
+      int n = 0;
+      const int i0 = (int)((int64_t)blockIdx.x * nitems / gridDim.x);  // balanced blocks
+      const int i1 = (int)((int64_t)(blockIdx.x + 1) * nitems / gridDim.x);
+      // the next item's problem fields load while this item streams
+      Item nxt = i0 < i1 ? item_at(P, s_live, i0) : Item{};
+      for (int i = i0; i < i1; ++i) {
+        const Item it = nxt;
+        if (i + 1 < i1) nxt = item_at(P, s_live, i + 1);
+        if (it.r1 <= it.r0) continue;
+        const uint8_t* wb = P.tiled + ((it.e * P.nft + it.ft) * P.nkb) * (int64_t)RG::WB;
+        const int npass = (int)((it.r1 - it.r0 + NT - 1) / NT);
+        for (int pass = 0; pass < npass; ++pass)
+          for (int kb = it.kb0; kb < it.kb1; ++kb, ++n) {
+            if (n >= RG::NST) mbar_wait_warp(&empty[s], ph ^ 1u);
+            if (elect_one()) {
+              mbar_arrive_expect_tx(&full[s], RG::WB);
+              bulk_load(ring + s * RG::WB, wb + (int64_t)kb * RG::WB, RG::WB, &full[s]);
+            }
+            __syncwarp();
+            if (++s == RG::NST) {
+              s = 0;
+              ph ^= 1u;
+            }
           }
-          __syncwarp();
-          if (++s == RG::NST) {
-            s = 0;
-            ph ^= 1u;
-          }
-        }
+      }
     }
   } else {
     // -------------------------------------------------------------- compute
@@ -304,25 +286,50 @@ __global__ void __launch_bounds__(kThreads, 3) gemv_kernel(const Params P) {
     int s = 0;
     uint32_t ph = 0;
     const int fg = warp * 16 + g;
-    int64_t staged_r = -1;  // rows / k range staged in xs (-1: none)
-    int staged_kb = -1, staged_ke = -1;
-    Seg nxt = seg_at(P, s_live, q0, q1, U, ga, b);
-    for (int64_t u = q0; u < q1;) {
-      const Seg sg = nxt;
-      u += sg.kbb - sg.kba;
-      if (u < q1) nxt = seg_at(P, s_live, u, q1, U, ga, b);  // in flight during this segment
-      const int64_t feat0 = (int64_t)sg.ft * 128 + warp * 16;
+    const int i0 = (int)((int64_t)blockIdx.x * nitems / gridDim.x);
+    const int i1 = (int)((int64_t)(blockIdx.x + 1) * nitems / gridDim.x);
+    int64_t staged_r = -1;  // first row staged in xs (-1: none)
+    int staged_kb = -1;
+    // the next item's problem fields (global loads) are in flight during
+    // this item: item boundaries do not wait on them
+    Item nxt = i0 < i1 ? item_at(P, s_live, i0) : Item{};
+    for (int i = i0; i < i1; ++i) {
+      const Item it = nxt;
+      if (i + 1 < i1) nxt = item_at(P, s_live, i + 1);
+      if (it.r1 <= it.r0) continue;
+      const int64_t feat0 = (int64_t)it.ft * 128 + warp * 16;
       float sc[2] = {1.f, 1.f}, bi[2] = {0.f, 0.f};
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int64_t f = feat0 + g + 8 * h;
         if (f < P.n) {
-          if (P.scales) sc[h] = h2f(P.scales[sg.e * P.n + f]);
-          bi[h] = h2f(P.bias[sg.e * P.n + f]);
+          if (P.scales) sc[h] = h2f(P.scales[it.e * P.n + f]);
+          bi[h] = h2f(P.bias[it.e * P.n + f]);
         }
       }
-      for (int64_t rb = sg.r0; rb < sg.r1; rb += NT) {
-        const int nrow = (int)(sg.r1 - rb < (int64_t)NT ? sg.r1 - rb : (int64_t)NT);
+      const int nkbl = it.kb1 - it.kb0;
+      const int kq = nkbl * 8;  // 16-byte pieces per staged row
+      for (int64_t rb = it.r0; rb < it.r1; rb += NT) {
+        const int nrow = (int)(it.r1 - rb < (int64_t)NT ? it.r1 - rb : (int64_t)NT);
+        long long tt0 = P.trace ? gv_time() : 0;
+        if (rb != staged_r || it.kb0 != staged_kb) {  // same rows as the last item: reuse
+          named_bar_sync(1, kCompute);  // everyone done with xs
+          for (int q = threadIdx.x; q < nrow * kq; q += kCompute) {
+            const int r = q / kq, c = q % kq;
+            const int64_t k = (int64_t)it.kb0 * 64 + c * 8;
+            const bool ok = k < P.m;
+            cp_async16(xs + r * kp + c * 8, ok ? P.x + (rb + r) * P.m + k : P.x, ok);
+          }
+          cp_async_commit();
+          cp_async_wait<0>();
+          named_bar_sync(1, kCompute);
+          staged_r = rb;
+          staged_kb = it.kb0;
+        }
+
+        long long tt1 = P.trace ? gv_time() : 0;
+        t_x += tt1 - tt0;
+        ++n_it;
         float acc[2][2][4];
 #pragma unroll
         for (int j = 0; j < 2; ++j)
@@ -330,65 +337,44 @@ __global__ void __launch_bounds__(kThreads, 3) gemv_kernel(const Params P) {
           for (int c = 0; c < 2; ++c)
 #pragma unroll
             for (int q = 0; q < 4; ++q) acc[j][c][q] = 0.f;
-        for (int c0 = sg.kba; c0 < sg.kbb; c0 += KCH) {
-          const int ce = ::min(sg.kbb, c0 + KCH);
-          long long tt0 = P.trace ? gv_time() : 0;
-          if (rb != staged_r || c0 != staged_kb || ce != staged_ke) {  // same rows / k: reuse
-            const int kq = (ce - c0) * 8;  // 16-byte pieces per staged row
-            named_bar_sync(1, kCompute);  // everyone done with xs
-            for (int q = threadIdx.x; q < nrow * kq; q += kCompute) {
-              const int r = q / kq, c = q % kq;
-              const int64_t k = (int64_t)c0 * 64 + c * 8;
-              const bool ok = k < P.m;
-              cp_async16(xs + r * kp + c * 8, ok ? P.x + (rb + r) * P.m + k : P.x, ok);
+        const uint16_t* xk0 = xs + 16 * t + g * kp;
+        auto kloop = [&](auto ntile_c) {
+          constexpr int NTL = decltype(ntile_c)::value;
+          const uint16_t* xk = xk0;
+          for (int kbl = 0; kbl < nkbl; ++kbl, xk += 64) {
+            mbar_wait_warp(&full[s], ph);
+            uint32_t w[F::NW];
+            frag_from_smem<BITS>(ring + s * RG::WB, fg, t, w);
+            uint32_t lo[8], hi[8];
+            dequant_fast<BITS>(w, P.db2, P.hb2, lo, hi);
+#pragma unroll
+            for (int j = 0; j < NTL; ++j) {
+              const uint4 xa = *reinterpret_cast<const uint4*>(xk + j * 8 * kp);
+              const uint4 xb = *reinterpret_cast<const uint4*>(xk + j * 8 * kp + 8);
+              const uint32_t xv[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const uint32_t a[4] = {lo[2 * q], hi[2 * q], lo[2 * q + 1], hi[2 * q + 1]};
+                mma_16816(acc[j][q & 1], a, xv[2 * q], xv[2 * q + 1]);
+              }
             }
-            cp_async_commit();
-            cp_async_wait<0>();
-            named_bar_sync(1, kCompute);
-            staged_r = rb;
-            staged_kb = c0;
-            staged_ke = ce;
+            // the MMAs consumed every word loaded from the stage (in every
+            // lane): only now may the producer refill it
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+            if (++s == RG::NST) {
+              s = 0;
+              ph ^= 1u;
+            }
           }
-          long long tt1 = P.trace ? gv_time() : 0;
-          t_x += tt1 - tt0;
-          ++n_it;
-          const uint16_t* xk0 = xs + 16 * t + g * kp;
-          auto kloop = [&](auto ntile_c) {
-            constexpr int NTL = decltype(ntile_c)::value;
-            const uint16_t* xk = xk0;
-            for (int kbl = c0; kbl < ce; ++kbl, xk += 64) {
-              mbar_wait_warp(&full[s], ph);
-              uint32_t w[F::NW];
-              frag_from_smem<BITS>(ring + s * RG::WB, fg, t, w);
-              uint32_t lo[8], hi[8];
-              dequant_fast<BITS>(w, P.db2, P.hb2, lo, hi);
-#pragma unroll
-              for (int j = 0; j < NTL; ++j) {
-                const uint4 xa = *reinterpret_cast<const uint4*>(xk + j * 8 * kp);
-                const uint4 xb = *reinterpret_cast<const uint4*>(xk + j * 8 * kp + 8);
-                const uint32_t xv[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                  const uint32_t a[4] = {lo[2 * q], hi[2 * q], lo[2 * q + 1], hi[2 * q + 1]};
-                  mma_16816(acc[j][q & 1], a, xv[2 * q], xv[2 * q + 1]);
-                }
-              }
-              // the MMAs consumed every word loaded from the stage (in every
-              // lane): only now may the producer refill it
-              __syncwarp();
-              if (lane == 0) mbar_arrive(&empty[s]);
-              if (++s == RG::NST) {
-                s = 0;
-                ph ^= 1u;
-              }
-            }
-          };
-          if (nrow > 8)
-            kloop(std::integral_constant<int, 2>{});
-          else
-            kloop(std::integral_constant<int, 1>{});
-          if (P.trace) t_k += gv_time() - tt1;
-        }
+        };
+        if (nrow > 8)
+          kloop(std::integral_constant<int, 2>{});
+        else
+          kloop(std::integral_constant<int, 1>{});
+        long long tt2 = P.trace ? gv_time() : 0;
+        t_k += tt2 - tt1;
+        tt0 = tt2;
 #pragma unroll
         for (int j = 0; j < 2; ++j)
 #pragma unroll
@@ -401,42 +387,42 @@ __global__ void __launch_bounds__(kThreads, 3) gemv_kernel(const Params P) {
             const int tok = j * 8 + 2 * t + (q & 1), h = q >> 1;
             const int64_t f = feat0 + g + 8 * h;
             if (tok < nrow && f < P.n) {
-              if (sg.npieces == 1) {
+              if (P.nsplit == 1) {
                 float v = fmaf(acc[j][0][q], sc[h], bi[h]);
                 if (P.relu) v = v > 0.f ? v : 0.f;
                 P.out[(rb + tok) * P.n + f] = f2h(v);
               } else {
-                P.part[((int64_t)sg.piece * P.rows + rb + tok) * P.n + f] = acc[j][0][q];
+                P.part[((int64_t)it.split * P.rows + rb + tok) * P.n + f] = acc[j][0][q];
               }
             }
           }
       }
       const long long te0 = P.trace ? gv_time() : 0;
-      if (sg.npieces > 1) {
-        // the last of the item's CTAs reduces its pieces in order
+      if (P.nsplit > 1) {
+        // last CTA of this (expert, feature tile) reduces the splits in order
         __threadfence();
         named_bar_sync(1, kCompute);
         if (threadIdx.x == 0) {
-          const uint32_t prev = atomicAdd(&P.ticket[sg.e * P.nft + sg.ft], 1u);
-          s_last = prev == (uint32_t)sg.npieces - 1;
+          const uint32_t prev = atomicAdd(&P.ticket[it.e * P.nft + it.ft], 1u);
+          s_last = prev == (uint32_t)P.nsplit - 1;
         }
         named_bar_sync(1, kCompute);
         if (s_last) {
           __threadfence();
-          const int64_t nrows = sg.r1 - sg.r0;
-          const int64_t fbase = (int64_t)sg.ft * 128;
+          const int64_t nrows = it.r1 - it.r0;
+          const int64_t fbase = (int64_t)it.ft * 128;
           for (int64_t q = threadIdx.x; q < nrows * 128; q += kCompute) {
-            const int64_t r = sg.r0 + q / 128, f = fbase + q % 128;
+            const int64_t r = it.r0 + q / 128, f = fbase + q % 128;
             if (f >= P.n) continue;
             float a = 0.f;
-            for (int s2 = 0; s2 < sg.npieces; ++s2)
+            for (int s2 = 0; s2 < P.nsplit; ++s2)
               a += __ldcg(&P.part[((int64_t)s2 * P.rows + r) * P.n + f]);
-            float v = fmaf(a, P.scales ? h2f(P.scales[sg.e * P.n + f]) : 1.f,
-                           h2f(P.bias[sg.e * P.n + f]));
+            float v = fmaf(a, P.scales ? h2f(P.scales[it.e * P.n + f]) : 1.f,
+                           h2f(P.bias[it.e * P.n + f]));
             if (P.relu) v = v > 0.f ? v : 0.f;
             P.out[r * P.n + f] = f2h(v);
           }
-          if (threadIdx.x == 0) P.ticket[sg.e * P.nft + sg.ft] = 0;
+          if (threadIdx.x == 0) P.ticket[it.e * P.nft + it.ft] = 0;
         }
       }
       if (P.trace) t_e += gv_time() - te0;
@@ -455,11 +441,12 @@ __global__ void __launch_bounds__(kThreads, 3) gemv_kernel(const Params P) {
 }
 }  // namespace gv
 
-int64_t gemv_part_floats(int64_t m, int64_t n, int64_t rows) {
-  // room for ~8 pieces per item at full rows: the kernel lowers its active
-  // CTA count if an item would be cut into more
-  (void)m;
-  return 8 * std::max<int64_t>(rows, 1) * n;
+int gemv_splits(int64_t m, int64_t n, double active_experts) {
+  const int64_t nft = (n + 127) / 128, nkb = (m + 63) / 64;
+  int s = 1;
+  while (s < 16 && nkb / (2 * s) >= 4 && active_experts * nft * s < 2.0 * 148) s *= 2;
+  while (s < 64 && (nkb + s - 1) / s > 16) s *= 2;  // <= 1024 inputs staged per CTA
+  return s;
 }
 
 static size_t ring_bytes(int bits) {
@@ -467,8 +454,10 @@ static size_t ring_bytes(int bits) {
   return (size_t)nst * wblock_bytes(bits) + 2 * nst * 8;
 }
 
-static size_t gemv_smem(int bits) {
-  return ring_bytes(bits) + (size_t)gv::NT * (gv::KCH * 64 + 8) * 2;
+size_t gemv_smem(int64_t m, int nsplit, int bits) {
+  const int64_t nkb = (m + 63) / 64;
+  const int64_t kbs = (nkb + nsplit - 1) / nsplit;
+  return ring_bytes(bits) + (size_t)gv::NT * (kbs * 64 + 8) * 2;
 }
 
 template <int BITS>
@@ -481,7 +470,6 @@ static int run_gemv(const GemmArgs& a, const GemvWork& w, cudaStream_t st) {
   P.problems = a.problems;
   P.out = a.out;
   P.part = w.part;
-  P.part_cap = w.part_floats;
   P.ticket = w.ticket;
   P.m = a.m;
   P.n = a.n;
@@ -489,6 +477,8 @@ static int run_gemv(const GemmArgs& a, const GemvWork& w, cudaStream_t st) {
   P.nft = (a.n + 127) / 128;
   P.nkb = (a.m + 63) / 64;
   P.np = (int)a.np;
+  P.kbs_per_split = (int)((P.nkb + w.nsplit - 1) / w.nsplit);
+  P.nsplit = (int)((P.nkb + P.kbs_per_split - 1) / P.kbs_per_split);  // no empty splits
   P.relu = a.relu;
   P.db2 = (uint32_t)a.debias | ((uint32_t)a.debias << 16);
   {
@@ -496,42 +486,44 @@ static int run_gemv(const GemmArgs& a, const GemvWork& w, cudaStream_t st) {
     const uint16_t hb = (uint16_t)(0x8000 | (21 << 10) | (off << 4));  // -(64 + off)
     P.hb2 = (uint32_t)hb | ((uint32_t)hb << 16);
   }
-  // no programmatic dependent launch: an early-started second GEMV competes
-  // with the first one's tail for SM slots and HBM (C3 T=64: 86.7 us per
-  // layer against 82.3 without; MOE_PDL=5 opts in for A/B)
+  P.nitems = (int)(a.np * P.nft * P.nsplit);
+  // no programmatic dependent launch by default: an early-started second
+  // GEMV competes with the first one's tail for SM slots and HBM (C3 T=64:
+  // 86.7 us per layer with it, 82.3 without); MOE_PDL=5 opts in (early
+  // prologue: weights stream before the wait, only x waits)
   P.early = a.second && pdl_enabled(4) ? 1 : 0;
-  const size_t smem = gemv_smem(BITS);
+  const size_t smem = gemv_smem(a.m, w.nsplit, BITS);
   static size_t attr = 0;
   if (smem > 48 * 1024 && smem > attr) {
     MOE_CUDA_TRY(cudaFuncSetAttribute(gv::gemv_kernel<BITS>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = smem;
   }
-  // persistent, at most 3 CTAs per SM, >= 4 weight blocks per CTA for the
-  // most units the live problems can hold (min(np, rows) of them are live)
+  // persistent: enough CTAs for the live items (empty problems are skipped
+  // inside), at most 3 per SM
+  // at most min(np, rows) problems are live (each holds >= 1 row): size the
+  // grid for those -- at T = 1 a grid for all E problems launched ~3x more
+  // CTAs than there were items, each paying the prologue
   const int64_t live = std::max<int64_t>(1, std::min<int64_t>(a.np, a.rows));
   static const int per_sm = std::getenv("MOE_GEMV_CTAS") ? std::atoi(std::getenv("MOE_GEMV_CTAS")) : 3;
-  const int64_t grid = std::max<int64_t>(
-      1, std::min<int64_t>((live * P.nft * P.nkb + 3) / 4, per_sm * (int64_t)sm_count()));
+  const int64_t grid =
+      std::max<int64_t>(1, std::min<int64_t>(live * P.nft * P.nsplit, per_sm * (int64_t)sm_count()));
   static long long* dtrace = nullptr;
   const bool tr = std::getenv("MOE_GEMV_TRACE") != nullptr;
   if (tr && !dtrace) MOE_CUDA_TRY(cudaMalloc(&dtrace, 8 * 8 * 4096));
   P.trace = tr ? dtrace : nullptr;
   if (tr) MOE_CUDA_TRY(cudaMemsetAsync(dtrace, 0, 8 * 8 * grid, st));
-  MOE_CUDA_TRY(launch_k(4, gv::gemv_kernel<BITS>, dim3((unsigned)grid),
-                        dim3(gv::kThreads), smem, st, P));
+  MOE_CUDA_TRY(launch_k(4, gv::gemv_kernel<BITS>, dim3((unsigned)grid), dim3(gv::kThreads), smem,
+                        st, P));
   note_launch();
-  if (tr) {  // dev instrumentation: per-CTA phase times (ns) of the CTAs that ran
+  if (tr) {  // dev instrumentation: per-CTA phase times (ns)
     std::vector<long long> h(8 * grid);
     cudaStreamSynchronize(st);
     cudaMemcpy(h.data(), dtrace, h.size() * 8, cudaMemcpyDeviceToHost);
-    long long lo = -1, hi = 0;
+    long long lo = h[0], hi = h[6];
     double pro = 0, items = 0, tk = 0, tx = 0, te = 0, span = 0;
-    int64_t ran = 0;
     for (int64_t b = 0; b < grid; ++b) {
-      if (h[8 * b] == 0) continue;
-      ++ran;
-      lo = lo < 0 ? h[8 * b] : std::min(lo, h[8 * b]);
+      lo = std::min(lo, h[8 * b]);
       hi = std::max(hi, h[8 * b + 6]);
       pro += h[8 * b + 1];
       items += h[8 * b + 2];
@@ -540,12 +532,11 @@ static int run_gemv(const GemmArgs& a, const GemvWork& w, cudaStream_t st) {
       te += h[8 * b + 5];
       span += h[8 * b + 6] - h[8 * b];
     }
-    ran = std::max<int64_t>(ran, 1);
     std::fprintf(stderr,
-                 "gemv m=%lld n=%lld rows=%lld grid=%lld ran=%lld: kernel span %lld ns; per CTA mean: "
-                 "life %.0f ns, prologue %.0f, chunks %.2f, x-stage %.0f, k-loop %.0f, epilogue %.0f\n",
-                 (long long)a.m, (long long)a.n, (long long)a.rows, (long long)grid, (long long)ran,
-                 hi - lo, span / ran, pro / ran, items / ran, tx / ran, tk / ran, te / ran);
+                 "gemv m=%lld n=%lld rows=%lld nsplit=%d grid=%lld: kernel span %lld ns; per CTA mean: "
+                 "life %.0f ns, prologue %.0f, items %.2f, x-stage %.0f, k-loop %.0f, epilogue %.0f\n",
+                 (long long)a.m, (long long)a.n, (long long)a.rows, P.nsplit, (long long)grid,
+                 hi - lo, span / grid, pro / grid, items / grid, tx / grid, tk / grid, te / grid);
   }
   return check_launch("gemv");
 }
@@ -554,8 +545,10 @@ int launch_gemv(const GemmArgs& a, const GemvWork& w, cudaStream_t st) {
   if (a.np == 0 || a.rows == 0) return MOE_OK;
   if (a.np > gv::kMaxGemvProblems) return set_error(MOE_EINVAL, "gemv: at most 1024 problems");
   if (a.m % 8 != 0) return set_error(MOE_EINVAL, "gemv: m must be a multiple of 8");
-  if (w.part == nullptr || w.ticket == nullptr || w.part_floats < a.rows * a.n)
-    return set_error(MOE_EINVAL, "gemv: split workspace missing");
+  if (w.nsplit > 1 && (w.part == nullptr || w.ticket == nullptr))
+    return set_error(MOE_EINVAL, "gemv: split-K workspace missing");
+  if (gemv_smem(a.m, w.nsplit, a.bits) > 200 * 1024)
+    return set_error(MOE_EINVAL, "gemv: k range too long for one CTA (raise nsplit)");
   switch (a.bits) {
     case 4: return run_gemv<4>(a, w, st);
     case 8: return run_gemv<8>(a, w, st);

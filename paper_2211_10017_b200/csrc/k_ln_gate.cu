@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(NT, 1) ln_gate_kernel(
     const uint16_t* __restrict__ gb, int E, int k, const uint8_t* __restrict__ finished,
     uint16_t* __restrict__ xn, uint32_t* __restrict__ expert, uint16_t* __restrict__ scale,
     uint32_t* __restrict__ blockcnt, uint32_t* bad_row, int rb, uint16_t* __restrict__ out_fin,
-    long long* trace) {
+    long long* trace, int pdl) {
   extern __shared__ __align__(128) uint8_t sm[];
   const g3::Cfg C = g3::cfg(d, E, gwp, rb, EPG, RPT, NT);
   uint16_t* xs = reinterpret_cast<uint16_t*>(sm);
@@ -268,19 +268,24 @@ __global__ void __launch_bounds__(NT, 1) ln_gate_kernel(
       mbar_arrive_expect_tx(&bars[0], (uint32_t)nrow * d * 2);
     }
     __syncwarp();
-    // the rows first (the LN chains wait on them; the weights are needed only
-    // by the logit phase), one copy per lane; then the gate weights
+    auto weights = [&] {
+      for (int c = 0; c < C.ns; ++c) {
+        const uint32_t bytes = (uint32_t)::min(C.kc, d - c * C.kc) * gwp * 4;
+        if (elect_one()) {
+          mbar_arrive_expect_tx(&bars[1 + c], bytes);
+          bulk_load(sm + C.off_w + c * C.wslot, gw32 + (size_t)c * C.kc * gwp, bytes, &bars[1 + c]);
+        }
+      }
+    };
+    // launched early (PDL): the gate weights never change, fetch them while
+    // the previous kernel retires; otherwise the rows first (the LN chains
+    // wait on them; the weights are needed only by the logit phase)
+    if (pdl) weights();
     griddep_wait();  // x and finished may be the previous kernel's output
     for (int r = tid; r < nrow; r += 32)
       bulk_load(xs + (size_t)r * xp, x + (r0 + r) * d, (uint32_t)d * 2, &bars[0]);
     __syncwarp();
-    for (int c = 0; c < C.ns; ++c) {
-      const uint32_t bytes = (uint32_t)::min(C.kc, d - c * C.kc) * gwp * 4;
-      if (elect_one()) {
-        mbar_arrive_expect_tx(&bars[1 + c], bytes);
-        bulk_load(sm + C.off_w + c * C.wslot, gw32 + (size_t)c * C.kc * gwp, bytes, &bars[1 + c]);
-      }
-    }
+    if (!pdl) weights();
   } else {
     // the small operands every later phase reads, fetched while the rows
     // land (each would otherwise cost an L2 round trip on the critical path)
@@ -321,6 +326,7 @@ __global__ void __launch_bounds__(NT, 1) ln_gate_kernel(
       dst[1] = make_float4(h2f(h[4]), h2f(h[5]), h2f(h[6]), h2f(h[7]));
     }
     __syncthreads();
+    G3_TRACE(8);
     const int d4 = d / 4;
     if (tid < nrow) {  // sum chain: loads run three pieces ahead of the FADDs
       const float4* row = reinterpret_cast<const float4*>(xf + (size_t)tid * fp);
@@ -338,7 +344,9 @@ __global__ void __launch_bounds__(NT, 1) ln_gate_kernel(
       }
       st[tid] = __fdiv_rn(s, (float)d);
     }
+    if (tid == 0) G3_TRACE(9);
     __syncthreads();
+    G3_TRACE(10);
     for (int i = tid; i < nrow * d4; i += NT) {  // squared deviations, in place
       const int r = i / d4;
       float4* p = reinterpret_cast<float4*>(xf + (size_t)r * fp + (size_t)(i - r * d4) * 4);
@@ -350,6 +358,7 @@ __global__ void __launch_bounds__(NT, 1) ln_gate_kernel(
       *p = v;
     }
     __syncthreads();
+    G3_TRACE(11);
     if (tid < nrow) {
       const float4* row = reinterpret_cast<const float4*>(xf + (size_t)tid * fp);
       float v2 = 0.f;
@@ -668,10 +677,11 @@ static int launch_g3(const GateFusedArgs& a, int rb, cudaStream_t st) {
   static long long* dtrace = nullptr;
   const bool tr = std::getenv("MOE_GATE_TRACE") != nullptr;
   if (tr && !dtrace) MOE_CUDA_TRY(cudaMalloc(&dtrace, 8 * (16 + 2 * 65536)));
-  MOE_CUDA_TRY(launch_k(0, ln_gate_kernel<EPG, RPT, NT>, dim3(grid), dim3(NT), C.total, st, a.x, a.T,
+  const int pdl = pdl_enabled(5) ? 1 : 0;
+  MOE_CUDA_TRY(launch_k(5, ln_gate_kernel<EPG, RPT, NT>, dim3(grid), dim3(NT), C.total, st, a.x, a.T,
                         (int)a.d, a.g, a.b, a.gw32, (int)a.gwp, a.gb, (int)a.E, a.k, a.finished,
                         a.xn, a.expert, a.scale, a.blockcnt, a.bad_row, rb, a.out_fin,
-                        tr ? dtrace : nullptr));
+                        tr ? dtrace : nullptr, pdl));
   note_launch();
   if (tr && grid <= 65536) {
     std::vector<long long> h(16 + 2 * grid);
@@ -686,9 +696,10 @@ static int launch_g3(const GateFusedArgs& a, int rb, cudaStream_t st) {
     std::fprintf(stderr,
                  "ln_gate EPG=%d RPT=%d NT=%d grid=%u rb=%d kc=%d nch=%d tasks=%d wide=%d: "
                  "span=%lld ns cta mean=%lld ns; cta0 clocks rows=%lld chains=%lld norm=%lld "
-                 "logits=%lld tail=%lld\n",
+                 "logits=%lld tail=%lld [widen %lld, mean chain %lld, sync %lld, sqdev %lld, var chain+ %lld]\n",
                  EPG, RPT, NT, grid, rb, C.kc, C.nch, C.ntask, C.wide, hi - lo, sum / grid,
-                 h[1] - h[0], h[2] - h[1], h[3] - h[2], h[4] - h[3], h[5] - h[4]);
+                 h[1] - h[0], h[2] - h[1], h[3] - h[2], h[4] - h[3], h[5] - h[4],
+                 h[8] - h[1], h[9] - h[8], h[10] - h[9], h[11] - h[10], h[2] - h[11]);
   }
   return check_launch("ln_gate");
 }

@@ -29,8 +29,9 @@ int sm_count();
 // pair and the combine); the other modes are A/B switches (abi.cu
 // pdl_enabled).
 // kind 0: routing kernels, 1: the grouped GEMMs, 2: the second GEMM of an
-// FFN pair, 3: the combine, 4: the decode GEMVs (MOE_PDL=1: all, 2: GEMMs,
-// 3: the second GEMM, 4: the second GEMM and the combine, 5: 4 + GEMVs)
+// FFN pair, 3: the combine, 4: the decode GEMVs, 5: the fused gate (MOE_PDL=
+// 1: all, 2: GEMMs, 3: the second GEMM, 4: the second GEMM and the combine,
+// 5: 4 + GEMVs, 6: 4 + the gate)
 bool pdl_enabled(int kind = 0);
 template <typename... KArgs, typename... Args>
 cudaError_t launch_k(int pdl_kind, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
@@ -156,11 +157,11 @@ int launch_gemm_exact(const GemmArgs& a, cudaStream_t st);
 // k_gemv.cu: decode-sized FAST path (mma.sync over the same weight tiles)
 constexpr int64_t kGemvMaxRows = 256;  // routed rows (T*k) up to which the layer uses it
 struct GemvWork {
-  float* part;          // partials of items split across CTAs: [piece][rows][n]
-  uint32_t* ticket;     // E * ceil(n/128), zero-initialised, self-resetting
-  int64_t part_floats;  // capacity of part (>= rows * n)
+  float* part;       // split-K partials, nsplit * rows * n
+  uint32_t* ticket;  // E * ceil(n/128), zero-initialised, self-resetting
+  int nsplit;
 };
-int64_t gemv_part_floats(int64_t m, int64_t n, int64_t rows);  // a good part size
+int gemv_splits(int64_t m, int64_t n, double active_experts);
 int launch_gemv(const GemmArgs& a, const GemvWork& w, cudaStream_t st);
 int launch_gemm_tc(const GemmArgs& a, cudaStream_t st);
 

@@ -29,7 +29,6 @@ struct moe_layer {
   int64_t ep_cap = 0;
   // decode GEMV split-K workspace (routed rows <= kGemvMaxRows)
   float* gv_part = nullptr;
-  int64_t gv_part_floats = 0;
   uint32_t* gv_ticket = nullptr;
   // host-path staging
   uint16_t *dx = nullptr, *dout = nullptr;
