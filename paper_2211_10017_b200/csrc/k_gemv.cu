@@ -257,11 +257,8 @@ __global__ void __launch_bounds__(kThreads, 3) gemv_kernel(const Params P) {
       int n = 0;
       const int i0 = (int)((int64_t)blockIdx.x * nitems / gridDim.x);  // balanced blocks
       const int i1 = (int)((int64_t)(blockIdx.x + 1) * nitems / gridDim.x);
-      // the next item's problem fields load while this item streams
-      Item nxt = i0 < i1 ? item_at(P, s_live, i0) : Item{};
       for (int i = i0; i < i1; ++i) {
-        const Item it = nxt;
-        if (i + 1 < i1) nxt = item_at(P, s_live, i + 1);
+        const Item it = item_at(P, s_live, i);
         if (it.r1 <= it.r0) continue;
         const uint8_t* wb = P.tiled + ((it.e * P.nft + it.ft) * P.nkb) * (int64_t)RG::WB;
         const int npass = (int)((it.r1 - it.r0 + NT - 1) / NT);
@@ -290,12 +287,8 @@ __global__ void __launch_bounds__(kThreads, 3) gemv_kernel(const Params P) {
     const int i1 = (int)((int64_t)(blockIdx.x + 1) * nitems / gridDim.x);
     int64_t staged_r = -1;  // first row staged in xs (-1: none)
     int staged_kb = -1;
-    // the next item's problem fields (global loads) are in flight during
-    // this item: item boundaries do not wait on them
-    Item nxt = i0 < i1 ? item_at(P, s_live, i0) : Item{};
     for (int i = i0; i < i1; ++i) {
-      const Item it = nxt;
-      if (i + 1 < i1) nxt = item_at(P, s_live, i + 1);
+      const Item it = item_at(P, s_live, i);
       if (it.r1 <= it.r0) continue;
       const int64_t feat0 = (int64_t)it.ft * 128 + warp * 16;
       float sc[2] = {1.f, 1.f}, bi[2] = {0.f, 0.f};

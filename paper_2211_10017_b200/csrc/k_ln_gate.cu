@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(NT, 1) ln_gate_kernel(
     const uint16_t* __restrict__ gb, int E, int k, const uint8_t* __restrict__ finished,
     uint16_t* __restrict__ xn, uint32_t* __restrict__ expert, uint16_t* __restrict__ scale,
     uint32_t* __restrict__ blockcnt, uint32_t* bad_row, int rb, uint16_t* __restrict__ out_fin,
-    long long* trace, int pdl) {
+    long long* trace, int pdl, int ln_wide) {
   extern __shared__ __align__(128) uint8_t sm[];
   const g3::Cfg C = g3::cfg(d, E, gwp, rb, EPG, RPT, NT);
   uint16_t* xs = reinterpret_cast<uint16_t*>(sm);
@@ -315,8 +315,13 @@ __global__ void __launch_bounds__(NT, 1) ln_gate_kernel(
     }
   }
 
-  // ---- LayerNorm chains (model.cpp:178-192): one thread per row, serial RN
-  if (C.wide) {
+  // ---- LayerNorm chains (model.cpp:178-192): one thread per row, serial RN.
+  // Default: the chain threads convert the fp16 row inline (the conversion,
+  // dx and dx*dx sit off the dependent FADD chain); ln_wide (MOE_GATE_LN_WIDE=1,
+  // A/B): all threads first widen the rows to f32 and later write the
+  // squared deviations, so the chain threads issue only FADDs -- measured
+  // 1790 + 1975 cycles of extra passes at C2 for no faster chains.
+  if (C.wide && ln_wide) {
     for (int i = tid; i < nrow * d8; i += NT) {  // widen (exact)
       const int r = i / d8, c = i - r * d8;
       const uint4 v = *reinterpret_cast<const uint4*>(xs + (size_t)r * xp + c * 8);
@@ -376,28 +381,33 @@ __global__ void __launch_bounds__(NT, 1) ln_gate_kernel(
       st[rb + tid] = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(v2, (float)d), 1e-5f)));
     }
   } else if (tid < nrow) {
+    // 8 inputs per 16-byte load, two loads ahead of the FADDs
     const uint4* row = reinterpret_cast<const uint4*>(xs + (size_t)tid * xp);
     float s = 0.f;
-    uint4 cur = row[0];
+    uint4 c0 = row[0], c1 = row[d8 > 1 ? 1 : 0];
     for (int c = 0; c < d8; ++c) {
-      const uint4 nxt = row[c + 1 < d8 ? c + 1 : c];
+      const uint4 cur = c0;
+      c0 = c1;
+      c1 = row[c + 2 < d8 ? c + 2 : d8 - 1];
       const uint16_t* h = reinterpret_cast<const uint16_t*>(&cur);
 #pragma unroll
       for (int i = 0; i < 8; ++i) s = __fadd_rn(s, h2f(h[i]));
-      cur = nxt;
     }
     const float mean = __fdiv_rn(s, (float)d);
+    G3_TRACE(9);
     float v2 = 0.f;
-    cur = row[0];
+    c0 = row[0];
+    c1 = row[d8 > 1 ? 1 : 0];
     for (int c = 0; c < d8; ++c) {
-      const uint4 nxt = row[c + 1 < d8 ? c + 1 : c];
+      const uint4 cur = c0;
+      c0 = c1;
+      c1 = row[c + 2 < d8 ? c + 2 : d8 - 1];
       const uint16_t* h = reinterpret_cast<const uint16_t*>(&cur);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const float dx = __fsub_rn(h2f(h[i]), mean);
         v2 = __fadd_rn(v2, __fmul_rn(dx, dx));
       }
-      cur = nxt;
     }
     st[tid] = mean;
     st[rb + tid] = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(v2, (float)d), 1e-5f)));
@@ -678,10 +688,11 @@ static int launch_g3(const GateFusedArgs& a, int rb, cudaStream_t st) {
   const bool tr = std::getenv("MOE_GATE_TRACE") != nullptr;
   if (tr && !dtrace) MOE_CUDA_TRY(cudaMalloc(&dtrace, 8 * (16 + 2 * 65536)));
   const int pdl = pdl_enabled(5) ? 1 : 0;
+  static const int ln_wide = std::getenv("MOE_GATE_LN_WIDE") ? std::atoi(std::getenv("MOE_GATE_LN_WIDE")) : 0;
   MOE_CUDA_TRY(launch_k(5, ln_gate_kernel<EPG, RPT, NT>, dim3(grid), dim3(NT), C.total, st, a.x, a.T,
                         (int)a.d, a.g, a.b, a.gw32, (int)a.gwp, a.gb, (int)a.E, a.k, a.finished,
                         a.xn, a.expert, a.scale, a.blockcnt, a.bad_row, rb, a.out_fin,
-                        tr ? dtrace : nullptr, pdl));
+                        tr ? dtrace : nullptr, pdl, ln_wide));
   note_launch();
   if (tr && grid <= 65536) {
     std::vector<long long> h(16 + 2 * grid);
