@@ -637,7 +637,13 @@ def run_native(args, wl):
         alg = (f"active*(d*f + 4(f+d)) + S*(d+f)*4 = {wbytes:.4g} B per step over 2 launches "
                f"(active experts {active:.1f}, from the runs' own routing plans)")
     roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["traffic"] = load_traffic(args.workload)
+    tr = load_traffic(args.workload)
+    roof["traffic"] = tr["dram_bytes_per_step"] if tr else None
+    if tr:
+        # algorithmic bytes of the pair: active experts' int4 weights +
+        # scales / biases, FFN1 x in + h out, FFN2 h in + y out
+        roof["traffic_over_algorithmic"] = tr["dram_bytes_per_step"] / wbytes
+        roof["traffic_source"] = "profiles/ncu_traffic.json (ncu dram__bytes_read+write, FFN1+FFN2)"
     kname = ("gemv_kernel<4> (K5 FFN1 + FFN2, mma.sync over the tcgen05 weight tiles)"
              if S <= 256 else "gemm_tc_kernel<4,BN> (FFN1 + FFN2, tcgen05 kind::f16, TMEM acc)")
     roof.update({"kernel": kname,

@@ -56,7 +56,7 @@ constexpr int kMaxProblems = 1024;
 // TS = true: A (dequantised weights) in TMEM, 2 x BN accumulator columns
 // (BN <= 224).  TS = false: A in shared memory (SS MMA), which frees TMEM for
 // two 256-column accumulators -- chosen when 256-token tiles fit one wave.
-template <int BITS, int BN, bool TS, int CL = 1>
+template <int BITS, int BN, bool TS, int CL = 1, int NSX = 8>
 struct Cfg {
   static constexpr int WBYTES = wblock_bytes(BITS);
   static constexpr int BBYTES = BN / CL * 128;   // this CTA's BN / CL rows x 64 fp16
@@ -74,13 +74,18 @@ struct Cfg {
   static constexpr int NA = TS ? ((512 - NACC * BN) / 32 >= 4 ? 4 : 2) : 2;
   static constexpr int BUDGET = 220 * 1024 - EPI - NA * ABYTES;  // TMA stages
   static constexpr int NS0 = BUDGET / STAGE;
-  // TMA stages, an even count: with an odd count the two dequant groups
-  // (alternate k-blocks) share stages in alternating order, and fp16-weight
-  // layers (NS = 3 / 7) faulted or gave non-deterministic outputs under
-  // repeated route+FFN stress (scripts/stress_layer.py; root cause not yet
-  // isolated); every measured config keeps its stage count or loses one
-  // at most 8 (16 measured no faster for C5's 96-token pair tiles)
-  static constexpr int NS = NS0 > 8 ? 8 : (NS0 & ~1);
+  // TMA stages, an EVEN count (root cause of the round-1 fault at NS = 3 / 7,
+  // fp16 weights): the two dequant groups take alternate k-blocks, and
+  // stage s serves k-blocks it, it + NS, it + 2NS, ...  With NS odd those
+  // alternate between the groups, so each group waits on every SECOND phase
+  // of full[s]; an mbarrier parity wait only tells adjacent phases apart, so
+  // a group waiting for phase n + 2 returned as soon as phase n had
+  // completed (the barrier still in phase n + 1) and dequantised stale or
+  // not-yet-landed weights.  With NS even a group owns every phase of its
+  // stages.  (The A ring is even for the same reason.)
+  // at most NSX (default 8; 16 measured no faster for C5's 96-token pair
+  // tiles; MOE_TC_NS12=1 tries 12 on the multi-wave 192-token pair tiles)
+  static constexpr int NS = NS0 > NSX ? NSX : (NS0 & ~1);
   // [TMA stages][B | W] | [SS: A stages] | epilogue staging | barriers | table
   static constexpr int OFF_A = NS * STAGE;
   static constexpr int OFF_EPI = OFF_A + NA * ABYTES;
@@ -170,10 +175,10 @@ constexpr int kTraceN = 1024;  // events per role slot
 // the single-CTA kernel.  Barriers the MMA waits on live in
 // rank 0: `full` counts both halves' TMA bytes, `afull` / `tempty` take the
 // peer's dequant / epilogue arrivals remotely; commits multicast to both.
-template <int BITS, int BN, bool TS, int CL>
+template <int BITS, int BN, bool TS, int CL, int NSX = 8>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const Params P) {
-  using C = Cfg<BITS, BN, TS, CL>;
+  using C = Cfg<BITS, BN, TS, CL, NSX>;
   constexpr bool PAIR = CL == 2;
   const int rank = CL > 1 ? (int)cluster_ctarank() : 0;
   const uint32_t cid = blockIdx.x / CL, ncl = gridDim.x / CL;  // cluster id / count
@@ -552,9 +557,9 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-template <int BITS, int BN, bool TS, int CL = 1>
+template <int BITS, int BN, bool TS, int CL = 1, int NSX = 8>
 static int run_tc(const GemmArgs& a, cudaStream_t st) {
-  using C = tc::Cfg<BITS, BN, TS, CL>;
+  using C = tc::Cfg<BITS, BN, TS, CL, NSX>;
   auto encode = get_encode();
   if (!encode) return set_error(MOE_ECUDA, "cuTensorMapEncodeTiled unavailable");
   CUtensorMap tmap;
@@ -592,7 +597,7 @@ static int run_tc(const GemmArgs& a, cudaStream_t st) {
   }
   static bool attr_set = false;
   if (!attr_set) {
-    MOE_CUDA_TRY(cudaFuncSetAttribute(tc::gemm_tc_kernel<BITS, BN, TS, CL>,
+    MOE_CUDA_TRY(cudaFuncSetAttribute(tc::gemm_tc_kernel<BITS, BN, TS, CL, NSX>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr_set = true;
   }
@@ -618,12 +623,12 @@ static int run_tc(const GemmArgs& a, cudaStream_t st) {
     cfg.numAttrs = pdl_enabled(a.second ? 2 : 1) ? 2 : 1;
     if (trace_path) {
       int nc = 0;
-      cudaOccupancyMaxActiveClusters(&nc, tc::gemm_tc_kernel<BITS, BN, TS, CL>, &cfg);
+      cudaOccupancyMaxActiveClusters(&nc, tc::gemm_tc_kernel<BITS, BN, TS, CL, NSX>, &cfg);
       std::fprintf(stderr, "gemm_tc pair BN=%d TS=%d: max active clusters %d\n", BN, (int)TS, nc);
     }
-    MOE_CUDA_TRY(cudaLaunchKernelEx(&cfg, tc::gemm_tc_kernel<BITS, BN, TS, CL>, tmap, P));
+    MOE_CUDA_TRY(cudaLaunchKernelEx(&cfg, tc::gemm_tc_kernel<BITS, BN, TS, CL, NSX>, tmap, P));
   } else {
-    MOE_CUDA_TRY(launch_k(a.second ? 2 : 1, tc::gemm_tc_kernel<BITS, BN, TS, CL>, dim3(sm_count()), dim3(tc::kThreads),
+    MOE_CUDA_TRY(launch_k(a.second ? 2 : 1, tc::gemm_tc_kernel<BITS, BN, TS, CL, NSX>, dim3(sm_count()), dim3(tc::kThreads),
                           C::SMEM, st, tmap, P));
   }
   note_launch();
@@ -677,7 +682,10 @@ static int run_tc_bits(const GemmArgs& a, cudaStream_t st) {
       switch (bn) {
         case 128: return run_tc<BITS, 128, true, 2>(a, st);
         case 160: return run_tc<BITS, 160, true, 2>(a, st);
-        case 192: return run_tc<BITS, 192, true, 2>(a, st);
+        case 192: {
+          static const bool ns12 = std::getenv("MOE_TC_NS12") && std::atoi(std::getenv("MOE_TC_NS12"));
+          return ns12 ? run_tc<BITS, 192, true, 2, 12>(a, st) : run_tc<BITS, 192, true, 2>(a, st);
+        }
         case 224: return run_tc<BITS, 224, true, 2>(a, st);
         case 257: return run_tc<BITS, 256, true, 2>(a, st);
         default: return run_tc<BITS, 256, false, 2>(a, st);

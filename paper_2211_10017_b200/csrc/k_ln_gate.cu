@@ -316,11 +316,11 @@ __global__ void __launch_bounds__(NT, 1) ln_gate_kernel(
   }
 
   // ---- LayerNorm chains (model.cpp:178-192): one thread per row, serial RN.
-  // Default: the chain threads convert the fp16 row inline (the conversion,
-  // dx and dx*dx sit off the dependent FADD chain); ln_wide (MOE_GATE_LN_WIDE=1,
-  // A/B): all threads first widen the rows to f32 and later write the
-  // squared deviations, so the chain threads issue only FADDs -- measured
-  // 1790 + 1975 cycles of extra passes at C2 for no faster chains.
+  // ln_wide (few rows per CTA): all threads first widen the rows to f32 and
+  // later write the squared deviations, so the chain threads issue only
+  // FADDs; otherwise the chain threads convert the fp16 row inline (the
+  // conversion, dx and dx*dx sit off the dependent FADD chain) -- with 28
+  // rows per CTA (C2) the two extra passes cost 1790 + 1975 cycles.
   if (C.wide && ln_wide) {
     for (int i = tid; i < nrow * d8; i += NT) {  // widen (exact)
       const int r = i / d8, c = i - r * d8;
@@ -688,7 +688,11 @@ static int launch_g3(const GateFusedArgs& a, int rb, cudaStream_t st) {
   const bool tr = std::getenv("MOE_GATE_TRACE") != nullptr;
   if (tr && !dtrace) MOE_CUDA_TRY(cudaMalloc(&dtrace, 8 * (16 + 2 * 65536)));
   const int pdl = pdl_enabled(5) ? 1 : 0;
-  static const int ln_wide = std::getenv("MOE_GATE_LN_WIDE") ? std::atoi(std::getenv("MOE_GATE_LN_WIDE")) : 0;
+  // widened LN chains only for a few rows per CTA (decode: the passes are
+  // short and the FADD-only chain is faster -- C3 T=1 10710 vs 12869 cycles);
+  // many rows (C2: 28): inline conversion (6980 vs 9196 cycles)
+  static const int force_wide = std::getenv("MOE_GATE_LN_WIDE") ? std::atoi(std::getenv("MOE_GATE_LN_WIDE")) : -1;
+  const int ln_wide = force_wide >= 0 ? force_wide : (rb <= 8 ? 1 : 0);
   MOE_CUDA_TRY(launch_k(5, ln_gate_kernel<EPG, RPT, NT>, dim3(grid), dim3(NT), C.total, st, a.x, a.T,
                         (int)a.d, a.g, a.b, a.gw32, (int)a.gwp, a.gb, (int)a.E, a.k, a.finished,
                         a.xn, a.expert, a.scale, a.blockcnt, a.bad_row, rb, a.out_fin,
