@@ -83,8 +83,8 @@ struct Cfg {
   // completed (the barrier still in phase n + 1) and dequantised stale or
   // not-yet-landed weights.  With NS even a group owns every phase of its
   // stages.  (The A ring is even for the same reason.)
-  // at most NSX (default 8; 16 measured no faster for C5's 96-token pair
-  // tiles; MOE_TC_NS12=1 tries 12 on the multi-wave 192-token pair tiles)
+  // at most NSX = 8 (16 measured no faster for C5's 96-token pair tiles,
+  // 12 no faster for C2 / C4's 192-token pair tiles)
   static constexpr int NS = NS0 > NSX ? NSX : (NS0 & ~1);
   // [TMA stages][B | W] | [SS: A stages] | epilogue staging | barriers | table
   static constexpr int OFF_A = NS * STAGE;
@@ -682,10 +682,7 @@ static int run_tc_bits(const GemmArgs& a, cudaStream_t st) {
       switch (bn) {
         case 128: return run_tc<BITS, 128, true, 2>(a, st);
         case 160: return run_tc<BITS, 160, true, 2>(a, st);
-        case 192: {
-          static const bool ns12 = std::getenv("MOE_TC_NS12") && std::atoi(std::getenv("MOE_TC_NS12"));
-          return ns12 ? run_tc<BITS, 192, true, 2, 12>(a, st) : run_tc<BITS, 192, true, 2>(a, st);
-        }
+        case 192: return run_tc<BITS, 192, true, 2>(a, st);
         case 224: return run_tc<BITS, 224, true, 2>(a, st);
         case 257: return run_tc<BITS, 256, true, 2>(a, st);
         default: return run_tc<BITS, 256, false, 2>(a, st);

@@ -652,6 +652,14 @@ static bool g3_pick(int64_t T, int64_t d, int64_t E, int k, G3Pick* p) {
   static const int kR[] = {1, 1, 1, 1, 2};
   static const int kT[] = {256, 256, 256, 256, 256};
   static const int first = std::getenv("MOE_GATE_EPG1") ? 0 : 1;
+  // dev A/B: MOE_GATE_CFG="EPG,RPT" forces a chain layout when it fits
+  if (const char* f = std::getenv("MOE_GATE_CFG")) {
+    int fe = 0, fr = 0;
+    if (std::sscanf(f, "%d,%d", &fe, &fr) == 2 && g3_fits(d, E, gwp, rb, fe, fr, 256, k)) {
+      *p = G3Pick{rb, fe, fr, 256};
+      return true;
+    }
+  }
   for (;;) {
     for (int i = first; i < 5; ++i)
       if (g3_fits(d, E, gwp, rb, kE[i], kR[i], kT[i], k)) {
@@ -725,8 +733,8 @@ int launch_ln_gate(const GateFusedArgs& a, cudaStream_t st) {
   if (!g3_pick(a.T, a.d, a.E, a.k, &p)) return set_error(MOE_EINVAL, "ln_gate: unsupported shape");
   if (p.rb != a.rows) return set_error(MOE_EINVAL, "ln_gate: row block mismatch");
   if (p.epg == 1) return launch_g3<1, 1, 256>(a, p.rb, st);
-  if (p.epg == 2) return launch_g3<2, 1, 256>(a, p.rb, st);
-  if (p.epg == 4) return launch_g3<4, 1, 256>(a, p.rb, st);
+  if (p.epg == 2) return p.rpt == 1 ? launch_g3<2, 1, 256>(a, p.rb, st) : launch_g3<2, 2, 256>(a, p.rb, st);
+  if (p.epg == 4) return p.rpt == 1 ? launch_g3<4, 1, 256>(a, p.rb, st) : launch_g3<4, 2, 256>(a, p.rb, st);
   if (p.rpt == 1) return launch_g3<8, 1, 256>(a, p.rb, st);
   return launch_g3<8, 2, 256>(a, p.rb, st);
 }

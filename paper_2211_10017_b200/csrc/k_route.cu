@@ -319,16 +319,12 @@ __global__ void __launch_bounds__(1024) plan_place_fused_kernel(int spb,
       mbar_init(rbar, 1);
       fence_barrier_init();
       mbar_arrive_expect_tx(rbar, (uint32_t)(nslots_b * cols * 2));
-      int64_t q = (b * spb) / k;
-      int r = (int)((b * spb) % k);
-      for (int i = 0; i < nslots_b; ++i) {
-        bulk_load(rows_sm + (int64_t)i * cols, src + q * cols, (uint32_t)(cols * 2), rbar);
-        if (++r == k) {
-          r = 0;
-          ++q;
-        }
-      }
     }
+    __syncwarp();
+    // one copy per lane at a time (slot i holds source row (b*spb + i) / k)
+    for (int i = lane; i < nslots_b; i += 32)
+      bulk_load(rows_sm + (int64_t)i * cols, src + ((b * spb + i) / k) * cols,
+                (uint32_t)(cols * 2), rbar);
     __syncwarp();
   }
   // this thread's slot key, loaded up front (overlaps the histogram loads)
@@ -359,17 +355,25 @@ __global__ void __launch_bounds__(1024) plan_place_fused_kernel(int spb,
   }
   for (int64_t i = threadIdx.x; i < nwarp * keys; i += blockDim.x) wcnt[i] = 0;
   __syncthreads();
-  for (int64_t kk = threadIdx.x; kk < keys; kk += blockDim.x) {
+  // a warp per key: lanes take strided blocks, then a shuffle reduction
+  // (integer sums: order-free)
+  for (int64_t kk = warp; kk < keys; kk += nwarp) {
     const uint32_t* row = cnt + kk * cp;
     uint32_t t = 0, pre = 0;
-#pragma unroll 4
-    for (int bb = 0; bb < (int)nblk; ++bb) {
+    for (int bb = lane; bb < (int)nblk; bb += 32) {
       const uint32_t v = row[bb];
       t += v;
       pre += bb < b ? v : 0u;
     }
-    tot[kk] = t;
-    base[kk] = pre;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      t += __shfl_xor_sync(0xffffffffu, t, o);
+      pre += __shfl_xor_sync(0xffffffffu, pre, o);
+    }
+    if (lane == 0) {
+      tot[kk] = t;
+      base[kk] = pre;
+    }
   }
   __syncthreads();
   PL_TRACE(1);
@@ -631,20 +635,35 @@ __global__ void combine_kernel(const uint16_t* __restrict__ x, const uint16_t* _
     const int64_t r = i / chunks, c = i % chunks;
     uint4 acc = reinterpret_cast<const uint4*>(x + r * d)[c];
     if (finished == nullptr || finished[r] == 0) {
-      for (int s = 0; s < k; ++s) {
-        const uint32_t p = inv[r * k + s];
-        const uint32_t sc = scale[r * k + s];
-        const uint32_t s2 = sc | (sc << 16);
-        const uint4 yv = reinterpret_cast<const uint4*>(y + (int64_t)p * d)[c];
-        uint32_t* a = reinterpret_cast<uint32_t*>(&acc);
-        const uint32_t* b = reinterpret_cast<const uint32_t*>(&yv);
+      // slots in groups of up to 4: every index / scale load, then every y
+      // row load of the group in flight before the (slot-ordered) folds
+      for (int s0 = 0; s0 < k; s0 += 4) {
+        const int ns = k - s0 < 4 ? k - s0 : 4;
+        uint32_t p[4], sc[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          uint32_t prod, sum;
-          asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(prod) : "r"(b[q]), "r"(s2));
-          asm("add.rn.f16x2 %0, %1, %2;" : "=r"(sum) : "r"(a[q]), "r"(prod));
-          a[q] = sum;
-        }
+        for (int s = 0; s < 4; ++s)
+          if (s < ns) {
+            p[s] = inv[r * k + s0 + s];
+            sc[s] = scale[r * k + s0 + s];
+          }
+        uint4 yv[4];
+#pragma unroll
+        for (int s = 0; s < 4; ++s)
+          if (s < ns) yv[s] = reinterpret_cast<const uint4*>(y + (int64_t)p[s] * d)[c];
+#pragma unroll
+        for (int s = 0; s < 4; ++s)
+          if (s < ns) {
+            const uint32_t s2 = sc[s] | (sc[s] << 16);
+            uint32_t* a = reinterpret_cast<uint32_t*>(&acc);
+            const uint32_t* b = reinterpret_cast<const uint32_t*>(&yv[s]);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              uint32_t prod, sum;
+              asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(prod) : "r"(b[q]), "r"(s2));
+              asm("add.rn.f16x2 %0, %1, %2;" : "=r"(sum) : "r"(a[q]), "r"(prod));
+              a[q] = sum;
+            }
+          }
       }
     }
     reinterpret_cast<uint4*>(out + r * d)[c] = acc;
