@@ -26,6 +26,7 @@ _SIGS = {
     "moe_cuda_free": (_int, [_vp]),
     "moe_cuda_host_alloc": (_int, [_vp, _sz]),
     "moe_cuda_host_free": (_int, [_vp]),
+    "moe_cuda_host_alloc_wc": (_int, [_vp, _sz]),
     "moe_cuda_memcpy": (_int, [_vp, _vp, _sz, _int, _vp]),
     "moe_cuda_memset": (_int, [_vp, _int, _sz, _vp]),
     "moe_cuda_sync": (_int, [_vp]),

@@ -134,6 +134,10 @@ int moe_cuda_host_alloc(void** p, size_t bytes) {
   MOE_CUDA_TRY(cudaMallocHost(p, bytes ? bytes : 16));
   return MOE_OK;
 }
+int moe_cuda_host_alloc_wc(void** p, size_t bytes) {
+  MOE_CUDA_TRY(cudaHostAlloc(p, bytes ? bytes : 16, cudaHostAllocWriteCombined));
+  return MOE_OK;
+}
 int moe_cuda_host_free(void* p) {
   if (p) MOE_CUDA_TRY(cudaFreeHost(p));
   return MOE_OK;
@@ -715,13 +719,13 @@ int moe_layer_forward(moe_layer* L, const uint16_t* x, const uint8_t* finished, 
 // chunking never changes a result.  Chunked when the PCIe time exceeds the
 // compute estimate and each chunk still routes >= 96 rows per expert (the
 // tcgen05 pair tiles; C5's 64 rows per expert would fall to short tiles and
-// re-stream 2 GB of weights).  Measured (pinned PCIe on the B200 boxes:
-// H2D ~25 GB/s, D2H ~50 GB/s): C2 305 us / step with 2 chunks against 405
-// with one; 4 chunks measured slower than 2 (per-chunk launch and
-// copy-engine costs).
+// re-stream 2 GB of weights).  Measured with torch-pinned buffers (H2D
+// ~25 GB/s): C2 305 us / step with 2 chunks against 405 with one; 4 chunks
+// measured slower than 2 (per-chunk launch and copy-engine costs).  Bandwidths: write-combined pinned input ~40 GB/s,
+// pinned output ~50 GB/s (moe_cuda_host_alloc[_wc]).
 static int host_chunks(const moe_layer* L, int64_t T, int k) {
   if (T * k < 1024) return 1;  // decode-sized: one launch sequence
-  const double h2d = 25e9, d2h = 50e9, hbm = 6.5e12, tc = 0.45e15;
+  const double h2d = 40e9, d2h = 50e9, hbm = 6.5e12, tc = 0.45e15;
   const double io = (double)T * L->d * 2 * (1 / h2d + 1 / d2h);
   const double wb = (double)L->El * L->d * L->f * (L->bits == 16 ? 2.0 : L->bits == 8 ? 1.0 : 0.5);
   const double comp = 4.0 * T * k * L->d * L->f / tc + wb / hbm;

@@ -53,7 +53,7 @@ struct Cfg {
 // squared deviations) made by all threads, so the chain thread issues only
 // its dependent FADDs
 __host__ __device__ inline Cfg cfg1(int64_t d, int64_t E, int64_t gwp, int rb, int epg, int rpt,
-                                    int nt, bool whole) {
+                                    int nt, bool whole, int maxns = 3) {
   Cfg c;
   c.nt = nt;
   c.rb = rb;
@@ -63,13 +63,13 @@ __host__ __device__ inline Cfg cfg1(int64_t d, int64_t E, int64_t gwp, int rb, i
   c.nrg = (rb + rpt - 1) / rpt;
   c.ntask = c.ng * c.nrg;
   // the whole weight matrix when it fits (no per-chunk barriers), else
-  // 16 KB chunks through a 3-slot ring
+  // 16 KB chunks through a ring of up to maxns slots
   int kc = whole && (size_t)d * gwp * 4 <= kWBudget ? (int)d : (int)(16384 / (gwp * 4)) / 8 * 8;
   if (kc < 8) kc = 8;
   if (kc > d) kc = (int)d;  // d % 8 == 0
   c.kc = kc;
   c.nch = (int)((d + kc - 1) / kc);
-  c.ns = c.nch < 3 ? c.nch : 3;
+  c.ns = c.nch < maxns ? c.nch : maxns;
   c.xp = (int)d + 8;  // 16-byte row pitch, rows on distinct 16-byte bank groups
   // (rb + rpt) rows + slack: a thread's last row group and the operand
   // prefetch may read past the rows (never used)
@@ -90,13 +90,20 @@ __host__ __device__ inline Cfg cfg1(int64_t d, int64_t E, int64_t gwp, int rb, i
   c.off_tab = (c.off_bias + (size_t)E * 4 + 15) & ~size_t(15);
   c.off_fin = c.off_tab + 32 * 8;
   c.off_bar = (c.off_fin + rb + 15) & ~size_t(15);
-  c.total = c.off_bar + 8 * 4 + 16;
+  c.total = c.off_bar + (size_t)(1 + c.ns) * 8 + 16;  // rows barrier + one per slot
   return c;
 }
 __host__ __device__ inline Cfg cfg(int64_t d, int64_t E, int64_t gwp, int rb, int epg, int rpt,
                                    int nt) {
   const Cfg c = cfg1(d, E, gwp, rb, epg, rpt, nt, true);
-  return c.total <= kSmemMax ? c : cfg1(d, E, gwp, rb, epg, rpt, nt, false);
+  if (c.total <= kSmemMax) return c;
+  // chunked weights: the deepest ring that fits (each 16 KB chunk is an L2
+  // round trip; C4's 256 KB of f32 gate weights stream 16 chunks per CTA)
+  for (int ns = 8; ns > 3; --ns) {
+    const Cfg r = cfg1(d, E, gwp, rb, epg, rpt, nt, false, ns);
+    if (r.total <= kSmemMax) return r;
+  }
+  return cfg1(d, E, gwp, rb, epg, rpt, nt, false, 3);
 }
 
 // c += a * b on two lanes (FFMA2), each RN: exact products, k order per chain

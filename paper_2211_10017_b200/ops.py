@@ -335,3 +335,28 @@ class MoELayer:
                     active_experts=int(r[E + 5]),
                     imbalance=float(r[E + 1]) / (live / E) if live else 0.0,
                     capacity_factor=capacity_factor)
+
+
+class HostBuffer:
+    """Pinned host memory from the library (moe_cuda_host_alloc, or
+    write-combined moe_cuda_host_alloc_wc for streaming inputs the host only
+    writes) exposed as a numpy array; freed with the object."""
+
+    def __init__(self, shape, dtype, write_combined=False):
+        import numpy as np
+        dt = np.dtype(dtype)
+        n = int(np.prod(shape)) * dt.itemsize
+        p = C.c_void_p()
+        abi.call("moe_cuda_host_alloc_wc" if write_combined else "moe_cuda_host_alloc", C.byref(p), n)
+        self._p = p
+        buf = (C.c_uint8 * n).from_address(p.value)
+        self.array = np.frombuffer(buf, dtype=dt).reshape(shape)
+
+    def __del__(self):
+        p = getattr(self, "_p", None)
+        if p:
+            try:
+                abi.lib().moe_cuda_host_free(p)
+            except Exception:
+                pass
+            self._p = None

@@ -13,8 +13,12 @@ g = torch.Generator(device="cuda"); g.manual_seed(1)
 w1 = (torch.randn((E, d, f), generator=g, device="cuda") / d ** 0.5).half()
 w2 = (torch.randn((E, f, d), generator=g, device="cuda") / f ** 0.5).half()
 L = MoELayer(lw.ln_g, lw.ln_b, lw.gw, lw.gb, w1, np.zeros((E, f), np.float16), w2, np.zeros((E, d), np.float16), bits=4)
-xt = torch.randn((T, d)).half().pin_memory(); ot = torch.empty_like(xt).pin_memory()
-xh = xt.view(torch.int16).numpy().view(np.float16); oh = ot.view(torch.int16).numpy().view(np.float16)
+from paper_2211_10017_b200.ops import HostBuffer
+xb, ob = HostBuffer((T, d), np.float16, write_combined=True), HostBuffer((T, d), np.float16)
+xh, oh = xb.array, ob.array
+xh[...] = np.random.default_rng(0).standard_normal((T, d)).astype(np.float16)
+xt = torch.from_numpy(xh.view(np.int16)).view(torch.float16)
+ot = torch.from_numpy(oh.view(np.int16)).view(torch.float16)
 for _ in range(10): L.forward_host(xh, None, k=k, mode=1, out_host=oh)
 ts = []
 for _ in range(200):

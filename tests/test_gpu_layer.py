@@ -229,3 +229,25 @@ def test_layer_host_pinned_chunked_pipeline(cuda, oracle, k):
     xh[3500, 7] = np.inf
     with pytest.raises(ValueError, match="non-finite logit at row 3500"):
         L.forward_host(xh, fh, k=k, mode=1, out_host=oh)
+
+
+@pytest.mark.parametrize("cf", [1.0, 1.25])
+def test_layer_load_report(cuda, cf):
+    """moe_layer_load_report (expert-capacity bookkeeping, north_star item 1):
+    per-expert live loads from the last plan, capacity ceil(cf * live / E),
+    max load, experts / rows over capacity -- against numpy on the routing."""
+    import math
+    lw, x, fin = _case(128, 256, 16, 700, seed=31, fin_frac=0.2)
+    L = _layer(lw, 4)
+    L.forward(to_dev(x), to_dev(fin), k=2, mode=1)
+    rep = L.load_report(cf)
+    off = L.routing(700, 2)["offsets"].astype(np.int64)
+    load = np.diff(off[:17])
+    live = int(off[16] - off[0])
+    cap = math.ceil(cf * live / 16)
+    assert rep["load"].tolist() == load.tolist()
+    assert rep["live_slots"] == live == 2 * int((fin == 0).sum())
+    assert rep["capacity"] == cap and rep["max_load"] == load.max()
+    assert rep["experts_over"] == int((load > cap).sum())
+    assert rep["overflow_rows"] == int(np.maximum(load - cap, 0).sum())
+    assert rep["active_experts"] == int((load > 0).sum())
