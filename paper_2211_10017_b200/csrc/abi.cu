@@ -441,12 +441,14 @@ int moecu::layer_reserve(moe_layer* L, int64_t T, int k) {
   }
   if (!L->offsets) {
     uint32_t* small = nullptr;
-    TRY(L->alloc(&small, ((E + 1) + 3 * E + 4) * 4));
+    TRY(L->alloc(&small, ((E + 1) + 3 * E + 8) * 4));
+    MOE_CUDA_TRY(cudaMemset(small, 0, ((E + 1) + 3 * E + 8) * 4));
     L->offsets = small;
     L->problems = small + (E + 1);
     L->active = L->problems + 3 * E;
     L->bad_row = L->active + 1;
     L->bad_expert = L->active + 2;
+    L->gsync = L->active + 4;  // grid barrier of the fused gate + plan (2 words)
   }
   L->cap_T = cT;
   L->cap_S = cS;
@@ -474,13 +476,24 @@ int moecu::layer_route(moe_layer* L, const uint16_t* x, const uint8_t* fin, int6
     GateFusedArgs ga{x, T, d, L->ln_g, L->ln_b, L->gw32, L->gwp, L->gb, E, k, fin, L->xn,
                      L->expert, L->scale, L->blockcnt, L->bad_row, ln_gate_rows(T, d, E, k),
                      out_fin};
+    const bool fuse_plan = ln_gate_plan_fusable(T, d, E, k);
+    if (fuse_plan) {  // one wave of row blocks: the plan + gather run in the gate kernel
+      ga.perm = L->perm;
+      ga.inv = L->inv;
+      ga.offsets = L->offsets;
+      ga.problems = L->problems;
+      ga.active = L->active;
+      ga.xp = L->xp;
+      ga.gsync = L->gsync;
+    }
     TRY(launch_ln_gate(ga, st));
     TRY(mark());
     TRY(mark());
     TRY(mark());
-    TRY(launch_plan_from_counts(L->expert, fin, T, k, E, (int64_t)ga.rows * k, w, L->perm,
-                                L->inv, L->offsets, L->problems, L->active, L->xn, d, L->xp,
-                                st));
+    if (!fuse_plan)
+      TRY(launch_plan_from_counts(L->expert, fin, T, k, E, (int64_t)ga.rows * k, w, L->perm,
+                                  L->inv, L->offsets, L->problems, L->active, L->xn, d, L->xp,
+                                  st));
   } else {
     TRY(launch_layer_norm(x, T, d, L->ln_g, L->ln_b, L->xn, st));
     TRY(mark());
