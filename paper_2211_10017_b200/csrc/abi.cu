@@ -448,7 +448,6 @@ int moecu::layer_reserve(moe_layer* L, int64_t T, int k) {
     L->active = L->problems + 3 * E;
     L->bad_row = L->active + 1;
     L->bad_expert = L->active + 2;
-    L->gsync = L->active + 4;  // grid barrier of the fused gate + plan (2 words)
   }
   L->cap_T = cT;
   L->cap_S = cS;
@@ -458,7 +457,8 @@ int moecu::layer_reserve(moe_layer* L, int64_t T, int k) {
 // LN -> gate -> top-k -> plan -> gather into L->xp (stages 0..3)
 // the one-kernel gate path applies (and with it the fused k = 1 combine)
 static bool fused_gate_ok(const moe_layer* L, const uint16_t* x, int64_t T, int k) {
-  return (reinterpret_cast<uintptr_t>(x) & 15) == 0 && L->gw32 != nullptr &&
+  static const bool off = std::getenv("MOE_GATE_UNFUSED") != nullptr;  // dev A/B
+  return !off && (reinterpret_cast<uintptr_t>(x) & 15) == 0 && L->gw32 != nullptr &&
          ln_gate_supported(T, L->d, L->E, k);
 }
 
@@ -476,24 +476,12 @@ int moecu::layer_route(moe_layer* L, const uint16_t* x, const uint8_t* fin, int6
     GateFusedArgs ga{x, T, d, L->ln_g, L->ln_b, L->gw32, L->gwp, L->gb, E, k, fin, L->xn,
                      L->expert, L->scale, L->blockcnt, L->bad_row, ln_gate_rows(T, d, E, k),
                      out_fin};
-    const bool fuse_plan = ln_gate_plan_fusable(T, d, E, k);
-    if (fuse_plan) {  // one wave of row blocks: the plan + gather run in the gate kernel
-      ga.perm = L->perm;
-      ga.inv = L->inv;
-      ga.offsets = L->offsets;
-      ga.problems = L->problems;
-      ga.active = L->active;
-      ga.xp = L->xp;
-      ga.gsync = L->gsync;
-    }
     TRY(launch_ln_gate(ga, st));
     TRY(mark());
     TRY(mark());
     TRY(mark());
-    if (!fuse_plan)
-      TRY(launch_plan_from_counts(L->expert, fin, T, k, E, (int64_t)ga.rows * k, w, L->perm,
-                                  L->inv, L->offsets, L->problems, L->active, L->xn, d, L->xp,
-                                  st));
+    TRY(launch_plan_from_counts(L->expert, fin, T, k, E, (int64_t)ga.rows * k, w, L->perm,
+                                L->inv, L->offsets, L->problems, L->active, L->xn, d, L->xp, st));
   } else {
     TRY(launch_layer_norm(x, T, d, L->ln_g, L->ln_b, L->xn, st));
     TRY(mark());

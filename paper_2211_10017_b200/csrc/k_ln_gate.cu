@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(NT, 1) ln_gate_kernel(
     const uint16_t* __restrict__ gb, int E, int k, const uint8_t* __restrict__ finished,
     uint16_t* __restrict__ xn, uint32_t* __restrict__ expert, uint16_t* __restrict__ scale,
     uint32_t* __restrict__ blockcnt, uint32_t* bad_row, int rb, uint16_t* __restrict__ out_fin,
-    long long* trace, int pdl, int ln_wide, const GateFusedArgs fa, int pad_off) {
+    long long* trace, int pdl, int ln_wide) {
   extern __shared__ __align__(128) uint8_t sm[];
   const g3::Cfg C = g3::cfg(d, E, gwp, rb, EPG, RPT, NT);
   uint16_t* xs = reinterpret_cast<uint16_t*>(sm);
@@ -453,14 +453,8 @@ __global__ void __launch_bounds__(NT, 1) ln_gate_kernel(
   // latency leaves room for a three-step-deep prefetch ring.
   constexpr int NP = EPG >= 2 ? EPG / 2 : 1;
   constexpr int KS = EPG * RPT <= 4 ? 8 : 4;
-  // row groups padded to a multiple of 32 when the expert groups still fit
-  // the block: every warp then holds ONE expert group, so its gate-weight
-  // loads are shared-memory broadcasts (one wavefront) instead of one per
-  // expert group a warp straddles
-  const int nrgp = (C.nrg + 31) / 32 * 32;
-  const int nrgm = C.ng * nrgp <= NT && !pad_off ? nrgp : C.nrg;
-  const int rg = tid % nrgm, eg = tid / nrgm, e0 = eg * EPG;
-  const bool active = rg < C.nrg && eg < C.ng;
+  const int rg = tid % C.nrg, eg = tid / C.nrg, e0 = eg * EPG;
+  const bool active = tid < C.ntask;
   float2 acc[RPT][NP];
 #pragma unroll
   for (int i = 0; i < RPT; ++i)
@@ -629,117 +623,6 @@ __global__ void __launch_bounds__(NT, 1) ln_gate_kernel(
   }
   __syncthreads();
   for (int i = tid; i <= E; i += NT) blockcnt[(int64_t)i * gridDim.x + blockIdx.x] = hist[i];
-  if (fa.perm != nullptr) {
-    // ---- fused routing plan (build_routing_plan, routing.cpp:43-87): a
-    // stable counting sort of the slots r*k + s by key (finished ? E :
-    // expert), every CTA resident (cooperative launch, one wave).
-    // 1. grid barrier, self-resetting: (arrival count, generation)
-    __syncthreads();
-    if (tid == 0) {
-      uint32_t g0;
-      asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(g0) : "l"(fa.gsync + 1) : "memory");
-      __threadfence();
-      if (atomicAdd(fa.gsync, 1u) == gridDim.x - 1) {
-        fa.gsync[0] = 0;
-        __threadfence();
-        atomicAdd(fa.gsync + 1, 1u);
-      } else {
-        uint32_t g;
-        do {
-          asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(g) : "l"(fa.gsync + 1) : "memory");
-        } while (g == g0);
-      }
-      __threadfence();
-    }
-    __syncthreads();
-    // 2. the whole (key x block) histogram -> key totals, this block's bases
-    const int keys = E + 1, nb = (int)gridDim.x, cp = nb + 1;
-    const int nw = NT / 32, warp = tid >> 5, lane = tid & 31;
-    uint32_t* H = reinterpret_cast<uint32_t*>(sm + C.off_w);  // [keys][nb + 1]
-    uint32_t* tot = H + keys * cp;                              // [keys + 1]
-    uint32_t* base = tot + keys + 1;                            // [keys]
-    uint32_t* wcnt = base + keys;                               // [nw][keys]
-    uint32_t* posl = wcnt + nw * keys;                          // [NT]
-    for (int i = tid; i < keys * nb; i += NT) {
-      const int kk = i / nb;
-      H[kk * cp + (i - kk * nb)] = __ldcg(blockcnt + i);
-    }
-    for (int i = tid; i < nw * keys; i += NT) wcnt[i] = 0;
-    __syncthreads();
-    for (int kk = warp; kk < keys; kk += nw) {
-      uint32_t t = 0, pre = 0;
-      for (int bb = lane; bb < nb; bb += 32) {
-        const uint32_t v = H[kk * cp + bb];
-        t += v;
-        pre += bb < (int)blockIdx.x ? v : 0u;
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        t += __shfl_xor_sync(0xffffffffu, t, o);
-        pre += __shfl_xor_sync(0xffffffffu, pre, o);
-      }
-      if (lane == 0) {
-        tot[kk] = t;
-        base[kk] = pre;
-      }
-    }
-    __syncthreads();
-    if (warp == 0) {  // exclusive scan of the key totals
-      uint32_t carry = 0;
-      for (int k0 = 0; k0 < keys; k0 += 32) {
-        const int key = k0 + lane;
-        const uint32_t v = key < keys ? tot[key] : 0u;
-        uint32_t in = v;
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t u = __shfl_up_sync(0xffffffffu, in, o);
-          if (lane >= o) in += u;
-        }
-        if (key < keys) {
-          tot[key] = carry + in - v;
-          base[key] += carry + in - v;
-        }
-        carry += __shfl_sync(0xffffffffu, in, 31);
-      }
-    }
-    __syncthreads();
-    if (blockIdx.x == 0) {
-      for (int key = tid; key < keys; key += NT) fa.offsets[key] = tot[key];
-      for (int e = tid; e < E; e += NT) {
-        fa.problems[3 * e] = (uint32_t)e;
-        fa.problems[3 * e + 1] = tot[e];
-        fa.problems[3 * e + 2] = tot[e + 1];
-      }
-      if (tid == 0) *fa.active = tot[E];
-    }
-    // 3. place this block's slots: rank among equal keys in slot order
-    const int nsl = nrow * k;
-    const bool live = tid < nsl;
-    uint32_t key = 0xFFFFFFFFu;
-    if (live) {
-      const int r = tid / k, s2 = tid - r * k;
-      key = fsm[r] != 0 ? (uint32_t)E : (sel[r * 8] == 0xFFFFFFFFu ? 0u : sel[r * 8 + s2]);
-    }
-    const uint32_t peers = __match_any_sync(0xffffffffu, key);
-    const uint32_t rank_w = __popc(peers & ((1u << lane) - 1u));
-    if (live && (peers >> lane) == 1u) wcnt[warp * keys + key] = __popc(peers);
-    __syncthreads();
-    if (live) {
-      uint32_t before = 0;
-      for (int w = 0; w < warp; ++w) before += wcnt[w * keys + key];
-      const uint32_t pos = base[key] + before + rank_w;
-      const int64_t slot = r0 * k + tid;
-      fa.perm[pos] = (uint32_t)slot;
-      fa.inv[slot] = pos;
-      posl[tid] = pos;
-    }
-    __syncthreads();
-    // 4. gather: the normalised rows are still in shared memory
-    for (int i = warp; i < nsl; i += nw) {
-      const uint4* a = reinterpret_cast<const uint4*>(xs + (size_t)(i / k) * xp);
-      uint4* b = reinterpret_cast<uint4*>(fa.xp + (int64_t)posl[i] * d);
-      for (int c = lane; c < d8; c += 32) b[c] = a[c];
-    }
-  }
   G3_TRACE(5);
 }
 
@@ -801,18 +684,6 @@ bool ln_gate_supported(int64_t T, int64_t d, int64_t E, int k) {
   return g3_pick(T, d, E, k, &p);
 }
 
-bool ln_gate_plan_fusable(int64_t T, int64_t d, int64_t E, int k) {
-  static const bool off = std::getenv("MOE_GATE_NO_PLAN") != nullptr;  // dev A/B
-  G3Pick p;
-  if (off || !g3_pick(T, d, E, k, &p)) return false;
-  const int64_t grid = (T + p.rb - 1) / p.rb;
-  if (grid > sm_count() || (int64_t)p.rb * k > p.nt) return false;  // one wave, a thread per slot
-  const g3::Cfg c = g3::cfg(d, E, gate_fused_pitch(E), p.rb, p.epg, p.rpt, p.nt);
-  const int64_t keys = E + 1;
-  const int64_t words = keys * (grid + 1) + (keys + 1) + keys + (p.nt / 32) * keys + p.nt;
-  return (int64_t)(c.off_st - c.off_w) >= words * 4;
-}
-
 int ln_gate_rows(int64_t T, int64_t d, int64_t E, int k) {
   G3Pick p;
   return g3_pick(T, d, E, k, &p) ? p.rb : 0;
@@ -832,36 +703,15 @@ static int launch_g3(const GateFusedArgs& a, int rb, cudaStream_t st) {
   const bool tr = std::getenv("MOE_GATE_TRACE") != nullptr;
   if (tr && !dtrace) MOE_CUDA_TRY(cudaMalloc(&dtrace, 8 * (16 + 2 * 65536)));
   const int pdl = pdl_enabled(5) ? 1 : 0;
-  static const int pad_off = std::getenv("MOE_GATE_NO_PAD") ? 1 : 0;  // dev A/B
   // widened LN chains only for a few rows per CTA (decode: the passes are
   // short and the FADD-only chain is faster -- C3 T=1 10710 vs 12869 cycles);
   // many rows (C2: 28): inline conversion (6980 vs 9196 cycles)
   static const int force_wide = std::getenv("MOE_GATE_LN_WIDE") ? std::atoi(std::getenv("MOE_GATE_LN_WIDE")) : -1;
   const int ln_wide = force_wide >= 0 ? force_wide : (rb <= 8 ? 1 : 0);
-  if (a.perm != nullptr) {
-    // fused plan: every CTA must be resident for the grid barrier
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(NT);
-    cfg.dynamicSmemBytes = C.total;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[2];
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = 1;
-    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[1].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = pdl ? 2 : 1;
-    MOE_CUDA_TRY(cudaLaunchKernelEx(&cfg, ln_gate_kernel<EPG, RPT, NT>, a.x, a.T, (int)a.d, a.g, a.b,
-                                    a.gw32, (int)a.gwp, a.gb, (int)a.E, a.k, a.finished, a.xn,
-                                    a.expert, a.scale, a.blockcnt, a.bad_row, rb, a.out_fin,
-                                    tr ? dtrace : nullptr, pdl, ln_wide, a, pad_off));
-  } else {
-    MOE_CUDA_TRY(launch_k(5, ln_gate_kernel<EPG, RPT, NT>, dim3(grid), dim3(NT), C.total, st, a.x,
-                          a.T, (int)a.d, a.g, a.b, a.gw32, (int)a.gwp, a.gb, (int)a.E, a.k,
-                          a.finished, a.xn, a.expert, a.scale, a.blockcnt, a.bad_row, rb,
-                          a.out_fin, tr ? dtrace : nullptr, pdl, ln_wide, a, pad_off));
-  }
+  MOE_CUDA_TRY(launch_k(5, ln_gate_kernel<EPG, RPT, NT>, dim3(grid), dim3(NT), C.total, st, a.x,
+                        a.T, (int)a.d, a.g, a.b, a.gw32, (int)a.gwp, a.gb, (int)a.E, a.k,
+                        a.finished, a.xn, a.expert, a.scale, a.blockcnt, a.bad_row, rb,
+                        a.out_fin, tr ? dtrace : nullptr, pdl, ln_wide));
   note_launch();
   if (tr && grid <= 65536) {
     std::vector<long long> h(16 + 2 * grid);

@@ -89,18 +89,7 @@ struct GateFusedArgs {
   uint32_t* bad_row;
   int rows;            // ln_gate_rows(T, d, E, k)
   uint16_t* out_fin = nullptr;  // non-null: write out[r] = x[r] for finished rows (fused combine)
-  // fused routing plan (single wave of row blocks, cooperative launch): after
-  // a grid barrier every CTA derives the key offsets from the histogram,
-  // places its own slots and gathers its normalised rows from shared memory
-  // into xp -- the plan kernel and its global re-read of xn disappear
-  uint32_t *perm = nullptr, *inv = nullptr, *offsets = nullptr, *problems = nullptr,
-           *active = nullptr;
-  uint16_t* xp = nullptr;
-  uint32_t* gsync = nullptr;  // 2 words, zero-initialised, self-resetting (count, generation)
 };
-// the fused plan applies (one wave of row blocks, shared memory for the
-// histogram): launch_ln_gate then does the plan when a.perm is set
-bool ln_gate_plan_fusable(int64_t T, int64_t d, int64_t E, int k);
 int64_t gate_fused_pitch(int64_t E);  // f32 gate weight pitch (multiple of 8)
 // k_ln_gate.cu: LN + logits + top-k + routing-key histogram, one kernel
 bool ln_gate_supported(int64_t T, int64_t d, int64_t E, int k);

@@ -24,7 +24,6 @@ struct moe_layer {
            *problems = nullptr, *active = nullptr, *bad_row = nullptr;
   uint16_t* scale = nullptr;
   uint32_t *blockcnt = nullptr, *blockbase = nullptr, *bad_expert = nullptr, *keytot = nullptr;
-  uint32_t* gsync = nullptr;  // grid-barrier words of the fused gate + plan
   // EP: hidden activations of rows received from peers
   uint16_t* ep_h = nullptr;
   int64_t ep_cap = 0;
