@@ -66,7 +66,7 @@ int moe_cuda_free(void* ptr);
 int moe_cuda_host_alloc(void** ptr, size_t bytes); /* pinned */
 /* Write-combined pinned host memory for streaming INPUTS (host writes,
  * device reads): measured on the B200 boxes 41.8 GB/s H2D (35.6 for default
- * pinned memory, 9.1 for torch's pin_memory), and 32.8 GB/s each way with a
+ * pinned memory, 9.1 for a framework's registered pinned buffers), and 32.8 GB/s each way with a
  * concurrent D2H (12.4 for default pinned).  Host reads of it are slow. */
 int moe_cuda_host_alloc_wc(void** p, size_t bytes);
 int moe_cuda_host_free(void* ptr);
