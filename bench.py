@@ -50,6 +50,10 @@ WORKLOADS = {
     "c3_64": (32, 1024, 4096, 64, 1, "C3 decode: E=32 d_model=1024 d_ff=4096 int4 top-1 64 tokens"),
     "c4": (64, 1024, 4096, 16384, 1, "C4 MoE layer: E=64 d_model=1024 d_ff=4096 int4 top-1 16384 tokens"),
     "c5": (128, 2048, 8192, 4096, 2, "C5 EP layer: E=128 d_model=2048 d_ff=8192 int4 top-2 4096 tokens/GPU"),
+    # C4's encoder-decoder MoE stack at prefill, MoE layers only (BASELINE.md
+    # §3: 18 MoE blocks of the 24-enc / 12-dec model, MoE every other layer)
+    "c4_stack": (64, 1024, 4096, 16384, 1, "C4 prefill, MoE layers only: 18 chained MoE blocks "
+                 "(E=64 d_model=1024 d_ff=4096 int4 top-1) over 16384 tokens"),
     # decode with batch pruning: C4's decoder MoE blocks
     "decode_prune": (64, 1024, 4096, 256, 1, "beam-search decode MoE blocks with batch pruning: "
                      "C4 decoder (6 MoE blocks of E=64 d_model=1024 d_ff=4096 int4, top-1), "
@@ -490,6 +494,68 @@ def run_decode(args, wl):
     print(json.dumps(line), flush=True)
 
 
+def run_stack(args, wl):
+    """C4's MoE stack at prefill: 18 distinct MoE blocks chained (block l's
+    output feeds block l+1; moe_decode_run with one step, no finished rows),
+    captured as one CUDA graph; value = tokens through the whole stack per
+    second.  Attention / dense FFN layers of the model are outside the hot
+    path."""
+    import torch
+    from paper_2211_10017_b200 import abi
+    from paper_2211_10017_b200.decode import decode_run
+    E, d, f, T, k, label = wl
+    nblk = 18
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    layers, _ = make_layers(E, d, f, T, k, nblk, dev, seed=41)
+    g = torch.Generator(device=dev)
+    g.manual_seed(3)
+    x = torch.randn((1, T, d), generator=g, device=dev).half()
+    out = torch.empty_like(x)
+    work = torch.empty((T, d), dtype=torch.float16, device=dev)
+    n_cap = abi.launch_count()
+    decode_run(layers, x, None, k=k, mode=1, prune=False, out=out, work=work)
+    torch.cuda.synchronize()
+    per_run = abi.launch_count() - n_cap
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr):
+        decode_run(layers, x, None, k=k, mode=1, prune=False, out=out, work=work)
+    for _ in range(args.warmup):
+        gr.replay()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            gr.replay()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    hbm, tc_burst, tc_sus, peak_src = load_peaks()
+    flops = nblk * 4.0 * T * k * d * f
+    t_roof = flops / (tc_burst * 1e12)
+    line = {
+        "metric": METRIC, "value": T / (ms * 1e-3), "unit": "tokens/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f16 (int4 weight-only experts, f32 accumulate)",
+        "data": "synthetic (random_model init distributions, seeded, generated on device)",
+        "config": {"workload": label, "E": E, "d_model": d, "d_ff": f, "tokens": T, "top_k": k,
+                   "moe_blocks": nblk, "bits": 4, "mode": "fast, whole stack in one CUDA graph",
+                   "step": "one pass of 16384 tokens through the 18 MoE blocks",
+                   "l2": f"weights {nblk * E * d * f / 2**20:.0f} MiB > L2"},
+        "roofline": {"bound": "tensor", "achieved": flops / (ms * 1e-3) / 1e12, "peak": tc_burst,
+                     "unit": "TFLOP/s", "frac": t_roof / (ms * 1e-3), "traffic": None,
+                     "kernel": "whole stack (layer-level: 18 x 4*T*d*f per step / step time)",
+                     "peak_source": peak_src,
+                     "baseline_md_roofline_ms": 3.01},
+        "gpu_launches": per_run * args.steps,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
 def run_native(args, wl):
     import numpy as np
     import torch
@@ -760,6 +826,8 @@ def main():
         run_reference_arm(args, wl)
     elif args.workload == "decode_prune":
         run_decode(args, wl)
+    elif args.workload == "c4_stack":
+        run_stack(args, wl)
     else:
         run_native(args, wl)
 

@@ -659,11 +659,12 @@ static bool g3_pick(int64_t T, int64_t d, int64_t E, int k, G3Pick* p) {
   static const int kR[] = {1, 1, 1, 1, 2};
   static const int kT[] = {256, 256, 256, 256, 256};
   static const int first = std::getenv("MOE_GATE_EPG1") ? 0 : 1;
-  // dev A/B: MOE_GATE_CFG="EPG,RPT" forces a chain layout when it fits
+  // dev A/B: MOE_GATE_CFG="EPG,RPT[,threads]" forces a chain layout when it fits
   if (const char* f = std::getenv("MOE_GATE_CFG")) {
-    int fe = 0, fr = 0;
-    if (std::sscanf(f, "%d,%d", &fe, &fr) == 2 && g3_fits(d, E, gwp, rb, fe, fr, 256, k)) {
-      *p = G3Pick{rb, fe, fr, 256};
+    int fe = 0, fr = 0, fnt = 256;
+    if (std::sscanf(f, "%d,%d,%d", &fe, &fr, &fnt) >= 2 && (fnt == 256 || fnt == 512) &&
+        g3_fits(d, E, gwp, rb, fe, fr, fnt, k)) {
+      *p = G3Pick{rb, fe, fr, fnt};
       return true;
     }
   }
@@ -739,6 +740,11 @@ int launch_ln_gate(const GateFusedArgs& a, cudaStream_t st) {
   G3Pick p;
   if (!g3_pick(a.T, a.d, a.E, a.k, &p)) return set_error(MOE_EINVAL, "ln_gate: unsupported shape");
   if (p.rb != a.rows) return set_error(MOE_EINVAL, "ln_gate: row block mismatch");
+  if (p.nt == 512) {  // dev A/B layouts with 16 warps
+    if (p.epg == 8) return p.rpt == 1 ? launch_g3<8, 1, 512>(a, p.rb, st) : launch_g3<8, 2, 512>(a, p.rb, st);
+    if (p.epg == 4) return launch_g3<4, 1, 512>(a, p.rb, st);
+    return launch_g3<2, 1, 512>(a, p.rb, st);
+  }
   if (p.epg == 1) return launch_g3<1, 1, 256>(a, p.rb, st);
   if (p.epg == 2) return p.rpt == 1 ? launch_g3<2, 1, 256>(a, p.rb, st) : launch_g3<2, 2, 256>(a, p.rb, st);
   if (p.epg == 4) return p.rpt == 1 ? launch_g3<4, 1, 256>(a, p.rb, st) : launch_g3<4, 2, 256>(a, p.rb, st);
