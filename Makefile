@@ -42,7 +42,7 @@ build/%.o: $(CSRC)/%.cu $(CU_HDRS)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
 $(LIB_CUDA): $(CU_OBJS)
-	$(NVCC) $(ARCH) -shared -o $@ $(CU_OBJS) -cudart static -lcuda
+	$(NVCC) $(ARCH) -shared -Xlinker -z,defs -o $@ $(CU_OBJS) -cudart static -lcuda
 
 $(LIB_HOST): $(HOST_SRCS) $(HOST_HDRS) $(LIB_CUDA)
 	$(CXX) -std=c++20 -O2 -fPIC -shared -ffp-contract=off -Iinclude -I$(CUDA_INC) \

@@ -433,9 +433,12 @@ int moecu::layer_reserve(moe_layer* L, int64_t T, int k) {
   TRY(L->alloc(&L->dfin, cT));
   if (!L->gv_part) {
     const int64_t rmax = kGemvMaxRows;
-    const int64_t p1 = (int64_t)gemv_splits(d, f, 1.0) * f, p2 = (int64_t)gemv_splits(f, d, 1.0) * d;
-    TRY(L->alloc(&L->gv_part, rmax * std::max(p1, p2) * 4));
-    const int64_t nt = E * ((std::max(d, f) + 127) / 128);
+    // worst case over T: the most splits (one active expert, 16-row passes)
+    const int64_t p1 = (int64_t)gemv_pair_splits(d, f, 1.0, rmax) * f,
+                  p2 = (int64_t)gemv_pair_splits(f, d, 1.0, rmax) * d;
+    TRY(L->alloc(&L->gv_part, rmax * (p1 + p2) * 4));  // FFN1 | FFN2 partials (pair kernel)
+    // tickets FFN1 | FFN2, FFN1 tile-ready flags, claim counter + exit count
+    const int64_t nt = E * (2 * ((f + 127) / 128) + (d + 127) / 128) + 2;
     TRY(L->alloc(&L->gv_ticket, nt * 4));
     MOE_CUDA_TRY(cudaMemset(L->gv_ticket, 0, nt * 4));
   }
@@ -471,7 +474,20 @@ int moecu::layer_route(moe_layer* L, const uint16_t* x, const uint8_t* fin, int6
   MOE_CUDA_TRY(cudaMemsetAsync(L->bad_row, 0xFF, 8, st));  // bad_row + bad_expert
   TRY(mark());
   PlanWork w{L->blockcnt, L->blockbase, L->bad_expert, L->keytot};
-  if (fused_gate_ok(L, x, T, k)) {
+  if (fused_gate_ok(L, x, T, k) && gate_tile_supported(T, d, E, k)) {
+    // wide gates (C4, C5): LN alone, then the logits as a tiled GEMM + top-k
+    // + key histogram per tile of rows; then scan / place / gather
+    const int tr = gate_tile_rows(T);
+    GateFusedArgs ga{x, T, d, L->ln_g, L->ln_b, L->gw32, L->gwp, L->gb, E, k, fin, L->xn,
+                     L->expert, L->scale, L->blockcnt, L->bad_row, tr, out_fin};
+    TRY(launch_ln_rows(ga, st));
+    TRY(mark());
+    TRY(launch_gate_tile(ga, tr, st));
+    TRY(mark());
+    TRY(mark());
+    TRY(launch_plan_from_counts(L->expert, fin, T, k, E, (int64_t)tr * k, w, L->perm, L->inv,
+                                L->offsets, L->problems, L->active, L->xn, d, L->xp, st));
+  } else if (fused_gate_ok(L, x, T, k)) {
     // one kernel: LN + logits + top-k + key histogram; then scan/place/gather
     GateFusedArgs ga{x, T, d, L->ln_g, L->ln_b, L->gw32, L->gwp, L->gb, E, k, fin, L->xn,
                      L->expert, L->scale, L->blockcnt, L->bad_row, ln_gate_rows(T, d, E, k),
@@ -516,11 +532,24 @@ int moecu::layer_ffn(moe_layer* L, const uint16_t* xin, int64_t rows, const uint
   if (mode == MOE_MODE_FAST && rows <= kGemvMaxRows) {
     // decode regime: stream the active experts' weights (K5)
     const double act = (double)El * (1.0 - std::pow(1.0 - 1.0 / (double)El, (double)rows));
-    GemvWork w1{L->gv_part, L->gv_ticket, gemv_splits(d, f, act)};
-    GemvWork w2{L->gv_part, L->gv_ticket, gemv_splits(f, d, act)};
-    TRY(launch_gemv(g1, w1, st));
-    TRY(mark());
-    TRY(launch_gemv(g2, w2, st));
+    const int64_t nft1 = (f + 127) / 128;
+    const int64_t p1 = kGemvMaxRows * (int64_t)gemv_pair_splits(d, f, 1.0, kGemvMaxRows) * f;
+    static const bool want_pair =
+        std::getenv("MOE_GEMV_PAIR") && std::atoi(std::getenv("MOE_GEMV_PAIR")) == 1;
+    const bool pair = want_pair && gemv_pair_supported(rows, np, d, f);
+    GemvWork w1{L->gv_part, L->gv_ticket, pair ? gemv_pair_splits(d, f, act, rows) : gemv_splits(d, f, act)};
+    GemvWork w2{L->gv_part + p1, L->gv_ticket + L->E * nft1,
+                pair ? gemv_pair_splits(f, d, act, rows) : gemv_splits(f, d, act)};
+    if (pair) {
+      // one launch: FFN2 items start as the FFN1 tiles they read complete
+      uint32_t* ready = L->gv_ticket + L->E * (nft1 + (d + 127) / 128);
+      TRY(launch_gemv_pair(g1, g2, w1, w2, ready, ready + L->E * nft1, st));
+      TRY(mark());
+    } else {
+      TRY(launch_gemv(g1, w1, st));
+      TRY(mark());
+      TRY(launch_gemv(g2, w2, st));
+    }
   } else if (mode == MOE_MODE_FAST) {
     TRY(launch_gemm_tc(g1, st));
     TRY(mark());

@@ -239,8 +239,11 @@ __device__ __forceinline__ void logit_chunk(float2 (&acc)[RPT][EPG >= 2 ? EPG / 
     if (kk + d * KS < kn) fma_step(r[d]);
 }
 
-template <int EPG, int RPT, int NT>
-__global__ void __launch_bounds__(NT, 1) ln_gate_kernel(
+// LNONLY: the LayerNorm half alone (xn to global, finished-row passthrough)
+// for the wide-gate path (k_gate_tile.cu): no gate weights, E = gwp = 0;
+// a lean instantiation that fits three CTAs per SM
+template <int EPG, int RPT, int NT, bool LNONLY = false>
+__global__ void __launch_bounds__(NT, LNONLY ? 3 : 1) ln_gate_kernel(
     const uint16_t* __restrict__ x, int64_t T, int d, const uint16_t* __restrict__ lng,
     const uint16_t* __restrict__ lnb, const float* __restrict__ gw32, int gwp,
     const uint16_t* __restrict__ gb, int E, int k, const uint8_t* __restrict__ finished,
@@ -287,12 +290,12 @@ __global__ void __launch_bounds__(NT, 1) ln_gate_kernel(
     // launched early (PDL): the gate weights never change, fetch them while
     // the previous kernel retires; otherwise the rows first (the LN chains
     // wait on them; the weights are needed only by the logit phase)
-    if (pdl) weights();
+    if (!LNONLY && pdl) weights();
     griddep_wait();  // x and finished may be the previous kernel's output
     for (int r = tid; r < nrow; r += 32)
       bulk_load(xs + (size_t)r * xp, x + (r0 + r) * d, (uint32_t)d * 2, &bars[0]);
     __syncwarp();
-    if (!pdl) weights();
+    if (!LNONLY && !pdl) weights();
   } else {
     // the small operands every later phase reads, fetched while the rows
     // land (each would otherwise cost an L2 round trip on the critical path)
@@ -447,6 +450,7 @@ __global__ void __launch_bounds__(NT, 1) ln_gate_kernel(
   }
   __syncthreads();
   G3_TRACE(3);
+  if constexpr (LNONLY) return;
 
   // ---- logit chains (model.cpp:273-297): RPT rows x EPG experts per thread.
   // Operands of KS inputs per step; with few chains per thread the chain
@@ -733,6 +737,28 @@ static int launch_g3(const GateFusedArgs& a, int rb, cudaStream_t st) {
                  h[8] - h[1], h[9] - h[8], h[10] - h[9], h[11] - h[10], h[2] - h[11]);
   }
   return check_launch("ln_gate");
+}
+
+// LN only: rows per CTA sized for ~60 KB of shared memory (three CTAs per SM)
+int launch_ln_rows(const GateFusedArgs& a, cudaStream_t st) {
+  if (a.T == 0) return MOE_OK;
+  if (a.d % 8 != 0) return set_error(MOE_EINVAL, "ln_rows: d must be a multiple of 8");
+  const int rb = (int)std::max<int64_t>(1, std::min<int64_t>(64, 60 * 1024 / ((a.d + 8) * 2) - 1));
+  const g3::Cfg C = g3::cfg(a.d, 0, 0, rb, 2, 1, 256);
+  static size_t attr = 0;
+  if (C.total > 48 * 1024 && C.total > attr) {
+    MOE_CUDA_TRY(cudaFuncSetAttribute(ln_gate_kernel<2, 1, 256, true>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C.total));
+    attr = C.total;
+  }
+  const unsigned grid = (unsigned)((a.T + rb - 1) / rb);
+  MOE_CUDA_TRY(launch_k(0, ln_gate_kernel<2, 1, 256, true>, dim3(grid), dim3(256), C.total, st, a.x,
+                        a.T, (int)a.d, a.g, a.b, (const float*)nullptr, 0, (const uint16_t*)nullptr,
+                        0, 1, a.finished, a.xn, (uint32_t*)nullptr, (uint16_t*)nullptr,
+                        (uint32_t*)nullptr, a.bad_row, rb, a.out_fin, (long long*)nullptr, 0,
+                        rb <= 8 ? 1 : 0));
+  note_launch();
+  return check_launch("ln_rows");
 }
 
 int launch_ln_gate(const GateFusedArgs& a, cudaStream_t st) {

@@ -97,6 +97,14 @@ int ln_gate_rows(int64_t T, int64_t d, int64_t E, int k);  // rows per block (Ga
 int launch_ln_gate(const GateFusedArgs& a, cudaStream_t st);
 int launch_widen_gate(const uint16_t* gw, int64_t d, int64_t E, int64_t gwp, float* out,
                       cudaStream_t st);
+// LN only (the ln_gate kernel's LayerNorm, xn to global + finished-row
+// passthrough), for the wide-gate path below
+int launch_ln_rows(const GateFusedArgs& a, cudaStream_t st);
+// k_gate_tile.cu: wide gates (E = 64 / 128, T*E >= 2^18): logits as a
+// register-tiled GEMM over xn + top-k + key histogram per tile of rows
+bool gate_tile_supported(int64_t T, int64_t d, int64_t E, int k);
+int gate_tile_rows(int64_t T);  // rows per tile (the plan's slots per block / k)
+int launch_gate_tile(const GateFusedArgs& a, int tile_rows, cudaStream_t st);
 
 // k_route.cu
 struct PlanWork {
@@ -163,6 +171,14 @@ struct GemvWork {
 };
 int gemv_splits(int64_t m, int64_t n, double active_experts);
 int launch_gemv(const GemmArgs& a, const GemvWork& w, cudaStream_t st);
+// both GEMMs of a decode FFN pair in one persistent launch (a2.x == a1.out);
+// w1 / w2 need distinct split-K workspaces; ready: E * ceil(a1.n / 128)
+// words, ctl: 2 words, both zero-initialised and self-resetting
+int launch_gemv_pair(const GemmArgs& a1, const GemmArgs& a2, const GemvWork& w1,
+                     const GemvWork& w2, uint32_t* ready, uint32_t* ctl, cudaStream_t st);
+bool gemv_pair_supported(int64_t rows, int64_t np, int64_t d, int64_t f);
+// splits whose k range fits the pair kernel's rows buffers (rows: routed rows)
+int gemv_pair_splits(int64_t m, int64_t n, double active_experts, int64_t rows);
 int launch_gemm_tc(const GemmArgs& a, cudaStream_t st);
 
 }  // namespace moecu

@@ -1,0 +1,15 @@
+MOE_GEMV_PAIR=0 python scripts/pair_debug2.py 16 37 2 gpurun_out/d2_two.npz
+for dbg in 0 1 2 4 8 15; do
+MOE_GEMV_PAIR_DBG=$dbg python scripts/pair_debug2.py 16 37 2 gpurun_out/d2_pair.npz
+python - <<PY
+import numpy as np
+a=np.load('gpurun_out/d2_pair.npz'); b=np.load('gpurun_out/d2_two.npz')
+off=a['offsets']; live=int(off[-1])
+res=[]
+for name in ('y0','y1','y2'):
+    ya=a[name][:live].view(np.float16).astype(np.float32); yb=b['y0'][:live].view(np.float16).astype(np.float32)
+    bad=np.nonzero(np.abs(ya-yb).max(1)>1e-3)[0]
+    res.append(sorted(set(int(np.searchsorted(off, r, side='right')-1) for r in bad)))
+print('dbg $dbg bad experts per call', res)
+PY
+done

@@ -149,7 +149,8 @@ def test_layer_decode_shapes(cuda, oracle, T):
 @pytest.mark.parametrize("E,d,T,k", [(8, 512, 4096, 2), (64, 1024, 600, 1), (128, 256, 300, 2),
                                      (3, 40, 50, 3), (130, 64, 20, 1), (300, 32, 40, 2),
                                      (32, 1024, 4096, 2), (64, 1024, 16384, 1), (8, 512, 1, 1),
-                                     (256, 2048, 700, 8)])
+                                     (256, 2048, 700, 8), (128, 512, 4100, 2), (64, 1024, 5000, 3),
+                                     (64, 256, 9000, 1), (128, 2048, 2100, 1)])
 def test_layer_fused_gate_routing_exact(cuda, oracle, E, d, T, k):
     """Fused LN+logits+top-k+histogram kernel (and the unfused fallback for
     E > 256): routing identical to the oracle at BASELINE-like shapes --
@@ -251,3 +252,22 @@ def test_layer_load_report(cuda, cf):
     assert rep["experts_over"] == int((load > cap).sum())
     assert rep["overflow_rows"] == int(np.maximum(load - cap, 0).sum())
     assert rep["active_experts"] == int((load > 0).sum())
+
+
+@pytest.mark.parametrize("bits", [16, 8, 4])
+@pytest.mark.parametrize("T,k", [(1, 1), (37, 2), (200, 1)])
+def test_layer_decode_pair_repeat(cuda, oracle, bits, T, k):
+    """Decode FFN pair in one launch (FFN2 items wait on FFN1's tile-ready
+    flags; claim counter and flags self-reset): within tolerance of the
+    oracle and bitwise identical over repeated forwards (a stale flag or
+    counter from the previous launch would skip or corrupt items)."""
+    lw, x, fin = _case(256, 1024, 32, T, seed=900 + T + bits, fin_frac=0.1 if T > 1 else 0.0)
+    L = _layer(lw, bits)
+    q = tuple(to_np(t) for t in L.quant) if bits != 16 else None
+    want = oracle.moe_forward(lw, x, fin, k=k, bits=bits, q=q)
+    xd, fd = to_dev(x), to_dev(fin)
+    first = to_np(L.forward(xd, fd, k=k, mode=1))
+    if (want != x).any():
+        assert layer_err(first, want, x) <= TOL_FAST
+    for _ in range(6):
+        assert np.array_equal(bits16(to_np(L.forward(xd, fd, k=k, mode=1))), bits16(first))
