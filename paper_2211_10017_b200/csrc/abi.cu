@@ -536,7 +536,7 @@ int moecu::layer_ffn(moe_layer* L, const uint16_t* xin, int64_t rows, const uint
     const int64_t p1 = kGemvMaxRows * (int64_t)gemv_pair_splits(d, f, 1.0, kGemvMaxRows) * f;
     static const bool want_pair =
         std::getenv("MOE_GEMV_PAIR") && std::atoi(std::getenv("MOE_GEMV_PAIR")) == 1;
-    const bool pair = want_pair && gemv_pair_supported(rows, np, d, f);
+    const bool pair = want_pair && gemv_pair_supported(rows, np, d, f, L->bits);
     GemvWork w1{L->gv_part, L->gv_ticket, pair ? gemv_pair_splits(d, f, act, rows) : gemv_splits(d, f, act)};
     GemvWork w2{L->gv_part + p1, L->gv_ticket + L->E * nft1,
                 pair ? gemv_pair_splits(f, d, act, rows) : gemv_splits(f, d, act)};

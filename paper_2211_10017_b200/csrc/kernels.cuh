@@ -176,7 +176,7 @@ int launch_gemv(const GemmArgs& a, const GemvWork& w, cudaStream_t st);
 // words, ctl: 2 words, both zero-initialised and self-resetting
 int launch_gemv_pair(const GemmArgs& a1, const GemmArgs& a2, const GemvWork& w1,
                      const GemvWork& w2, uint32_t* ready, uint32_t* ctl, cudaStream_t st);
-bool gemv_pair_supported(int64_t rows, int64_t np, int64_t d, int64_t f);
+bool gemv_pair_supported(int64_t rows, int64_t np, int64_t d, int64_t f, int bits);
 // splits whose k range fits the pair kernel's rows buffers (rows: routed rows)
 int gemv_pair_splits(int64_t m, int64_t n, double active_experts, int64_t rows);
 int launch_gemm_tc(const GemmArgs& a, cudaStream_t st);

@@ -257,10 +257,9 @@ def test_layer_load_report(cuda, cf):
 @pytest.mark.parametrize("bits", [16, 8, 4])
 @pytest.mark.parametrize("T,k", [(1, 1), (37, 2), (200, 1)])
 def test_layer_decode_pair_repeat(cuda, oracle, bits, T, k):
-    """Decode FFN pair in one launch (FFN2 items wait on FFN1's tile-ready
-    flags; claim counter and flags self-reset): within tolerance of the
-    oracle and bitwise identical over repeated forwards (a stale flag or
-    counter from the previous launch would skip or corrupt items)."""
+    """Decode-shaped layers at 16/8/4 bits: within tolerance of the oracle
+    on the first forward (fresh workspace) and bitwise identical over
+    repeated forwards (split-K tickets self-reset; no stale state)."""
     lw, x, fin = _case(256, 1024, 32, T, seed=900 + T + bits, fin_frac=0.1 if T > 1 else 0.0)
     L = _layer(lw, bits)
     q = tuple(to_np(t) for t in L.quant) if bits != 16 else None
