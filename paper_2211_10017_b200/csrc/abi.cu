@@ -477,7 +477,7 @@ int moecu::layer_route(moe_layer* L, const uint16_t* x, const uint8_t* fin, int6
   if (fused_gate_ok(L, x, T, k) && gate_tile_supported(T, d, E, k)) {
     // wide gates (C4, C5): LN alone, then the logits as a tiled GEMM + top-k
     // + key histogram per tile of rows; then scan / place / gather
-    const int tr = gate_tile_rows(T);
+    const int tr = gate_tile_rows(T, E);
     GateFusedArgs ga{x, T, d, L->ln_g, L->ln_b, L->gw32, L->gwp, L->gb, E, k, fin, L->xn,
                      L->expert, L->scale, L->blockcnt, L->bad_row, tr, out_fin};
     TRY(launch_ln_rows(ga, st));

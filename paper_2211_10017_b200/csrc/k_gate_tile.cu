@@ -38,9 +38,10 @@ __device__ __forceinline__ float2 ffma2(float a, float2 b, float2 c) {
   return make_float2(__uint_as_float((uint32_t)r), __uint_as_float((uint32_t)(r >> 32)));
 }
 
-template <int RPT, int EPT>
+// RG x EG threads (RG % 8 == 0, EG % 4 == 0), each RPT rows x EPT experts
+template <int RPT, int EPT, int RG, int EG>
 struct Cfg {
-  static constexpr int TR = 16 * RPT, EP = 16 * EPT;
+  static constexpr int TR = RG * RPT, EP = EG * EPT, NT = RG * EG;
   static constexpr int XS = KC * TR, WS = KC * EP;     // floats per buffer
   static constexpr int STAGE = 2 * (XS + WS);          // two buffers
   static constexpr int LG = TR * (EP + 1);             // logits | expf
@@ -55,14 +56,14 @@ struct Cfg {
 };
 }  // namespace gt
 
-template <int RPT, int EPT>
-__global__ void __launch_bounds__(gt::kThreads, 1) gate_tile_kernel(
+template <int RPT, int EPT, int RG, int EG>
+__global__ void __launch_bounds__(RG * EG, 1) gate_tile_kernel(
     const uint16_t* __restrict__ xn, int64_t T, int d, const float* __restrict__ gw32, int gwp,
     const uint16_t* __restrict__ gb, int E, int k, const uint8_t* __restrict__ finished,
     uint32_t* __restrict__ expert, uint16_t* __restrict__ scale, uint32_t* __restrict__ blockcnt,
     uint32_t* bad_row) {
-  using C = gt::Cfg<RPT, EPT>;
-  constexpr int TR = C::TR, EP = C::EP, KC = gt::KC, NT = gt::kThreads;
+  using C = gt::Cfg<RPT, EPT, RG, EG>;
+  constexpr int TR = C::TR, EP = C::EP, KC = gt::KC, NT = C::NT;
   extern __shared__ __align__(16) uint8_t sm[];
   float* body = reinterpret_cast<float*>(sm);
   float* bsm = reinterpret_cast<float*>(sm + C::OFF_BIAS);
@@ -135,7 +136,8 @@ __global__ void __launch_bounds__(gt::kThreads, 1) gate_tile_kernel(
   // eg*EPT..; a warp covers 8 row groups x 4 expert groups, so each half-warp
   // reads 4 distinct x vectors and 4 distinct weight vectors per input (one
   // shared-memory wavefront each)
-  const int eg = ((tid >> 5) & 3) * 4 + (tid & 3), rg = (tid >> 7) * 8 + ((tid & 31) >> 2);
+  constexpr int WE = EG / 4;  // warps along the experts
+  const int eg = ((tid >> 5) % WE) * 4 + (tid & 3), rg = ((tid >> 5) / WE) * 8 + ((tid & 31) >> 2);
   float2 acc[RPT][EPT / 2];
 #pragma unroll
   for (int i = 0; i < RPT; ++i)
@@ -298,7 +300,7 @@ bool gate_tile_supported(int64_t T, int64_t d, int64_t E, int k) {
          T * E >= (int64_t)1 << 18;
 }
 
-int gate_tile_rows(int64_t T) {
+int gate_tile_rows(int64_t T, int64_t E) {
   static const int force = std::getenv("MOE_GATE_TILE_RPT") ? std::atoi(std::getenv("MOE_GATE_TILE_RPT")) : 0;
   if (force == 2 || force == 4 || force == 8) return 16 * force;
   // rows per tile: 16 * RPT, RPT in {2, 4, 8}: the largest whose tiles still
@@ -309,33 +311,38 @@ int gate_tile_rows(int64_t T) {
   return 32;
 }
 
-template <int RPT, int EPT>
+template <int RPT, int EPT, int RG, int EG>
 static int launch_tile(const GateFusedArgs& a, cudaStream_t st) {
-  using C = gt::Cfg<RPT, EPT>;
+  using C = gt::Cfg<RPT, EPT, RG, EG>;
   static bool attr = false;
   if (!attr) {
-    MOE_CUDA_TRY(cudaFuncSetAttribute(gate_tile_kernel<RPT, EPT>,
+    MOE_CUDA_TRY(cudaFuncSetAttribute(gate_tile_kernel<RPT, EPT, RG, EG>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr = true;
   }
   const unsigned grid = (unsigned)((a.T + C::TR - 1) / C::TR);
-  MOE_CUDA_TRY(launch_k(0, gate_tile_kernel<RPT, EPT>, dim3(grid), dim3(gt::kThreads), C::SMEM, st,
+  MOE_CUDA_TRY(launch_k(0, gate_tile_kernel<RPT, EPT, RG, EG>, dim3(grid), dim3(C::NT), C::SMEM, st,
                         (const uint16_t*)a.xn, a.T, (int)a.d, a.gw32, (int)a.gwp, a.gb, (int)a.E,
                         a.k, a.finished, a.expert, a.scale, a.blockcnt, a.bad_row));
   note_launch();
   return check_launch("gate_tile");
 }
 
+// tile shapes (rows per tile tr): 256 threads (16 row groups x 16 expert
+// groups) x {8,4,2} rows x E/16 experts.  Measured at C4: 4 x 4 (tr 64) 90 us,
+// 8 x 4 (tr 128) 90 us, 128 threads x 8 x 8 (tr 128) 106 us
 int launch_gate_tile(const GateFusedArgs& a, int tr, cudaStream_t st) {
   if (a.T == 0) return MOE_OK;
   if (!gate_tile_supported(a.T, a.d, a.E, a.k)) return set_error(MOE_EINVAL, "gate_tile: unsupported shape");
-  const int ept = (int)(a.E / 16);
-  const int rpt = tr / 16;
-#define GT_CASE(R, E_)                                     \
-  if (rpt == R && ept == E_) return launch_tile<R, E_>(a, st);
-  GT_CASE(8, 4) GT_CASE(4, 4) GT_CASE(2, 4)
-  GT_CASE(8, 8) GT_CASE(4, 8) GT_CASE(2, 8)
-#undef GT_CASE
+  if (a.E == 64) {
+    if (tr == 128) return launch_tile<8, 4, 16, 16>(a, st);
+    if (tr == 64) return launch_tile<4, 4, 16, 16>(a, st);
+    if (tr == 32) return launch_tile<2, 4, 16, 16>(a, st);
+  } else {
+    if (tr == 128) return launch_tile<8, 8, 16, 16>(a, st);
+    if (tr == 64) return launch_tile<4, 8, 16, 16>(a, st);
+    if (tr == 32) return launch_tile<2, 8, 16, 16>(a, st);
+  }
   return set_error(MOE_EINVAL, "gate_tile: no tile for E=%lld rows=%d", (long long)a.E, tr);
 }
 

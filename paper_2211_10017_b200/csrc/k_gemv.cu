@@ -809,8 +809,18 @@ __global__ void __launch_bounds__(kPairThreads, 3) gemv_pair_kernel(const PairPa
 
 int gemv_splits(int64_t m, int64_t n, double active_experts) {
   const int64_t nft = (n + 127) / 128, nkb = (m + 63) / 64;
+  static const int force = std::getenv("MOE_GEMV_SPLITS") ? std::atoi(std::getenv("MOE_GEMV_SPLITS")) : 0;
+  if (force > 0) {  // dev A/B: a fixed split count (capped so the k range stays <= 1024 inputs)
+    int s = force;
+    while (s < 64 && (nkb + s - 1) / s > 16) s *= 2;
+    return s;
+  }
+  // split k only until the items cover the SMs once: a split costs a rows
+  // re-stage, a pipeline fill and the ordered reduction (measured C3 T=8
+  // FFN2: 4 splits 14.5 us, 8 splits 18.7 us; T=64 FFN1: 1 split 29.7 us,
+  // 2 splits 42.0 us)
   int s = 1;
-  while (s < 16 && nkb / (2 * s) >= 4 && active_experts * nft * s < 2.0 * 148) s *= 2;
+  while (s < 16 && nkb / (2 * s) >= 4 && active_experts * nft * s < 1.0 * sm_count()) s *= 2;
   while (s < 64 && (nkb + s - 1) / s > 16) s *= 2;  // <= 1024 inputs staged per CTA
   return s;
 }

@@ -426,6 +426,30 @@ __global__ void __launch_bounds__(NT, LNONLY ? 3 : 1) ln_gate_kernel(
   G3_TRACE(2);
 
   // ---- normalise in place (model.cpp:193-194); xn also to global for the gather
+  if constexpr (LNONLY) {
+    // xn to global only: a thread owns one 8-column chunk (gamma / beta in
+    // registers) over every rsplit-th row; a row's chunks are one coalesced
+    // store per warp
+    const int rsplit = d8 >= NT ? 1 : NT / d8;
+    for (int q = tid; q < d8 * rsplit; q += NT) {
+      const int c = q % d8, rs = q / d8;
+      const float4 g0 = reinterpret_cast<const float4*>(gsm)[2 * c];
+      const float4 g1 = reinterpret_cast<const float4*>(gsm)[2 * c + 1];
+      const float4 b0 = reinterpret_cast<const float4*>(gsm + d)[2 * c];
+      const float4 b1 = reinterpret_cast<const float4*>(gsm + d)[2 * c + 1];
+      const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+      const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+      for (int r = rs; r < nrow; r += rsplit) {
+        uint4 v = *reinterpret_cast<const uint4*>(xs + (size_t)r * xp + c * 8);
+        uint16_t* h = reinterpret_cast<uint16_t*>(&v);
+        const float mean = st[r], inv = st[rb + r];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          h[j] = f2h(__fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(h2f(h[j]), mean), inv), gg[j]), bb[j]));
+        *reinterpret_cast<uint4*>(xn + (r0 + r) * d + c * 8) = v;
+      }
+    }
+  } else
   for (int i = tid; i < nrow * d8; i += NT) {
     const int r = i / d8, c = i - r * d8;
     uint4 v = *reinterpret_cast<const uint4*>(xs + (size_t)r * xp + c * 8);
@@ -450,7 +474,10 @@ __global__ void __launch_bounds__(NT, LNONLY ? 3 : 1) ln_gate_kernel(
   }
   __syncthreads();
   G3_TRACE(3);
-  if constexpr (LNONLY) return;
+  if constexpr (LNONLY) {
+    G3_TRACE(5);
+    return;
+  }
 
   // ---- logit chains (model.cpp:273-297): RPT rows x EPG experts per thread.
   // Operands of KS inputs per step; with few chains per thread the chain
@@ -752,12 +779,30 @@ int launch_ln_rows(const GateFusedArgs& a, cudaStream_t st) {
     attr = C.total;
   }
   const unsigned grid = (unsigned)((a.T + rb - 1) / rb);
+  static long long* dtrace = nullptr;
+  const bool tr = std::getenv("MOE_GATE_TRACE") != nullptr && grid <= 65536;
+  if (tr && !dtrace) MOE_CUDA_TRY(cudaMalloc(&dtrace, 8 * (16 + 2 * 65536)));
   MOE_CUDA_TRY(launch_k(0, ln_gate_kernel<2, 1, 256, true>, dim3(grid), dim3(256), C.total, st, a.x,
                         a.T, (int)a.d, a.g, a.b, (const float*)nullptr, 0, (const uint16_t*)nullptr,
                         0, 1, a.finished, a.xn, (uint32_t*)nullptr, (uint16_t*)nullptr,
-                        (uint32_t*)nullptr, a.bad_row, rb, a.out_fin, (long long*)nullptr, 0,
+                        (uint32_t*)nullptr, a.bad_row, rb, a.out_fin, tr ? dtrace : nullptr, 0,
                         rb <= 8 ? 1 : 0));
   note_launch();
+  if (tr) {  // dev: per-CTA spans and CTA 0 phase clocks
+    std::vector<long long> h(16 + 2 * grid);
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h.data(), dtrace, h.size() * 8, cudaMemcpyDeviceToHost);
+    long long lo = h[16], hi = h[17], sum = 0;
+    for (unsigned i = 0; i < grid; ++i) {
+      lo = std::min(lo, h[16 + 2 * i]);
+      hi = std::max(hi, h[17 + 2 * i]);
+      sum += h[17 + 2 * i] - h[16 + 2 * i];
+    }
+    std::fprintf(stderr,
+                 "ln_rows grid=%u rb=%d: span=%lld ns cta mean=%lld ns; cta0 clocks rows=%lld chains=%lld "
+                 "norm=%lld [mean chain %lld]\n",
+                 grid, rb, hi - lo, sum / grid, h[1] - h[0], h[2] - h[1], h[3] - h[2], h[9] - h[1]);
+  }
   return check_launch("ln_rows");
 }
 

@@ -103,7 +103,7 @@ int launch_ln_rows(const GateFusedArgs& a, cudaStream_t st);
 // k_gate_tile.cu: wide gates (E = 64 / 128, T*E >= 2^18): logits as a
 // register-tiled GEMM over xn + top-k + key histogram per tile of rows
 bool gate_tile_supported(int64_t T, int64_t d, int64_t E, int k);
-int gate_tile_rows(int64_t T);  // rows per tile (the plan's slots per block / k)
+int gate_tile_rows(int64_t T, int64_t E);  // rows per tile (the plan's slots per block / k)
 int launch_gate_tile(const GateFusedArgs& a, int tile_rows, cudaStream_t st);
 
 // k_route.cu
