@@ -425,11 +425,11 @@ __global__ void __launch_bounds__(NT, LNONLY ? 3 : 1) ln_gate_kernel(
   __syncthreads();
   G3_TRACE(2);
 
-  // ---- normalise in place (model.cpp:193-194); xn also to global for the gather
-  if constexpr (LNONLY) {
-    // xn to global only: a thread owns one 8-column chunk (gamma / beta in
-    // registers) over every rsplit-th row; a row's chunks are one coalesced
-    // store per warp
+  // ---- normalise in place (model.cpp:193-194); xn also to global for the
+  // gather.  A thread owns one 8-column chunk (gamma / beta in registers)
+  // over every rsplit-th row: no per-element index division, and a row's
+  // chunks are one coalesced store per warp
+  {
     const int rsplit = d8 >= NT ? 1 : NT / d8;
     for (int q = tid; q < d8 * rsplit; q += NT) {
       const int c = q % d8, rs = q / d8;
@@ -447,29 +447,15 @@ __global__ void __launch_bounds__(NT, LNONLY ? 3 : 1) ln_gate_kernel(
         for (int j = 0; j < 8; ++j)
           h[j] = f2h(__fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(h2f(h[j]), mean), inv), gg[j]), bb[j]));
         *reinterpret_cast<uint4*>(xn + (r0 + r) * d + c * 8) = v;
+        if constexpr (!LNONLY) {
+          *reinterpret_cast<uint4*>(xs + (size_t)r * xp + c * 8) = v;
+          if (C.wide) {  // f32 copy for the logit chains (no conversion on their path)
+            float4* dst = reinterpret_cast<float4*>(xf + (size_t)r * fp + c * 8);
+            dst[0] = make_float4(h2f(h[0]), h2f(h[1]), h2f(h[2]), h2f(h[3]));
+            dst[1] = make_float4(h2f(h[4]), h2f(h[5]), h2f(h[6]), h2f(h[7]));
+          }
+        }
       }
-    }
-  } else
-  for (int i = tid; i < nrow * d8; i += NT) {
-    const int r = i / d8, c = i - r * d8;
-    uint4 v = *reinterpret_cast<const uint4*>(xs + (size_t)r * xp + c * 8);
-    uint16_t* h = reinterpret_cast<uint16_t*>(&v);
-    const float4 g0 = reinterpret_cast<const float4*>(gsm)[2 * c];
-    const float4 g1 = reinterpret_cast<const float4*>(gsm)[2 * c + 1];
-    const float4 b0 = reinterpret_cast<const float4*>(gsm + d)[2 * c];
-    const float4 b1 = reinterpret_cast<const float4*>(gsm + d)[2 * c + 1];
-    const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-    const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-    const float mean = st[r], inv = st[rb + r];
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-      h[j] = f2h(__fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(h2f(h[j]), mean), inv), gg[j]), bb[j]));
-    *reinterpret_cast<uint4*>(xs + (size_t)r * xp + c * 8) = v;
-    *reinterpret_cast<uint4*>(xn + (r0 + r) * d + c * 8) = v;
-    if (C.wide) {  // f32 copy for the logit chains (no conversion on their path)
-      float4* dst = reinterpret_cast<float4*>(xf + (size_t)r * fp + c * 8);
-      dst[0] = make_float4(h2f(h[0]), h2f(h[1]), h2f(h[2]), h2f(h[3]));
-      dst[1] = make_float4(h2f(h[4]), h2f(h[5]), h2f(h[6]), h2f(h[7]));
     }
   }
   __syncthreads();
