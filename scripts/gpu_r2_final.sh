@@ -10,6 +10,7 @@ python bench.py 2>&1 | tail -1 > gpurun_out/final_c2.json; cat gpurun_out/final_
 python bench.py --impl reference --steps 3 --warmup 1 2>&1 | tail -1 > gpurun_out/final_ref.json; cat gpurun_out/final_ref.json
 for w in c1i4 c3_1 c3_8 c3_64 c4 c5; do python bench.py --workload $w --steps 100 --warmup 5 --no-cpu-baseline 2>&1 | tail -1 > gpurun_out/final_$w.json; cat gpurun_out/final_$w.json | cut -c1-200; done
 python bench.py --workload decode_prune --steps 5 --warmup 3 2>&1 | tail -1 > gpurun_out/final_decode.json
+python bench.py --workload c4_stack --steps 10 --warmup 3 2>&1 | tail -1 > gpurun_out/final_c4_stack.json
 python bench.py --force-ep --workload c5 --steps 20 --warmup 3 2>/dev/null | tail -1 > gpurun_out/final_ep_c5.json
 python scripts/quant_bench.py > gpurun_out/final_quant.jsonl 2>&1
 for w in c2 c3_64 c4; do
@@ -18,5 +19,5 @@ for w in c2 c3_64 c4; do
 done
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"gemm_tc|ln_gate|plan|combine" -s 5 -c 5 -o gpurun_out/prof_final_c2 python scripts/layer_once_gpu.py 512 2048 8 4096 2 3 > /dev/null 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"gemv|ln_gate" -s 3 -c 3 -o gpurun_out/prof_final_c3 python scripts/layer_once_gpu.py 1024 4096 32 64 1 3 > /dev/null 2>&1
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:"gemm_tc" -s 2 -c 2 -o gpurun_out/prof_final_c4 python scripts/layer_once_gpu.py 1024 4096 64 16384 1 3 > /dev/null 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"gemm_tc|gate_tile|ln_gate" -s 4 -c 4 -o gpurun_out/prof_final_c4 python scripts/layer_once_gpu.py 1024 4096 64 16384 1 3 > /dev/null 2>&1
 ls -la gpurun_out | tail -30
