@@ -15,7 +15,8 @@ CSRC     := $(PKG)/csrc
 ARCH     := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS  := -std=c++17 -O3 $(ARCH) -lineinfo --fmad=false -Xcompiler -fPIC -Xcompiler -ffp-contract=off \
             -I$(CSRC) -Iinclude --expt-relaxed-constexpr
-CUDA_INC := /usr/local/cuda/include
+CUDA_HOME ?= /usr/local/cuda
+CUDA_INC := $(CUDA_HOME)/include
 PYINC    := $(shell $(PY) -c "import sysconfig;print(sysconfig.get_paths()['include'])")
 PYBIND   := $(shell $(PY) -c "import pybind11;print(pybind11.get_include())")
 PYEXT    := $(shell $(PY) -c "import sysconfig;print(sysconfig.get_config_var('EXT_SUFFIX'))")
@@ -29,13 +30,15 @@ HOST_HDRS := $(wildcard include/moeinfer/*.hpp) include/moe_cuda.h
 LIB_CUDA := $(PKG)/libmoe_cuda.so
 LIB_HOST := $(PKG)/libmoeinfer_b200.so
 PYMOD    := $(PKG)/_moeinfer$(PYEXT)
+BENCHCLI := $(PKG)/moe_bench
 
-.PHONY: all cuda host py oracle clean
-all: cuda host py oracle
+.PHONY: all cuda host py tools oracle clean
+all: cuda host py tools oracle
 
 cuda: $(LIB_CUDA)
 host: $(LIB_HOST)
 py: $(PYMOD)
+tools: $(BENCHCLI)
 
 build/%.o: $(CSRC)/%.cu $(CU_HDRS)
 	@mkdir -p build
@@ -52,8 +55,13 @@ $(PYMOD): $(CSRC)/py_module.cpp $(HOST_HDRS) $(LIB_HOST)
 	$(CXX) -std=c++20 -O2 -fPIC -shared -Iinclude -I$(PYINC) -I$(PYBIND) -I$(CUDA_INC) \
 	  -o $@ $(CSRC)/py_module.cpp -L$(PKG) -lmoeinfer_b200 -lmoe_cuda -Wl,-rpath,'$$ORIGIN'
 
+# the reference CLI's `moe bench` over a .moec checkpoint's MoE blocks
+$(BENCHCLI): $(CSRC)/tools/moe_bench.cpp include/moe_cuda.h $(LIB_CUDA)
+	$(CXX) -std=c++17 -O2 -Iinclude -I$(CUDA_INC) -o $@ $(CSRC)/tools/moe_bench.cpp \
+	  -L$(PKG) -lmoe_cuda -L$(CUDA_HOME)/lib64 -lcudart -Wl,-rpath,'$$ORIGIN' -Wl,-rpath,$(CUDA_HOME)/lib64
+
 oracle:
 	$(MAKE) -C oracle
 
 clean:
-	rm -rf build $(LIB_CUDA) $(LIB_HOST) $(PYMOD)
+	rm -rf build $(LIB_CUDA) $(LIB_HOST) $(PYMOD) $(BENCHCLI)

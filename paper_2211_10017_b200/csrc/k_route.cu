@@ -516,7 +516,9 @@ int launch_plan_from_counts(const uint32_t* expert, const uint8_t* finished, int
   if (S == 0) return MOE_OK;
   if (E + 1 > 1024) return set_error(MOE_EINVAL, "routing plan: at most 1023 experts");
   const int64_t nblk = (S + spb - 1) / spb;
-  if ((E + 1) * nblk <= kFusedScanMax && (cols % 8) == 0 && spb <= 1024) {
+  static const int64_t fused_max =
+      std::getenv("MOE_PLAN_FUSED_MAX") ? std::atoll(std::getenv("MOE_PLAN_FUSED_MAX")) : kFusedScanMax;
+  if ((E + 1) * nblk <= fused_max && (cols % 8) == 0 && spb <= 1024) {
     const int threads = (int)std::max<int64_t>(kPlaceThreads, (spb + 31) / 32 * 32);
     // tot | base | wcnt[warps] | pos | staged histogram [(E+1) x nblk]
     const size_t smem0 = ((E + 1) * 2 + 1 + (threads / 32) * (E + 1) + threads +
