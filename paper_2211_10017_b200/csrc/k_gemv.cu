@@ -124,6 +124,7 @@ struct Params {
                           // the programmatic-dependent-launch wait (only x is the previous
                           // kernel's output)
   long long* trace;       // dev-only (MOE_GEMV_TRACE): per CTA [start, prologue, items, k-loop ns, x-stage ns, epi ns, end]
+  int chunked;            // item blocks of ceil(items / grid) (spare CTAs exit)
 };
 
 // Both GEMMs of the FFN pair in one persistent launch (decode): FFN1 items
@@ -287,13 +288,27 @@ __device__ __forceinline__ void mma_pass(const Phase& ph, const Item& it, int64_
 #pragma unroll
       for (int q = 0; q < 4; ++q) acc[j][c][q] = 0.f;
   const uint16_t* xk0 = xs + 16 * t + g * kp;
+  // int4: the lane's fragment words sit at a fixed offset in every stage
+  // (chunk t/2, half t%2, features fg and fg+8): shared-window addresses
+  // computed once, so the loop body is waits, two 8-byte loads, dequant
+  // and MMAs (no per-iteration address rebuild)
+  const uint32_t ring_s = smem_u32(ring) + (uint32_t)((t >> 1) * 2048 + (t & 1) * 8 + fg * 16);
+  const uint32_t full_s = smem_u32(full);
   auto kloop = [&](auto ntile_c) {
     constexpr int NTL = decltype(ntile_c)::value;
     const uint16_t* xk = xk0;
     for (int kbl = 0; kbl < nkbl; ++kbl, xk += 64) {
-      mbar_wait_warp(&full[s], phs);
       uint32_t w[F::NW];
-      frag_from_smem<BITS>(ring + s * RG::WB, fg, t, w);
+      if constexpr (BITS == 4) {
+        while (!mbar_try_wait(full_s + 8u * (uint32_t)s, phs)) {
+        }
+        const uint32_t a = ring_s + (uint32_t)s * (uint32_t)RG::WB;
+        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(w[0]), "=r"(w[1]) : "r"(a));
+        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(w[2]), "=r"(w[3]) : "r"(a + 128u));
+      } else {
+        mbar_wait_warp(&full[s], phs);
+        frag_from_smem<BITS>(ring + s * RG::WB, fg, t, w);
+      }
       uint32_t lo[8], hi[8];
       dequant_fast<BITS>(w, db2, hb2, lo, hi);
 #pragma unroll
@@ -401,8 +416,8 @@ __device__ __forceinline__ bool finish_item(const Phase& ph, const Item& it, int
 // through the ring (it never drains between items); the compute warps stage
 // only the live rows of each item (the MMA's unused B rows only feed
 // discarded columns).
-template <int BITS>
-__global__ void __launch_bounds__(kThreads, 3) gemv_kernel(const Params P) {
+template <int BITS, int MINB = 3>
+__global__ void __launch_bounds__(kThreads, MINB) gemv_kernel(const Params P) {
   using RG = Ring<BITS>;
   extern __shared__ __align__(1024) uint8_t gsm[];
   uint8_t* ring = gsm;                                            // [NST][WB]
@@ -434,8 +449,19 @@ __global__ void __launch_bounds__(kThreads, 3) gemv_kernel(const Params P) {
   __syncthreads();
   const int nitems = s_nlive * P.ph.nsplit * P.ph.nft;
   const long long t_pro = tr ? gv_time() : 0;
-  const int i0 = (int)((int64_t)blockIdx.x * nitems / gridDim.x);  // balanced blocks
-  const int i1 = (int)((int64_t)(blockIdx.x + 1) * nitems / gridDim.x);
+  // contiguous blocks of `per` items (MOE_GEMV_CHUNKED, dev A/B): when the
+  // live items just exceed a multiple of the grid, the spare CTAs exit and
+  // the busy ones share their SMs with fewer neighbours, instead of two or
+  // three CTAs running one extra item alone at the end
+  int i0, i1;
+  if (P.chunked) {
+    const int per = (nitems + (int)gridDim.x - 1) / (int)gridDim.x;
+    i0 = ::min(nitems, (int)blockIdx.x * per);
+    i1 = ::min(nitems, i0 + per);
+  } else {
+    i0 = (int)((int64_t)blockIdx.x * nitems / gridDim.x);  // balanced blocks
+    i1 = (int)((int64_t)(blockIdx.x + 1) * nitems / gridDim.x);
+  }
   int s = 0, n = 0;
   uint32_t phs = 0;
   if (warp == kWarps) {
@@ -875,10 +901,17 @@ static int run_gemv(const GemmArgs& a, const GemvWork& w, cudaStream_t st) {
   // 86.7 us per layer with it, 82.3 without); MOE_PDL=5 opts in (early
   // prologue: weights stream before the wait, only x waits)
   P.early = a.second && pdl_enabled(4) ? 1 : 0;
+  static const int chunked = std::getenv("MOE_GEMV_CHUNKED") ? std::atoi(std::getenv("MOE_GEMV_CHUNKED")) : 0;
+  P.chunked = chunked;
   const size_t smem = gemv_smem(a.m, w.nsplit, BITS);
+  static const int per_sm = std::getenv("MOE_GEMV_CTAS") ? std::atoi(std::getenv("MOE_GEMV_CTAS")) : 3;
+  // MOE_GEMV_CTAS=2: the 2-CTA/SM instantiation (register cap 113 instead of 72)
+  auto kern = per_sm == 2 ? gv::gemv_kernel<BITS, 2> : gv::gemv_kernel<BITS, 3>;
   static size_t attr = 0;
   if (smem > 48 * 1024 && smem > attr) {
-    MOE_CUDA_TRY(cudaFuncSetAttribute(gv::gemv_kernel<BITS>,
+    MOE_CUDA_TRY(cudaFuncSetAttribute(gv::gemv_kernel<BITS, 2>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    MOE_CUDA_TRY(cudaFuncSetAttribute(gv::gemv_kernel<BITS, 3>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = smem;
   }
@@ -888,7 +921,6 @@ static int run_gemv(const GemmArgs& a, const GemvWork& w, cudaStream_t st) {
   // grid for those -- at T = 1 a grid for all E problems launched ~3x more
   // CTAs than there were items, each paying the prologue
   const int64_t live = std::max<int64_t>(1, std::min<int64_t>(a.np, a.rows));
-  static const int per_sm = std::getenv("MOE_GEMV_CTAS") ? std::atoi(std::getenv("MOE_GEMV_CTAS")) : 3;
   const int64_t grid = std::max<int64_t>(
       1, std::min<int64_t>(live * P.ph.nft * P.ph.nsplit, per_sm * (int64_t)sm_count()));
   static long long* dtrace = nullptr;
@@ -896,8 +928,7 @@ static int run_gemv(const GemmArgs& a, const GemvWork& w, cudaStream_t st) {
   if (tr && !dtrace) MOE_CUDA_TRY(cudaMalloc(&dtrace, 8 * 8 * 4096));
   P.trace = tr ? dtrace : nullptr;
   if (tr) MOE_CUDA_TRY(cudaMemsetAsync(dtrace, 0, 8 * 8 * grid, st));
-  MOE_CUDA_TRY(launch_k(4, gv::gemv_kernel<BITS>, dim3((unsigned)grid), dim3(gv::kThreads), smem,
-                        st, P));
+  MOE_CUDA_TRY(launch_k(4, kern, dim3((unsigned)grid), dim3(gv::kThreads), smem, st, P));
   note_launch();
   if (tr) {  // dev instrumentation: per-CTA phase times (ns)
     std::vector<long long> h(8 * grid);
