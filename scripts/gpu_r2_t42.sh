@@ -1,0 +1,3 @@
+for c in 1 2 3 4 8; do MOE_HOST_CHUNKS=$c timeout 300 python scripts/e2e_probe.py 512 2048 8 4096 2 2>&1 | tail -1; done
+for c in 1 2 4; do MOE_HOST_CHUNKS=$c timeout 300 python scripts/e2e_probe.py 1024 4096 64 16384 1 2>&1 | tail -1; done
+timeout 900 python -m pytest tests/test_gpu_layer.py tests/test_gpu_dropin.py -q -x -k "host or pinned or chunk" 2>&1 | tail -2
