@@ -333,6 +333,18 @@ int moe_moec_info(const moe_moec* m, uint32_t* cfg9, int* precision, int* n_moe_
 int moe_moec_block(const moe_moec* m, int i, moe_layer** layer, char* name, size_t name_len);
 int moe_moec_destroy(moe_moec* m);
 
+/* ---- encoder_forward on the device (new; csrc/encoder.cu) ----
+ * proj/src/model.cpp:351-398 over a checkpoint loaded with create_layers:
+ * embeddings, every encoder layer (attention: LN, Q/K/V/O projections,
+ * per-sentence softmax attention; then the MoE block or the dense FFN),
+ * final LayerNorm.  tokens: HOST int32 [batch][len] (the reference's range
+ * checks and messages); out: device (batch * len, d_model) fp16.  EXACT
+ * mode is bit-identical to encoder_forward; FAST runs the projections and
+ * experts on the tensor cores (layer tolerance).  Synchronises once (token
+ * range check). */
+int moe_encoder_forward(moe_moec* m, const int32_t* tokens, int64_t batch, int64_t len, int mode,
+                        uint16_t* out, moe_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

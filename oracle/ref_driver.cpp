@@ -477,4 +477,18 @@ int ref_moec_block_forward(const char* path, int block, const uint16_t* x, size_
   });
 }
 
+// encoder_forward (model.cpp:351-398) of a loaded .moec over `batch`
+// sentences of `len` token ids: embeddings, every encoder layer (attention,
+// then the MoE or dense FFN), final LayerNorm -> out (batch * len, d).
+int ref_encoder_forward(const char* path, const int32_t* tokens, size_t batch, size_t len,
+                        uint16_t* out) {
+  return guarded([&] {
+    const Model m = load_model(path);
+    std::vector<std::vector<int32_t>> src(batch, std::vector<int32_t>(len));
+    for (size_t s = 0; s < batch; ++s)
+      for (size_t p = 0; p < len; ++p) src[s][p] = tokens[s * len + p];
+    out_mat(encoder_forward(m, src, nullptr, 1), out);
+  });
+}
+
 }  // extern "C"

@@ -1,0 +1,220 @@
+// encoder.cu -- encoder_forward (proj/src/model.cpp:351-398) of a .moec
+// checkpoint on the GPU.  Per encoder layer:
+//   attention_forward (model.cpp:207-256): LN -> Q, K, V = gemm_f16 ->
+//     per (sentence, head) attend_one (attn_inner.hpp:20-50) -> O = gemm_f16
+//     -> x + O (half_add);
+//   then the layer's FFN: the MoE block (layer_forward, top-1, no finished
+//   rows: model.cpp:387) or dense_ffn_forward (model.cpp:258-271: LN ->
+//   gemm_f16 ReLU -> gemm_f16 -> half_add);
+// then the final LayerNorm.  EXACT mode is bit-identical to the reference:
+// LayerNorm and the gemm_f16 panels run the reference's serial f32 chains
+// (k_gate.cu, k_gemm_exact.cu), attend_one's chains are restated below in
+// the same order (f32 products and sums RN, glibc expf port, p = s_j / sum
+// per element), half_add is fp16 RN.  FAST mode runs the projections and the
+// MoE experts on the tcgen05 path (within the layer tolerance).
+#include <cmath>
+#include <cstring>
+
+#include "encoder.cuh"
+#include "glibc_expf.h"
+
+namespace moecu {
+
+EncoderDev::~EncoderDev() {
+  for (void* p : allocs) cudaFree(p);
+  for (void* p : {(void*)x, (void*)x2, (void*)xn, (void*)q, (void*)k, (void*)v, (void*)ctx,
+                  (void*)o, (void*)h, (void*)tokens, (void*)problem, (void*)bad})
+    if (p) cudaFree(p);
+}
+
+int enc_upload(EncoderDev* E, const uint16_t* host, int64_t count, uint16_t** out) {
+  MOE_CUDA_TRY(cudaMalloc(out, count * 2));
+  E->allocs.push_back(*out);
+  MOE_CUDA_TRY(cudaMemcpy(*out, host, count * 2, cudaMemcpyHostToDevice));
+  return MOE_OK;
+}
+
+int enc_linear(EncoderDev* E, const uint16_t* w, const uint16_t* b, int64_t m, int64_t n,
+               DevLinear* out) {
+  out->m = m;
+  out->n = n;
+  uint16_t* tmp = nullptr;
+  MOE_CUDA_TRY(cudaMalloc(&tmp, m * n * 2));
+  MOE_CUDA_TRY(cudaMemcpy(tmp, w, m * n * 2, cudaMemcpyHostToDevice));
+  MOE_CUDA_TRY(cudaMalloc(&out->tiled, tiled_bytes(1, m, n, 16)));
+  E->allocs.push_back(out->tiled);
+  const int st = launch_tile_weights(tmp, 1, m, n, 16, out->tiled, nullptr);
+  MOE_CUDA_TRY(cudaDeviceSynchronize());
+  cudaFree(tmp);
+  TRY(st);
+  return enc_upload(E, b, n, &out->bias);
+}
+
+namespace {
+
+__device__ __forceinline__ uint16_t hadd(uint16_t a, uint16_t b) {
+  return __half_as_ushort(__hadd_rn(__ushort_as_half(a), __ushort_as_half(b)));
+}
+
+// x[s * len + p] = tok_embed[src[s][p]] (+) pos_embed[p]   (model.cpp:373-382)
+__global__ void embed_kernel(const int32_t* __restrict__ tok, int64_t t, int64_t len, int64_t d,
+                             const uint16_t* __restrict__ te, const uint16_t* __restrict__ pe,
+                             int64_t vocab, uint16_t* __restrict__ x, uint32_t* bad) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < t * d;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / d, c = i - r * d;
+    const int32_t id = tok[r];
+    if (id < 0 || id >= vocab) {
+      atomicMin(bad, (uint32_t)r);
+      x[i] = 0;
+      continue;
+    }
+    x[i] = hadd(te[(int64_t)id * d + c], pe[(r % len) * d + c]);
+  }
+}
+
+// out = a (+) b, fp16 RN (the residuals: model.cpp:252-254, 267-269)
+__global__ void add_kernel(const uint16_t* __restrict__ a, const uint16_t* __restrict__ b,
+                           int64_t n, uint16_t* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = hadd(a[i], b[i]);
+}
+
+// attend_one (attn_inner.hpp:20-50) for every query row of one sentence and
+// one head: CTA (sentence, head), a thread per query row; the head's K and V
+// slices of the sentence and the expf table in shared memory, the row's
+// scores in shared memory.  Every chain in the reference's order.
+__global__ void attention_kernel(const uint16_t* __restrict__ q, const uint16_t* __restrict__ k,
+                                 const uint16_t* __restrict__ v, int64_t len, int64_t d, int dk,
+                                 float inv_sqrt_dk, uint16_t* __restrict__ ctx) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  uint64_t* tab = reinterpret_cast<uint64_t*>(sm);
+  uint16_t* ks = reinterpret_cast<uint16_t*>(sm + 32 * 8);
+  uint16_t* vs = ks + len * dk;
+  float* sc = reinterpret_cast<float*>(vs + len * dk + ((len * dk) & 1));  // [blockDim][len]
+  const int64_t s0 = (int64_t)blockIdx.x * len;  // first row of the sentence
+  const int h0 = blockIdx.y * dk;
+  for (int i = threadIdx.x; i < 32; i += blockDim.x) tab[i] = moe_expf_tab_dev[i];
+  for (int64_t i = threadIdx.x; i < len * dk; i += blockDim.x) {
+    const int64_t j = i / dk, c = i - j * dk;
+    ks[i] = k[(s0 + j) * d + h0 + c];
+    vs[i] = v[(s0 + j) * d + h0 + c];
+  }
+  __syncthreads();
+  float* s = sc + (int64_t)threadIdx.x * len;
+  for (int64_t r = threadIdx.x; r < len; r += blockDim.x) {
+    const uint16_t* qr = q + (s0 + r) * d + h0;
+    for (int64_t j = 0; j < len; ++j) {
+      const uint16_t* kr = ks + j * dk;
+      float a = 0.0f;
+      for (int c = 0; c < dk; ++c) a = __fadd_rn(a, __fmul_rn(h2f(qr[c]), h2f(kr[c])));
+      s[j] = __fmul_rn(a, inv_sqrt_dk);
+    }
+    float mx = s[0];
+    for (int64_t j = 1; j < len; ++j) mx = fmaxf(mx, s[j]);
+    float sum = 0.0f;
+    for (int64_t j = 0; j < len; ++j) {
+      s[j] = moe_glibc_expf_t(__fsub_rn(s[j], mx), tab);
+      sum = __fadd_rn(sum, s[j]);
+    }
+    for (int c = 0; c < dk; ++c) {
+      float acc = 0.0f;
+      for (int64_t j = 0; j < len; ++j)
+        acc = __fadd_rn(acc, __fmul_rn(__fdiv_rn(s[j], sum), h2f(vs[j * dk + c])));
+      ctx[(s0 + r) * d + h0 + c] = f2h(acc);
+    }
+  }
+}
+
+int gemm(EncoderDev* E, const uint16_t* x, int64_t t, const DevLinear& w, int relu, int mode,
+         uint16_t* out, cudaStream_t st) {
+  GemmArgs g{x, t, w.m, E->problem, 1, w.tiled, nullptr, 16, 1, w.n, w.bias, relu, out,
+             0, t};
+  return mode == MOE_MODE_EXACT ? launch_gemm_exact(g, st) : launch_gemm_tc(g, st);
+}
+
+int blocks_for(int64_t n) { return (int)std::min<int64_t>((n + 255) / 256, 148 * 8); }
+
+}  // namespace
+}  // namespace moecu
+
+using namespace moecu;
+
+struct moe_moec;
+namespace moecu {
+EncoderDev* moec_encoder(moe_moec* M);
+moe_layer* moec_layer(moe_moec* M, int i);
+}  // namespace moecu
+
+extern "C" int moe_encoder_forward(moe_moec* M, const int32_t* tokens, int64_t batch, int64_t len,
+                                   int mode, uint16_t* out, moe_stream_t stream) {
+  if (!M) return set_error(MOE_EINVAL, "encoder: null argument");
+  // encoder_forward's checks first (model.cpp:354-366)
+  if (batch <= 0 || !tokens) return set_error(MOE_EINVAL, "encoder: empty batch");
+  if (!out) return set_error(MOE_EINVAL, "encoder: null argument");
+  EncoderDev* E = moec_encoder(M);
+  if (!E) return set_error(MOE_EINVAL, "encoder: checkpoint was loaded without device layers");
+  if (mode != MOE_MODE_EXACT && mode != MOE_MODE_FAST) return set_error(MOE_EINVAL, "encoder: bad mode");
+  if (len < 1 || len > E->maxlen) return set_error(MOE_EINVAL, "encoder: source length out of range");
+  const int64_t t = batch * len, d = E->d;
+  if (len > 256) return set_error(MOE_EINVAL, "encoder: sentences longer than 256 tokens");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (t > E->cap_t) {
+    for (void* p : {(void*)E->x, (void*)E->x2, (void*)E->xn, (void*)E->q, (void*)E->k, (void*)E->v,
+                    (void*)E->ctx, (void*)E->o, (void*)E->h, (void*)E->tokens})
+      if (p) cudaFree(p);
+    for (uint16_t** p : {&E->x, &E->x2, &E->xn, &E->q, &E->k, &E->v, &E->ctx, &E->o})
+      MOE_CUDA_TRY(cudaMalloc(p, t * d * 2));
+    MOE_CUDA_TRY(cudaMalloc(&E->h, t * E->f * 2));
+    MOE_CUDA_TRY(cudaMalloc(&E->tokens, t * 4));
+    E->cap_t = t;
+  }
+  if (!E->problem) {
+    MOE_CUDA_TRY(cudaMalloc(&E->problem, 3 * 4));
+    MOE_CUDA_TRY(cudaMalloc(&E->bad, 4));
+  }
+  const uint32_t prob[3] = {0u, 0u, (uint32_t)t};
+  MOE_CUDA_TRY(cudaMemcpyAsync(E->problem, prob, 12, cudaMemcpyHostToDevice, st));
+  MOE_CUDA_TRY(cudaMemcpyAsync(E->tokens, tokens, t * 4, cudaMemcpyHostToDevice, st));
+  MOE_CUDA_TRY(cudaMemsetAsync(E->bad, 0xFF, 4, st));
+  embed_kernel<<<blocks_for(t * d), 256, 0, st>>>(E->tokens, t, len, d, E->tok, E->pos, E->vocab,
+                                                  E->x, E->bad);
+  uint32_t bad = 0;
+  MOE_CUDA_TRY(cudaMemcpyAsync(&bad, E->bad, 4, cudaMemcpyDeviceToHost, st));
+  MOE_CUDA_TRY(cudaStreamSynchronize(st));
+  if (bad != 0xFFFFFFFFu) return set_error(MOE_EINVAL, "encoder: token id out of range");
+  const int dk = (int)(d / E->heads);
+  const float inv_sqrt_dk = 1.0f / std::sqrt((float)dk);
+  const size_t att_smem = 32 * 8 + (size_t)2 * len * dk * 2 + 4 + (size_t)128 * len * 4;
+  if (att_smem > 48 * 1024)
+    MOE_CUDA_TRY(cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)att_smem));
+  uint16_t* x = E->x;
+  uint16_t* y = E->x2;
+  for (const EncLayerDev& l : E->layers) {
+    // attention_forward (model.cpp:207-256)
+    TRY(launch_layer_norm(x, t, d, l.ln_g, l.ln_b, E->xn, st));
+    TRY(gemm(E, E->xn, t, l.q, 0, mode, E->q, st));
+    TRY(gemm(E, E->xn, t, l.k, 0, mode, E->k, st));
+    TRY(gemm(E, E->xn, t, l.v, 0, mode, E->v, st));
+    attention_kernel<<<dim3((unsigned)batch, (unsigned)E->heads), 128, att_smem, st>>>(
+        E->q, E->k, E->v, len, d, dk, inv_sqrt_dk, E->ctx);
+    TRY(check_launch("encoder attention"));
+    TRY(gemm(E, E->ctx, t, l.o, 0, mode, E->o, st));
+    add_kernel<<<blocks_for(t * d), 256, 0, st>>>(x, E->o, t * d, y);
+    std::swap(x, y);
+    // the FFN: MoE block (moe_ffn_forward, no finished rows) or dense
+    if (l.moe_block >= 0) {
+      TRY(layer_forward(moec_layer(M, l.moe_block), x, nullptr, t, 1, mode, y, st));
+    } else {
+      TRY(launch_layer_norm(x, t, d, l.fln_g, l.fln_b, E->xn, st));
+      TRY(gemm(E, E->xn, t, l.w1, 1, mode, E->h, st));
+      TRY(gemm(E, E->h, t, l.w2, 0, mode, E->o, st));
+      add_kernel<<<blocks_for(t * d), 256, 0, st>>>(x, E->o, t * d, y);
+    }
+    std::swap(x, y);
+  }
+  TRY(launch_layer_norm(x, t, d, E->ln_g, E->ln_b, out, st));
+  return check_launch("encoder");
+}

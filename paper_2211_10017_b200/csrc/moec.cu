@@ -21,7 +21,7 @@
 #include <string>
 #include <vector>
 
-#include "layer.cuh"
+#include "encoder.cuh"
 
 namespace {
 
@@ -92,10 +92,17 @@ struct moe_moec {
   int precision = 0;
   std::vector<std::string> names;
   std::vector<moe_layer*> layers;
+  std::unique_ptr<moecu::EncoderDev> enc;  // attention / dense-FFN weights (create_layers)
   ~moe_moec() {
+    enc.reset();
     for (moe_layer* L : layers) moe_layer_destroy(L);
   }
 };
+
+namespace moecu {
+EncoderDev* moec_encoder(moe_moec* M) { return M->enc.get(); }
+moe_layer* moec_layer(moe_moec* M, int i) { return M->layers[i]; }
+}  // namespace moecu
 
 using namespace moecu;
 
@@ -132,14 +139,25 @@ int walk(const std::vector<uint8_t>& bytes, moe_moec* M, bool create) {
     const uint32_t n_records = (uint32_t)r.uint(4);
     const uint64_t d = c.d, f = c.f, E = c.E;
     uint64_t count = 0;
-    auto attn = [&](const std::string& p) {
-      r.f16(p + ".ln_g", {d});
-      r.f16(p + ".ln_b", {d});
+    // attention records; encoder layers' go to the device (encoder_forward)
+    auto attn = [&](const std::string& p, EncLayerDev* dev) -> int {
+      const uint16_t* g = r.f16(p + ".ln_g", {d});
+      const uint16_t* b = r.f16(p + ".ln_b", {d});
+      DevLinear* lin[4] = {dev ? &dev->q : nullptr, dev ? &dev->k : nullptr, dev ? &dev->v : nullptr,
+                           dev ? &dev->o : nullptr};
+      int i = 0;
       for (const char* w : {"q", "k", "v", "o"}) {
-        r.f16(p + ".w" + w, {d, d});
-        r.f16(p + ".b" + w, {d});
+        const uint16_t* wp = r.f16(p + ".w" + w, {d, d});
+        const uint16_t* bp = r.f16(p + ".b" + w, {d});
+        if (dev) TRY(enc_linear(M->enc.get(), wp, bp, (int64_t)d, (int64_t)d, lin[i]));
+        ++i;
+      }
+      if (dev) {
+        TRY(enc_upload(M->enc.get(), g, (int64_t)d, &dev->ln_g));
+        TRY(enc_upload(M->enc.get(), b, (int64_t)d, &dev->ln_b));
       }
       count += 10;
+      return MOE_OK;
     };
     auto quant = [&](const std::string& name, uint64_t m, uint64_t n, const uint8_t** packed,
                      const uint16_t** scales) {
@@ -148,17 +166,24 @@ int walk(const std::vector<uint8_t>& bytes, moe_moec* M, bool create) {
       if (r.uint(8) != E * n) throw Fail{"record '" + name + "' has wrong scale count"};
       *scales = reinterpret_cast<const uint16_t*>(r.take(E * n * 2));
     };
-    auto ffn = [&](const std::string& p, uint32_t idx) -> int {
+    auto ffn = [&](const std::string& p, uint32_t idx, EncLayerDev* dev) -> int {
       if (idx % c.every != 0) {  // dense FFN block
-        r.f16(p + ".ln_g", {d});
-        r.f16(p + ".ln_b", {d});
-        r.f16(p + ".w1", {d, f});
-        r.f16(p + ".b1", {f});
-        r.f16(p + ".w2", {f, d});
-        r.f16(p + ".b2", {d});
+        const uint16_t* g = r.f16(p + ".ln_g", {d});
+        const uint16_t* b = r.f16(p + ".ln_b", {d});
+        const uint16_t* w1 = r.f16(p + ".w1", {d, f});
+        const uint16_t* b1 = r.f16(p + ".b1", {f});
+        const uint16_t* w2 = r.f16(p + ".w2", {f, d});
+        const uint16_t* b2 = r.f16(p + ".b2", {d});
+        if (dev) {
+          TRY(enc_upload(M->enc.get(), g, (int64_t)d, &dev->fln_g));
+          TRY(enc_upload(M->enc.get(), b, (int64_t)d, &dev->fln_b));
+          TRY(enc_linear(M->enc.get(), w1, b1, (int64_t)d, (int64_t)f, &dev->w1));
+          TRY(enc_linear(M->enc.get(), w2, b2, (int64_t)f, (int64_t)d, &dev->w2));
+        }
         count += 6;
         return MOE_OK;
       }
+      if (dev) dev->moe_block = (int)M->names.size();
       moe_layer_desc D{};
       D.d = (int64_t)d;
       D.f = (int64_t)f;
@@ -187,21 +212,38 @@ int walk(const std::vector<uint8_t>& bytes, moe_moec* M, bool create) {
       }
       return MOE_OK;
     };
-    r.f16("tok_embed", {c.vocab, d});
-    r.f16("pos_embed", {c.maxlen, d});
+    const uint16_t* tok = r.f16("tok_embed", {c.vocab, d});
+    const uint16_t* pos = r.f16("pos_embed", {c.maxlen, d});
     count += 2;
+    if (create) {
+      M->enc = std::make_unique<EncoderDev>();
+      EncoderDev* E = M->enc.get();
+      E->d = d;
+      E->f = f;
+      E->heads = c.heads;
+      E->vocab = c.vocab;
+      E->maxlen = c.maxlen;
+      E->layers.resize(c.nenc);
+      TRY(enc_upload(E, tok, (int64_t)c.vocab * d, &E->tok));
+      TRY(enc_upload(E, pos, (int64_t)c.maxlen * d, &E->pos));
+    }
     for (uint32_t i = 0; i < c.nenc; ++i) {
       const std::string p = "enc." + std::to_string(i);
-      attn(p + ".attn");
-      TRY(ffn(p + ".ffn", i));
+      EncLayerDev* dev = create ? &M->enc->layers[i] : nullptr;
+      TRY(attn(p + ".attn", dev));
+      TRY(ffn(p + ".ffn", i, dev));
     }
     for (uint32_t i = 0; i < c.ndec; ++i) {
       const std::string p = "dec." + std::to_string(i);
-      attn(p + ".self");
-      attn(p + ".cross");
-      TRY(ffn(p + ".ffn", i));
+      TRY(attn(p + ".self", nullptr));
+      TRY(attn(p + ".cross", nullptr));
+      TRY(ffn(p + ".ffn", i, nullptr));
     }
-    for (const char* nm : {"enc_ln_g", "enc_ln_b", "dec_ln_g", "dec_ln_b"}) r.f16(nm, {d});
+    for (const char* nm : {"enc_ln_g", "enc_ln_b", "dec_ln_g", "dec_ln_b"}) {
+      const uint16_t* v = r.f16(nm, {d});
+      if (create && std::strcmp(nm, "enc_ln_g") == 0) TRY(enc_upload(M->enc.get(), v, (int64_t)d, &M->enc->ln_g));
+      if (create && std::strcmp(nm, "enc_ln_b") == 0) TRY(enc_upload(M->enc.get(), v, (int64_t)d, &M->enc->ln_b));
+    }
     r.f16("out_w", {d, c.vocab});
     r.f16("out_b", {c.vocab});
     count += 6;

@@ -62,3 +62,20 @@ class MoecModel:
             except Exception:
                 pass
             self._h = None
+
+    def encoder_forward(self, tokens, mode: int = 1, stream=None):
+        """encoder_forward (proj/src/model.cpp:351-398) on the device:
+        tokens int32 [batch, len] (host) -> fp16 (batch * len, d_model)
+        torch tensor on the current device.  mode 0 EXACT (bit-identical to
+        the reference), 1 FAST."""
+        import torch
+        from .ops import _stream
+        tok = np.ascontiguousarray(tokens, dtype=np.int32)
+        if tok.ndim != 2:
+            raise ValueError("encoder: tokens must be [batch, len]")
+        batch, length = tok.shape
+        out = torch.empty((batch * length, self.config["d_model"]), dtype=torch.float16,
+                          device="cuda")
+        abi.call("moe_encoder_forward", self._h, C.c_void_p(tok.ctypes.data), batch, length, mode,
+                 C.c_void_p(out.data_ptr()), _stream(stream))
+        return out

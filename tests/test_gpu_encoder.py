@@ -1,0 +1,50 @@
+"""encoder_forward on the device (csrc/encoder.cu) against
+the UNMODIFIED reference's encoder_forward (proj/src/model.cpp:351-398) over
+the committed checkpoints (tests/golden/make_encoder_golden.py): EXACT mode
+bit for bit, FAST mode within the layer tolerance."""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import bits16
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+GOLD = os.path.join(HERE, "golden")
+TOL_FAST = 1e-2
+
+
+def _vectors():
+    return np.load(os.path.join(GOLD, "encoder_vectors.npz"))
+
+
+@pytest.mark.parametrize("name", ["model_int4", "model_f16"])
+@pytest.mark.parametrize("case", [0, 1, 2, 3])
+def test_encoder_matches_reference(cuda, name, case):
+    from paper_2211_10017_b200.moec import MoecModel
+    v = _vectors()
+    tok, want = v[f"{name}_{case}_tok"], v[f"{name}_{case}_out"]
+    m = MoecModel(os.path.join(GOLD, name + ".moec"))
+    exact = m.encoder_forward(tok, mode=0).cpu().numpy().view(np.uint16)
+    assert np.array_equal(exact, want), int((exact != want).sum())
+    fast = m.encoder_forward(tok, mode=1).cpu().numpy().astype(np.float64)
+    w = want.view(np.float16).astype(np.float64)
+    err = np.abs(fast - w).max() / max(np.abs(w).max(), 1e-30)
+    assert err <= TOL_FAST, err
+
+
+def test_encoder_errors(cuda):
+    from paper_2211_10017_b200.moec import MoecModel
+    m = MoecModel(os.path.join(GOLD, "model_int4.moec"))
+    with pytest.raises(ValueError, match="token id out of range"):
+        m.encoder_forward(np.full((2, 3), 16, np.int32))
+    with pytest.raises(ValueError, match="source length out of range"):
+        m.encoder_forward(np.zeros((2, 9), np.int32))  # max_seq_len = 8
+    with pytest.raises(ValueError, match="empty batch"):
+        m.encoder_forward(np.zeros((0, 3), np.int32))
+    # the same checkpoint without device layers has no encoder
+    m2 = MoecModel(os.path.join(GOLD, "model_int4.moec"), create_layers=False)
+    with pytest.raises(ValueError, match="without device layers"):
+        m2.encoder_forward(np.zeros((1, 3), np.int32))
