@@ -54,6 +54,12 @@ WORKLOADS = {
     # §3: 18 MoE blocks of the 24-enc / 12-dec model, MoE every other layer)
     "c4_stack": (64, 1024, 4096, 16384, 1, "C4 prefill, MoE layers only: 18 chained MoE blocks "
                  "(E=64 d_model=1024 d_ff=4096 int4 top-1) over 16384 tokens"),
+    # C4's whole encoder at prefill: 24 layers of attention
+    # + FFN (12 MoE, 12 dense), batch 128 x 128 tokens, from a synthetic
+    # checkpoint in the reference's format
+    "c4_encoder": (64, 1024, 4096, 16384, 1, "C4 prefill, whole encoder: 24 layers (16-head "
+                   "attention, 12 MoE E=64 int4 top-1 + 12 dense FFN, d_model=1024 d_ff=4096), "
+                   "128 sentences x 128 tokens"),
     # decode with batch pruning: C4's decoder MoE blocks
     "decode_prune": (64, 1024, 4096, 256, 1, "beam-search decode MoE blocks with batch pruning: "
                      "C4 decoder (6 MoE blocks of E=64 d_model=1024 d_ff=4096 int4, top-1), "
@@ -494,6 +500,72 @@ def run_decode(args, wl):
     print(json.dumps(line), flush=True)
 
 
+def run_encoder(args, wl):
+    """C4's encoder prefill end to end on the device (encoder_forward,
+    proj/src/model.cpp:351-398; csrc/encoder.cu): embeddings, 24 x
+    (attention + FFN), final LN, FAST mode, over 128 sentences x 128 tokens.
+    Weights: a synthetic checkpoint in the reference's .moec format
+    (moe_moec_write_synthetic) loaded through the reference-format loader.
+    Each step is one encoder_forward (its token-range check synchronises
+    once); value = tokens per second."""
+    import ctypes as C
+    import tempfile
+    import numpy as np
+    import torch
+    from paper_2211_10017_b200 import abi
+    from paper_2211_10017_b200.moec import MoecModel
+    E, d, f, T, k, label = wl
+    nenc, heads, vocab, length = 24, 16, 8192, 128
+    batch = T // length
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    tmp = tempfile.mkdtemp(prefix="moec_")
+    path = os.path.join(tmp, "c4_encoder.moec")
+    cfg = (C.c_uint32 * 9)(d, f, nenc, 1, E, heads, vocab, 2, length)
+    abi.call("moe_moec_write_synthetic", path.encode(), cfg, 4, 2024)
+    m = MoecModel(path)
+    os.remove(path)
+    tok = np.random.default_rng(7).integers(0, vocab, (batch, length)).astype(np.int32)
+    for _ in range(args.warmup):
+        m.encoder_forward(tok, mode=1)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    n0 = abi.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            m.encoder_forward(tok, mode=1)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    launches = abi.launch_count() - n0
+    hbm, tc_burst, tc_sus, peak_src = load_peaks()
+    # FLOP of the step: per layer Q/K/V/O projections 4 * 2 T d^2, attention
+    # scores and context 2 * 2 T len d, FFN 2 * 2 T d f (dense or the top-1
+    # expert)
+    flops = nenc * (8.0 * T * d * d + 4.0 * T * length * d + 4.0 * T * d * f)
+    line = {
+        "metric": METRIC, "value": T / (ms * 1e-3), "unit": "tokens/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f16 (int4 weight-only experts, fp16 attention / dense weights, f32 accumulate)",
+        "data": "synthetic checkpoint (moe_moec_write_synthetic, reference .moec format), seeded tokens",
+        "config": {"workload": label, "E": E, "d_model": d, "d_ff": f, "n_enc_layers": nenc,
+                   "n_heads": heads, "batch": batch, "src_len": length, "tokens": T, "top_k": 1,
+                   "bits": 4, "mode": "fast (tcgen05 projections and experts)",
+                   "step": "one encoder_forward of 16384 tokens",
+                   "l2": f"weights {(12 * E * d * f + 12 * 2 * d * f * 4 + nenc * 4 * d * d * 2) / 2**20:.0f} MiB > L2"},
+        "roofline": {"bound": "tensor", "achieved": flops / (ms * 1e-3) / 1e12, "peak": tc_burst,
+                     "unit": "TFLOP/s", "frac": flops / (ms * 1e-3) / 1e12 / tc_burst,
+                     "traffic": None, "kernel": "whole encoder (layer-level FLOP / step time)",
+                     "peak_source": peak_src},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
 def run_stack(args, wl):
     """C4's MoE stack at prefill: 18 distinct MoE blocks chained (block l's
     output feeds block l+1; moe_decode_run with one step, no finished rows),
@@ -828,6 +900,8 @@ def main():
         run_decode(args, wl)
     elif args.workload == "c4_stack":
         run_stack(args, wl)
+    elif args.workload == "c4_encoder":
+        run_encoder(args, wl)
     else:
         run_native(args, wl)
 

@@ -342,6 +342,10 @@ int moe_moec_destroy(moe_moec* m);
  * mode is bit-identical to encoder_forward; FAST runs the projections and
  * experts on the tensor cores (layer tolerance).  Synchronises once (token
  * range check). */
+/* A synthetic .moec in the reference's format (random fp16 tensors, random
+ * int4/int8 codes with per-column scales) for benchmarks at model sizes no
+ * fixture covers (C4: 24 encoder layers, E = 64, d 1024 / 4096).  Host-only. */
+int moe_moec_write_synthetic(const char* path, const uint32_t* cfg9, int bits, uint64_t seed);
 int moe_encoder_forward(moe_moec* m, const int32_t* tokens, int64_t batch, int64_t len, int mode,
                         uint16_t* out, moe_stream_t stream);
 

@@ -79,6 +79,7 @@ _SIGS = {
     "moe_moec_block": (_int, [_vp, _int, _vp, _vp, _sz]),
     "moe_moec_destroy": (_int, [_vp]),
     "moe_encoder_forward": (_int, [_vp, _vp, _i64, _i64, _int, _vp, _vp]),
+    "moe_moec_write_synthetic": (_int, [C.c_char_p, _vp, _int, C.c_uint64]),
     "moe_decode_run": (_int, [_vp, _int, _vp, _vp, _int, _i64, _int, _int, _int, _vp, _vp, _vp]),
 }
 

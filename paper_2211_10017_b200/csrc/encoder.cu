@@ -82,47 +82,91 @@ __global__ void add_kernel(const uint16_t* __restrict__ a, const uint16_t* __res
 }
 
 // attend_one (attn_inner.hpp:20-50) for every query row of one sentence and
-// one head: CTA (sentence, head), a thread per query row; the head's K and V
-// slices of the sentence and the expf table in shared memory, the row's
-// scores in shared memory.  Every chain in the reference's order.
+// one head: CTA (sentence, head).  Every chain keeps the reference's order;
+// the chains themselves are independent, so they are spread over the
+// threads, four per thread in flight:
+//   1. s[r][j] = (sum_c q[r][c] k[j][c]) * inv_sqrt_dk   (c ascending)
+//   2. per row: max, e_j = expf(s_j - max), sum_j e_j (j ascending),
+//      p[r][j] = e_j / sum (the reference's per-element division)
+//   3. ctx[r][c] = sum_j p[r][j] v[j][c]                   (j ascending)
+// q rows, the head's K and V slices and the score matrix live in shared
+// memory; the expf table too.
 __global__ void attention_kernel(const uint16_t* __restrict__ q, const uint16_t* __restrict__ k,
-                                 const uint16_t* __restrict__ v, int64_t len, int64_t d, int dk,
+                                 const uint16_t* __restrict__ v, int len, int64_t d, int dk,
                                  float inv_sqrt_dk, uint16_t* __restrict__ ctx) {
   extern __shared__ __align__(16) uint8_t sm[];
   uint64_t* tab = reinterpret_cast<uint64_t*>(sm);
-  uint16_t* ks = reinterpret_cast<uint16_t*>(sm + 32 * 8);
+  float* sc = reinterpret_cast<float*>(sm + 32 * 8);  // [len][len + 1]
+  const int lp = len + 1;
+  uint16_t* qs = reinterpret_cast<uint16_t*>(sc + (int64_t)len * lp);  // [len][dk]
+  uint16_t* ks = qs + len * dk;
   uint16_t* vs = ks + len * dk;
-  float* sc = reinterpret_cast<float*>(vs + len * dk + ((len * dk) & 1));  // [blockDim][len]
   const int64_t s0 = (int64_t)blockIdx.x * len;  // first row of the sentence
   const int h0 = blockIdx.y * dk;
-  for (int i = threadIdx.x; i < 32; i += blockDim.x) tab[i] = moe_expf_tab_dev[i];
-  for (int64_t i = threadIdx.x; i < len * dk; i += blockDim.x) {
-    const int64_t j = i / dk, c = i - j * dk;
-    ks[i] = k[(s0 + j) * d + h0 + c];
-    vs[i] = v[(s0 + j) * d + h0 + c];
+  const int nt = blockDim.x;
+  for (int i = threadIdx.x; i < 32; i += nt) tab[i] = moe_expf_tab_dev[i];
+  for (int i = threadIdx.x; i < len * dk; i += nt) {
+    const int j = i / dk, c = i - j * dk;
+    const int64_t g = (s0 + j) * d + h0 + c;
+    qs[i] = q[g];
+    ks[i] = k[g];
+    vs[i] = v[g];
   }
   __syncthreads();
-  float* s = sc + (int64_t)threadIdx.x * len;
-  for (int64_t r = threadIdx.x; r < len; r += blockDim.x) {
-    const uint16_t* qr = q + (s0 + r) * d + h0;
-    for (int64_t j = 0; j < len; ++j) {
-      const uint16_t* kr = ks + j * dk;
-      float a = 0.0f;
-      for (int c = 0; c < dk; ++c) a = __fadd_rn(a, __fmul_rn(h2f(qr[c]), h2f(kr[c])));
-      s[j] = __fmul_rn(a, inv_sqrt_dk);
+  // 1. scores: pairs (r, j), four chains per thread
+  const int npair = len * len;
+  for (int p0 = threadIdx.x; p0 < npair; p0 += 4 * nt) {
+    float a[4] = {0.f, 0.f, 0.f, 0.f};
+    const uint16_t* qr[4];
+    const uint16_t* kr[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int pp = ::min(p0 + u * nt, npair - 1);
+      qr[u] = qs + (pp / len) * dk;
+      kr[u] = ks + (pp % len) * dk;
     }
+    for (int c = 0; c < dk; ++c)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) a[u] = __fadd_rn(a[u], __fmul_rn(h2f(qr[u][c]), h2f(kr[u][c])));
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int pp = p0 + u * nt;
+      if (pp < npair) sc[(pp / len) * lp + (pp % len)] = __fmul_rn(a[u], inv_sqrt_dk);
+    }
+  }
+  __syncthreads();
+  // 2. softmax per row (serial over j, as attend_one)
+  for (int r = threadIdx.x; r < len; r += nt) {
+    float* s = sc + r * lp;
     float mx = s[0];
-    for (int64_t j = 1; j < len; ++j) mx = fmaxf(mx, s[j]);
+    for (int j = 1; j < len; ++j) mx = fmaxf(mx, s[j]);
     float sum = 0.0f;
-    for (int64_t j = 0; j < len; ++j) {
+    for (int j = 0; j < len; ++j) {
       s[j] = moe_glibc_expf_t(__fsub_rn(s[j], mx), tab);
       sum = __fadd_rn(sum, s[j]);
     }
-    for (int c = 0; c < dk; ++c) {
-      float acc = 0.0f;
-      for (int64_t j = 0; j < len; ++j)
-        acc = __fadd_rn(acc, __fmul_rn(__fdiv_rn(s[j], sum), h2f(vs[j * dk + c])));
-      ctx[(s0 + r) * d + h0 + c] = f2h(acc);
+    for (int j = 0; j < len; ++j) s[j] = __fdiv_rn(s[j], sum);
+  }
+  __syncthreads();
+  // 3. context: outputs (r, c), four chains per thread
+  const int nout = len * dk;
+  for (int o0 = threadIdx.x; o0 < nout; o0 += 4 * nt) {
+    float a[4] = {0.f, 0.f, 0.f, 0.f};
+    const float* pr[4];
+    int cc[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int oo = ::min(o0 + u * nt, nout - 1);
+      pr[u] = sc + (oo / dk) * lp;
+      cc[u] = oo % dk;
+    }
+    for (int j = 0; j < len; ++j)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) a[u] = __fadd_rn(a[u], __fmul_rn(pr[u][j], h2f(vs[j * dk + cc[u]])));
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int oo = o0 + u * nt;
+      if (oo < nout) ctx[(s0 + oo / dk) * d + h0 + oo % dk] = f2h(a[u]);
     }
   }
 }
@@ -180,13 +224,16 @@ extern "C" int moe_encoder_forward(moe_moec* M, const int32_t* tokens, int64_t b
   MOE_CUDA_TRY(cudaMemsetAsync(E->bad, 0xFF, 4, st));
   embed_kernel<<<blocks_for(t * d), 256, 0, st>>>(E->tokens, t, len, d, E->tok, E->pos, E->vocab,
                                                   E->x, E->bad);
+  note_launch();
   uint32_t bad = 0;
   MOE_CUDA_TRY(cudaMemcpyAsync(&bad, E->bad, 4, cudaMemcpyDeviceToHost, st));
   MOE_CUDA_TRY(cudaStreamSynchronize(st));
   if (bad != 0xFFFFFFFFu) return set_error(MOE_EINVAL, "encoder: token id out of range");
   const int dk = (int)(d / E->heads);
   const float inv_sqrt_dk = 1.0f / std::sqrt((float)dk);
-  const size_t att_smem = 32 * 8 + (size_t)2 * len * dk * 2 + 4 + (size_t)128 * len * 4;
+  const size_t att_smem = 32 * 8 + (size_t)len * (len + 1) * 4 + (size_t)3 * len * dk * 2;
+  if (att_smem > 220 * 1024)
+    return set_error(MOE_EINVAL, "encoder: sentence too long for the attention kernel's shared memory");
   if (att_smem > 48 * 1024)
     MOE_CUDA_TRY(cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)att_smem));
@@ -198,11 +245,13 @@ extern "C" int moe_encoder_forward(moe_moec* M, const int32_t* tokens, int64_t b
     TRY(gemm(E, E->xn, t, l.q, 0, mode, E->q, st));
     TRY(gemm(E, E->xn, t, l.k, 0, mode, E->k, st));
     TRY(gemm(E, E->xn, t, l.v, 0, mode, E->v, st));
-    attention_kernel<<<dim3((unsigned)batch, (unsigned)E->heads), 128, att_smem, st>>>(
-        E->q, E->k, E->v, len, d, dk, inv_sqrt_dk, E->ctx);
+    attention_kernel<<<dim3((unsigned)batch, (unsigned)E->heads), 256, att_smem, st>>>(
+        E->q, E->k, E->v, (int)len, d, dk, inv_sqrt_dk, E->ctx);
+    note_launch();
     TRY(check_launch("encoder attention"));
     TRY(gemm(E, E->ctx, t, l.o, 0, mode, E->o, st));
     add_kernel<<<blocks_for(t * d), 256, 0, st>>>(x, E->o, t * d, y);
+    note_launch();
     std::swap(x, y);
     // the FFN: MoE block (moe_ffn_forward, no finished rows) or dense
     if (l.moe_block >= 0) {
@@ -212,6 +261,7 @@ extern "C" int moe_encoder_forward(moe_moec* M, const int32_t* tokens, int64_t b
       TRY(gemm(E, E->xn, t, l.w1, 1, mode, E->h, st));
       TRY(gemm(E, E->h, t, l.w2, 0, mode, E->o, st));
       add_kernel<<<blocks_for(t * d), 256, 0, st>>>(x, E->o, t * d, y);
+      note_launch();
     }
     std::swap(x, y);
   }

@@ -15,6 +15,7 @@
 // are re-tiled on the device into the tcgen05/TMA weight layout.
 // Attention, dense-FFN, embedding and projection records are checked and
 // skipped (outside the hot path).
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -307,6 +308,150 @@ int moe_moec_block(const moe_moec* M, int i, moe_layer** layer, char* name, size
 int moe_moec_destroy(moe_moec* M) {
   delete M;
   return MOE_OK;
+}
+
+// A synthetic checkpoint in the reference's format (the records walk()
+// reads, in the same order; checkpoint.cpp:390-415 writer layout) for
+// benchmarks at model sizes no fixture covers: fp16 tensors ~ N(0, s) with
+// random_model-like scales (s = 1/sqrt(fan-in) for projections, 0.02 for
+// biases and embeddings, LN gamma 1 + 0.1 N, beta 0.05 N), quantized records
+// random codes with per-column scales 1/(7 sqrt(fan-in)).  Deterministic in
+// the seed; not a reference model (no parity use).
+int moe_moec_write_synthetic(const char* path, const uint32_t* cfg9, int bits, uint64_t seed) {
+  if (!path || !cfg9) return set_error(MOE_EINVAL, "checkpoint: null argument");
+  if (bits != 4 && bits != 8 && bits != 16) return set_error(MOE_EINVAL, "checkpoint: bits must be 4, 8 or 16");
+  FILE* fp = std::fopen(path, "wb");
+  if (!fp) return set_error(MOE_EIO, "checkpoint: cannot open '%s'", path);
+  uint64_t h = 0xcbf29ce484222325ull, rs = seed * 0x9e3779b97f4a7c15ull + 1;
+  std::vector<uint8_t> buf;
+  auto flush = [&]() {
+    for (uint8_t b : buf) {
+      h ^= b;
+      h *= 0x100000001b3ull;
+    }
+    std::fwrite(buf.data(), 1, buf.size(), fp);
+    buf.clear();
+  };
+  auto put = [&](uint64_t v, int n) {
+    for (int i = 0; i < n; ++i) buf.push_back((uint8_t)(v >> (8 * i)));
+    if (buf.size() > (1u << 24)) flush();
+  };
+  auto rnd = [&]() {  // xorshift64*
+    rs ^= rs >> 12;
+    rs ^= rs << 25;
+    rs ^= rs >> 27;
+    return rs * 0x2545f4914f6cdd1dull;
+  };
+  auto f2h = [](float f) -> uint16_t {  // RN, |f| well inside the fp16 range
+    uint32_t x;
+    std::memcpy(&x, &f, 4);
+    const uint32_t sign = (x >> 16) & 0x8000u;
+    const int e = (int)((x >> 23) & 0xFF) - 112;
+    if (e <= 0) return (uint16_t)sign;
+    uint32_t m = (x & 0x7FFFFFu), r = ((uint32_t)e << 10) | (m >> 13);
+    const uint32_t rem = m & 0x1FFFu;
+    if (rem > 0x1000u || (rem == 0x1000u && (r & 1u))) ++r;
+    return (uint16_t)(sign | r);
+  };
+  auto normal = [&]() {  // sum of 4 uniforms, unit variance
+    float a = 0.f;
+    for (int i = 0; i < 4; ++i) a += (float)(rnd() >> 40) * (1.0f / 16777216.0f) - 0.5f;
+    return a * 1.7320508f;
+  };
+  uint32_t nrec = 0;
+  auto header = [&](const std::string& name, int dt, int ly, std::initializer_list<uint64_t> dims) {
+    put(name.size(), 2);
+    for (char ch : name) put((uint8_t)ch, 1);
+    put(dt, 1);
+    put(ly, 1);
+    put(dims.size(), 1);
+    for (uint64_t v : dims) put(v, 8);
+    ++nrec;
+  };
+  auto f16rec = [&](const std::string& name, std::initializer_list<uint64_t> dims, float scale,
+                    float offset) {
+    header(name, 0, 0, dims);
+    uint64_t n = 1;
+    for (uint64_t v : dims) n *= v;
+    for (uint64_t i = 0; i < n; ++i) put(f2h(offset + scale * normal()), 2);
+  };
+  const uint32_t d = cfg9[0], f = cfg9[1], nenc = cfg9[2], ndec = cfg9[3], E = cfg9[4];
+  const uint32_t vocab = cfg9[6], every = cfg9[7], maxlen = cfg9[8];
+  auto qrec = [&](const std::string& name, uint64_t m, uint64_t n) {
+    const uint64_t payload = bits == 4 ? E * m * n / 2 : E * m * n;
+    header(name, bits == 4 ? 2 : 1, bits == 4 ? 1 : 0, {E, m, n});
+    for (uint64_t i = 0; i < payload; i += 8) {
+      const uint64_t r = rnd();
+      for (uint64_t j = 0; j < 8 && i + j < payload; ++j) put((r >> (8 * j)) & 0xFF, 1);
+    }
+    put(E * n, 8);
+    const uint16_t sc = f2h(1.0f / (7.0f * std::sqrt((float)m)));
+    for (uint64_t i = 0; i < E * n; ++i) put(sc, 2);
+  };
+  auto attn = [&](const std::string& p) {
+    f16rec(p + ".ln_g", {d}, 0.1f, 1.0f);
+    f16rec(p + ".ln_b", {d}, 0.05f, 0.f);
+    for (const char* w : {"q", "k", "v", "o"}) {
+      f16rec(p + ".w" + w, {d, d}, 1.0f / std::sqrt((float)d), 0.f);
+      f16rec(p + ".b" + w, {d}, 0.02f, 0.f);
+    }
+  };
+  auto ffn = [&](const std::string& p, uint32_t idx) {
+    f16rec(p + ".ln_g", {d}, 0.1f, 1.0f);
+    f16rec(p + ".ln_b", {d}, 0.05f, 0.f);
+    if (idx % every != 0) {
+      f16rec(p + ".w1", {d, f}, 1.0f / std::sqrt((float)d), 0.f);
+      f16rec(p + ".b1", {f}, 0.02f, 0.f);
+      f16rec(p + ".w2", {f, d}, 1.0f / std::sqrt((float)f), 0.f);
+      f16rec(p + ".b2", {d}, 0.02f, 0.f);
+      return;
+    }
+    f16rec(p + ".gate_w", {d, E}, 1.0f / std::sqrt((float)d), 0.f);
+    f16rec(p + ".gate_b", {E}, 0.02f, 0.f);
+    if (bits == 16) {
+      f16rec(p + ".w1", {E, d, f}, 1.0f / std::sqrt((float)d), 0.f);
+      f16rec(p + ".w2", {E, f, d}, 1.0f / std::sqrt((float)f), 0.f);
+    } else {
+      qrec(p + ".w1", d, f);
+      qrec(p + ".w2", f, d);
+    }
+    f16rec(p + ".b1", {E, f}, 0.02f, 0.f);
+    f16rec(p + ".b2", {E, d}, 0.02f, 0.f);
+  };
+  // header (the record count is patched in once known: it precedes the
+  // records, so count first)
+  uint32_t count = 2 + 6;
+  for (uint32_t i = 0; i < nenc; ++i) count += 10 + (i % every ? 6 : 8);
+  for (uint32_t i = 0; i < ndec; ++i) count += 20 + (i % every ? 6 : 8);
+  for (char ch : std::string("MOEC")) put((uint8_t)ch, 1);
+  put(kVersion, 4);
+  for (int i = 0; i < 9; ++i) put(cfg9[i], 4);
+  put(bits == 16 ? 0 : bits == 8 ? 1 : 2, 1);
+  put(count, 4);
+  f16rec("tok_embed", {vocab, d}, 0.02f, 0.f);
+  f16rec("pos_embed", {maxlen, d}, 0.02f, 0.f);
+  for (uint32_t i = 0; i < nenc; ++i) {
+    const std::string p = "enc." + std::to_string(i);
+    attn(p + ".attn");
+    ffn(p + ".ffn", i);
+  }
+  for (uint32_t i = 0; i < ndec; ++i) {
+    const std::string p = "dec." + std::to_string(i);
+    attn(p + ".self");
+    attn(p + ".cross");
+    ffn(p + ".ffn", i);
+  }
+  for (const char* nm : {"enc_ln_g", "enc_ln_b", "dec_ln_g", "dec_ln_b"})
+    f16rec(nm, {d}, nm[std::strlen(nm) - 1] == 'g' ? 0.1f : 0.05f, nm[std::strlen(nm) - 1] == 'g' ? 1.0f : 0.f);
+  f16rec("out_w", {d, vocab}, 1.0f / std::sqrt((float)d), 0.f);
+  f16rec("out_b", {vocab}, 0.02f, 0.f);
+  flush();
+  const bool ok_count = nrec == count;
+  uint64_t hv = h;
+  for (int i = 0; i < 8; ++i) std::fputc((int)((hv >> (8 * i)) & 0xFF), fp);
+  const bool ok = std::fclose(fp) == 0;
+  if (!ok_count) return set_error(MOE_EINVAL, "checkpoint: synthetic record count mismatch");
+  return ok ? MOE_OK : set_error(MOE_EIO, "checkpoint: write to '%s' failed", path);
 }
 
 }  // extern "C"

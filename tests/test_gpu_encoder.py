@@ -48,3 +48,29 @@ def test_encoder_errors(cuda):
     m2 = MoecModel(os.path.join(GOLD, "model_int4.moec"), create_layers=False)
     with pytest.raises(ValueError, match="without device layers"):
         m2.encoder_forward(np.zeros((1, 3), np.int32))
+
+
+@pytest.mark.parametrize("bits", [4, 16])
+def test_encoder_synthetic_checkpoint_matches_reference(cuda, tmp_path, bits):
+    """A wider encoder (d=128, 8 heads of 16, 4 layers: two MoE, two dense,
+    E=8) from moe_moec_write_synthetic: the reference's own loader and
+    encoder_forward (oracle/_ref) against the device, EXACT bit for bit."""
+    import ctypes as C
+    from oracle.oracle import REF_SO
+    from paper_2211_10017_b200 import abi
+    from paper_2211_10017_b200.moec import MoecModel
+    if not os.path.exists(REF_SO):
+        pytest.skip("reference library not built")
+    path = str(tmp_path / f"syn{bits}.moec")
+    cfg = (C.c_uint32 * 9)(128, 256, 4, 1, 8, 8, 40, 2, 32)
+    abi.call("moe_moec_write_synthetic", path.encode(), cfg, bits, 11)
+    tok = np.random.default_rng(bits).integers(0, 40, (6, 16)).astype(np.int32)
+    lib = C.CDLL(REF_SO)
+    lib.ref_last_error.restype = C.c_char_p
+    want = np.zeros((6 * 16, 128), np.uint16)
+    st = lib.ref_encoder_forward(path.encode(), tok.ctypes.data_as(C.c_void_p), C.c_size_t(6),
+                                 C.c_size_t(16), want.ctypes.data_as(C.c_void_p))
+    assert st == 0, lib.ref_last_error()
+    m = MoecModel(path)
+    got = m.encoder_forward(tok, mode=0).cpu().numpy().view(np.uint16)
+    assert np.array_equal(got, want), int((got != want).sum())
