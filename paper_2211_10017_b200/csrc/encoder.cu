@@ -98,9 +98,12 @@ __global__ void attention_kernel(const uint16_t* __restrict__ q, const uint16_t*
   uint64_t* tab = reinterpret_cast<uint64_t*>(sm);
   float* sc = reinterpret_cast<float*>(sm + 32 * 8);  // [len][len + 1]
   const int lp = len + 1;
-  uint16_t* qs = reinterpret_cast<uint16_t*>(sc + (int64_t)len * lp);  // [len][dk]
-  uint16_t* ks = qs + len * dk;
-  uint16_t* vs = ks + len * dk;
+  // K rows at a pitch of dk + 2 halves: lanes reading one column of
+  // consecutive keys hit consecutive banks (at dk they all hit one bank)
+  const int kp = dk + 4;  // 8-byte aligned rows for the 4-column vector loads
+  uint16_t* qs = reinterpret_cast<uint16_t*>(sc + (int64_t)len * lp);  // [len][kp]
+  uint16_t* ks = qs + len * kp;                                        // [len][kp]
+  uint16_t* vs = ks + len * kp;                                        // [len][kp]
   const int64_t s0 = (int64_t)blockIdx.x * len;  // first row of the sentence
   const int h0 = blockIdx.y * dk;
   const int nt = blockDim.x;
@@ -108,31 +111,56 @@ __global__ void attention_kernel(const uint16_t* __restrict__ q, const uint16_t*
   for (int i = threadIdx.x; i < len * dk; i += nt) {
     const int j = i / dk, c = i - j * dk;
     const int64_t g = (s0 + j) * d + h0 + c;
-    qs[i] = q[g];
-    ks[i] = k[g];
-    vs[i] = v[g];
+    qs[j * kp + c] = q[g];
+    ks[j * kp + c] = k[g];
+    vs[j * kp + c] = v[g];
   }
   __syncthreads();
-  // 1. scores: pairs (r, j), four chains per thread
-  const int npair = len * len;
-  for (int p0 = threadIdx.x; p0 < npair; p0 += 4 * nt) {
-    float a[4] = {0.f, 0.f, 0.f, 0.f};
+  // 1. scores: a thread owns a 4 x 4 tile of (query row, key) chains; per
+  // input column c it reads 4 q and 4 k values (4-column vectors) and runs
+  // 16 independent chains (c ascending in each)
+  const int nr4 = (len + 3) / 4, ntile = nr4 * nr4;
+  for (int tix = threadIdx.x; tix < ntile; tix += nt) {
+    const int r0 = (tix / nr4) * 4, j0 = (tix % nr4) * 4;
+    float a[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int w = 0; w < 4; ++w) a[u][w] = 0.f;
     const uint16_t* qr[4];
     const uint16_t* kr[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const int pp = ::min(p0 + u * nt, npair - 1);
-      qr[u] = qs + (pp / len) * dk;
-      kr[u] = ks + (pp % len) * dk;
+      qr[u] = qs + ::min(r0 + u, len - 1) * kp;
+      kr[u] = ks + ::min(j0 + u, len - 1) * kp;
     }
-    for (int c = 0; c < dk; ++c)
+    for (int c0 = 0; c0 < dk; c0 += 4) {
+      uint2 qv[4], kv[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) a[u] = __fadd_rn(a[u], __fmul_rn(h2f(qr[u][c]), h2f(kr[u][c])));
+      for (int u = 0; u < 4; ++u) {
+        qv[u] = *reinterpret_cast<const uint2*>(qr[u] + c0);
+        kv[u] = *reinterpret_cast<const uint2*>(kr[u] + c0);
+      }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int pp = p0 + u * nt;
-      if (pp < npair) sc[(pp / len) * lp + (pp % len)] = __fmul_rn(a[u], inv_sqrt_dk);
+      for (int cc = 0; cc < 4; ++cc) {
+        float qf[4], kf[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t qw = cc < 2 ? qv[u].x : qv[u].y, kw = cc < 2 ? kv[u].x : kv[u].y;
+          qf[u] = h2f((uint16_t)((cc & 1) ? qw >> 16 : qw & 0xFFFFu));
+          kf[u] = h2f((uint16_t)((cc & 1) ? kw >> 16 : kw & 0xFFFFu));
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int w = 0; w < 4; ++w) a[u][w] = __fadd_rn(a[u][w], __fmul_rn(qf[u], kf[w]));
+      }
     }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int w = 0; w < 4; ++w)
+        if (r0 + u < len && j0 + w < len) sc[(r0 + u) * lp + j0 + w] = __fmul_rn(a[u][w], inv_sqrt_dk);
   }
   __syncthreads();
   // 2. softmax per row (serial over j, as attend_one)
@@ -148,26 +176,35 @@ __global__ void attention_kernel(const uint16_t* __restrict__ q, const uint16_t*
     for (int j = 0; j < len; ++j) s[j] = __fdiv_rn(s[j], sum);
   }
   __syncthreads();
-  // 3. context: outputs (r, c), four chains per thread
-  const int nout = len * dk;
-  for (int o0 = threadIdx.x; o0 < nout; o0 += 4 * nt) {
-    float a[4] = {0.f, 0.f, 0.f, 0.f};
+  // 3. context: a thread owns 4 rows x 4 columns of outputs; per key j it
+  // reads 4 probabilities and one 4-column vector of v (j ascending)
+  const int nc4 = dk / 4, nout = nr4 * nc4;
+  for (int tix = threadIdx.x; tix < nout; tix += nt) {
+    const int r0 = (tix / nc4) * 4, c0 = (tix % nc4) * 4;
+    float a[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int w = 0; w < 4; ++w) a[u][w] = 0.f;
     const float* pr[4];
-    int cc[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int oo = ::min(o0 + u * nt, nout - 1);
-      pr[u] = sc + (oo / dk) * lp;
-      cc[u] = oo % dk;
+    for (int u = 0; u < 4; ++u) pr[u] = sc + ::min(r0 + u, len - 1) * lp;
+    for (int j = 0; j < len; ++j) {
+      const uint2 vv = *reinterpret_cast<const uint2*>(vs + j * kp + c0);
+      const float vf[4] = {h2f((uint16_t)(vv.x & 0xFFFFu)), h2f((uint16_t)(vv.x >> 16)),
+                           h2f((uint16_t)(vv.y & 0xFFFFu)), h2f((uint16_t)(vv.y >> 16))};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float pu = pr[u][j];
+#pragma unroll
+        for (int w = 0; w < 4; ++w) a[u][w] = __fadd_rn(a[u][w], __fmul_rn(pu, vf[w]));
+      }
     }
-    for (int j = 0; j < len; ++j)
 #pragma unroll
-      for (int u = 0; u < 4; ++u) a[u] = __fadd_rn(a[u], __fmul_rn(pr[u][j], h2f(vs[j * dk + cc[u]])));
+    for (int u = 0; u < 4; ++u)
+      if (r0 + u < len)
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int oo = o0 + u * nt;
-      if (oo < nout) ctx[(s0 + oo / dk) * d + h0 + oo % dk] = f2h(a[u]);
-    }
+        for (int w = 0; w < 4; ++w) ctx[(s0 + r0 + u) * d + h0 + c0 + w] = f2h(a[u][w]);
   }
 }
 
@@ -179,6 +216,20 @@ int gemm(EncoderDev* E, const uint16_t* x, int64_t t, const DevLinear& w, int re
 }
 
 int blocks_for(int64_t n) { return (int)std::min<int64_t>((n + 255) / 256, 148 * 8); }
+
+// LayerNorm rows (model.cpp:175-195): the LN-only instantiation of the fused
+// gate kernel (same serial chains; rows staged by bulk copies) when the rows
+// are 16-byte aligned, else the standalone row kernel
+int layer_norm(EncoderDev* E, const uint16_t* x, int64_t t, const uint16_t* g, const uint16_t* b,
+               uint16_t* out, cudaStream_t st) {
+  const int64_t d = E->d;
+  if (d % 8 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0) {
+    GateFusedArgs a{x, t, d, g, b, nullptr, 0, nullptr, 0, 1, nullptr, out, nullptr, nullptr,
+                    nullptr, E->bad, 0, nullptr};
+    return launch_ln_rows(a, st);
+  }
+  return launch_layer_norm(x, t, d, g, b, out, st);
+}
 
 }  // namespace
 }  // namespace moecu
@@ -230,8 +281,9 @@ extern "C" int moe_encoder_forward(moe_moec* M, const int32_t* tokens, int64_t b
   MOE_CUDA_TRY(cudaStreamSynchronize(st));
   if (bad != 0xFFFFFFFFu) return set_error(MOE_EINVAL, "encoder: token id out of range");
   const int dk = (int)(d / E->heads);
+  if (dk % 4 != 0) return set_error(MOE_EINVAL, "encoder: head width (d_model / n_heads) must be a multiple of 4");
   const float inv_sqrt_dk = 1.0f / std::sqrt((float)dk);
-  const size_t att_smem = 32 * 8 + (size_t)len * (len + 1) * 4 + (size_t)3 * len * dk * 2;
+  const size_t att_smem = 32 * 8 + (size_t)len * (len + 1) * 4 + (size_t)3 * len * (dk + 4) * 2 + 16;
   if (att_smem > 220 * 1024)
     return set_error(MOE_EINVAL, "encoder: sentence too long for the attention kernel's shared memory");
   if (att_smem > 48 * 1024)
@@ -241,7 +293,7 @@ extern "C" int moe_encoder_forward(moe_moec* M, const int32_t* tokens, int64_t b
   uint16_t* y = E->x2;
   for (const EncLayerDev& l : E->layers) {
     // attention_forward (model.cpp:207-256)
-    TRY(launch_layer_norm(x, t, d, l.ln_g, l.ln_b, E->xn, st));
+    TRY(layer_norm(E, x, t, l.ln_g, l.ln_b, E->xn, st));
     TRY(gemm(E, E->xn, t, l.q, 0, mode, E->q, st));
     TRY(gemm(E, E->xn, t, l.k, 0, mode, E->k, st));
     TRY(gemm(E, E->xn, t, l.v, 0, mode, E->v, st));
@@ -257,7 +309,7 @@ extern "C" int moe_encoder_forward(moe_moec* M, const int32_t* tokens, int64_t b
     if (l.moe_block >= 0) {
       TRY(layer_forward(moec_layer(M, l.moe_block), x, nullptr, t, 1, mode, y, st));
     } else {
-      TRY(launch_layer_norm(x, t, d, l.fln_g, l.fln_b, E->xn, st));
+      TRY(layer_norm(E, x, t, l.fln_g, l.fln_b, E->xn, st));
       TRY(gemm(E, E->xn, t, l.w1, 1, mode, E->h, st));
       TRY(gemm(E, E->h, t, l.w2, 0, mode, E->o, st));
       add_kernel<<<blocks_for(t * d), 256, 0, st>>>(x, E->o, t * d, y);
@@ -265,6 +317,6 @@ extern "C" int moe_encoder_forward(moe_moec* M, const int32_t* tokens, int64_t b
     }
     std::swap(x, y);
   }
-  TRY(launch_layer_norm(x, t, d, E->ln_g, E->ln_b, out, st));
+  TRY(layer_norm(E, x, t, E->ln_g, E->ln_b, out, st));
   return check_launch("encoder");
 }
