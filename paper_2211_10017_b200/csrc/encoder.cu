@@ -103,7 +103,8 @@ __global__ void attention_kernel(const uint16_t* __restrict__ q, const uint16_t*
   const int kp = dk + 4;  // 8-byte aligned rows for the 4-column vector loads
   uint16_t* qs = reinterpret_cast<uint16_t*>(sc + (int64_t)len * lp);  // [len][kp]
   uint16_t* ks = qs + len * kp;                                        // [len][kp]
-  uint16_t* vs = ks + len * kp;                                        // [len][kp]
+  uint16_t* vs = ks;  // V replaces K after the scores (two CTAs per SM at len 128)
+  float* rsum = reinterpret_cast<float*>(ks + len * kp);              // [len]
   const int64_t s0 = (int64_t)blockIdx.x * len;  // first row of the sentence
   const int h0 = blockIdx.y * dk;
   const int nt = blockDim.x;
@@ -113,7 +114,6 @@ __global__ void attention_kernel(const uint16_t* __restrict__ q, const uint16_t*
     const int64_t g = (s0 + j) * d + h0 + c;
     qs[j * kp + c] = q[g];
     ks[j * kp + c] = k[g];
-    vs[j * kp + c] = v[g];
   }
   __syncthreads();
   // 1. scores: a thread owns a 4 x 4 tile of (query row, key) chains; per
@@ -150,10 +150,12 @@ __global__ void attention_kernel(const uint16_t* __restrict__ q, const uint16_t*
           qf[u] = h2f((uint16_t)((cc & 1) ? qw >> 16 : qw & 0xFFFFu));
           kf[u] = h2f((uint16_t)((cc & 1) ? kw >> 16 : kw & 0xFFFFu));
         }
+        // fp16 x fp16 products are exact in f32, so one FMA equals the
+        // reference's separately rounded multiply-then-add
 #pragma unroll
         for (int u = 0; u < 4; ++u)
 #pragma unroll
-          for (int w = 0; w < 4; ++w) a[u][w] = __fadd_rn(a[u][w], __fmul_rn(qf[u], kf[w]));
+          for (int w = 0; w < 4; ++w) a[u][w] = __fmaf_rn(qf[u], kf[w], a[u][w]);
       }
     }
 #pragma unroll
@@ -163,17 +165,38 @@ __global__ void attention_kernel(const uint16_t* __restrict__ q, const uint16_t*
         if (r0 + u < len && j0 + w < len) sc[(r0 + u) * lp + j0 + w] = __fmul_rn(a[u][w], inv_sqrt_dk);
   }
   __syncthreads();
-  // 2. softmax per row (serial over j, as attend_one)
+  // V into the K slots (K is no longer read)
+  for (int i = threadIdx.x; i < len * dk; i += nt) {
+    const int j = i / dk, c = i - j * dk;
+    vs[j * kp + c] = v[(s0 + j) * d + h0 + c];
+  }
+  // 2. softmax (attend_one's order where it matters): the row max is exact
+  // in any order (a warp per row); every expf in parallel; the row sums
+  // serially in key order (a thread per row); every p = e / sum in parallel
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int r = warp; r < len; r += nt / 32) {
+    float m = -INFINITY;
+    for (int j = lane; j < len; j += 32) m = fmaxf(m, sc[r * lp + j]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) rsum[r] = m;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < len * len; i += nt) {
+    const int r = i / len, j = i - r * len;
+    sc[r * lp + j] = moe_glibc_expf_t(__fsub_rn(sc[r * lp + j], rsum[r]), tab);
+  }
+  __syncthreads();
   for (int r = threadIdx.x; r < len; r += nt) {
-    float* s = sc + r * lp;
-    float mx = s[0];
-    for (int j = 1; j < len; ++j) mx = fmaxf(mx, s[j]);
+    const float* e = sc + r * lp;
     float sum = 0.0f;
-    for (int j = 0; j < len; ++j) {
-      s[j] = moe_glibc_expf_t(__fsub_rn(s[j], mx), tab);
-      sum = __fadd_rn(sum, s[j]);
-    }
-    for (int j = 0; j < len; ++j) s[j] = __fdiv_rn(s[j], sum);
+    for (int j = 0; j < len; ++j) sum = __fadd_rn(sum, e[j]);
+    rsum[r] = sum;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < len * len; i += nt) {
+    const int r = i / len, j = i - r * len;
+    sc[r * lp + j] = __fdiv_rn(sc[r * lp + j], rsum[r]);
   }
   __syncthreads();
   // 3. context: a thread owns 4 rows x 4 columns of outputs; per key j it
@@ -283,7 +306,7 @@ extern "C" int moe_encoder_forward(moe_moec* M, const int32_t* tokens, int64_t b
   const int dk = (int)(d / E->heads);
   if (dk % 4 != 0) return set_error(MOE_EINVAL, "encoder: head width (d_model / n_heads) must be a multiple of 4");
   const float inv_sqrt_dk = 1.0f / std::sqrt((float)dk);
-  const size_t att_smem = 32 * 8 + (size_t)len * (len + 1) * 4 + (size_t)3 * len * (dk + 4) * 2 + 16;
+  const size_t att_smem = 32 * 8 + (size_t)len * (len + 1) * 4 + (size_t)2 * len * (dk + 4) * 2 + (size_t)len * 4 + 16;
   if (att_smem > 220 * 1024)
     return set_error(MOE_EINVAL, "encoder: sentence too long for the attention kernel's shared memory");
   if (att_smem > 48 * 1024)
