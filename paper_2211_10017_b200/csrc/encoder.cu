@@ -231,6 +231,150 @@ __global__ void attention_kernel(const uint16_t* __restrict__ q, const uint16_t*
   }
 }
 
+// FAST mode (sentences of <= 128 tokens, head width a multiple of 16): the
+// same attention on the tensor cores, flash-style in registers -- a warp owns
+// 16 query rows: S = Q K^T by mma.m16n8k16 (f16 in, f32 accumulate), scale,
+// row max / exp / row sum by quad shuffles, P = e / sum rounded to fp16 and
+// reused in registers as the A operand of O = P V (V transposed in shared
+// memory).  Not bit-exact (tensor-core sums, fp16 P, fast exp); within the
+// layer tolerance.
+constexpr int kAttMaxLen = 128;
+
+__device__ __forceinline__ void mma16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                         uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
+  return (uint32_t)f2h(lo) | ((uint32_t)f2h(hi) << 16);
+}
+
+template <int DK>
+__global__ void __launch_bounds__(256) attention_tc_kernel(const uint16_t* __restrict__ q,
+                                                           const uint16_t* __restrict__ k,
+                                                           const uint16_t* __restrict__ v, int len,
+                                                           int64_t d, float inv_sqrt_dk,
+                                                           uint16_t* __restrict__ ctx) {
+  constexpr int P = DK + 8;                  // Q / K row pitch (halves): conflict-free fragments
+  constexpr int NT = kAttMaxLen / 8;         // key tiles of 8
+  constexpr int PV = kAttMaxLen + 8;         // V^T row pitch
+  extern __shared__ __align__(16) uint16_t att_sm[];
+  uint16_t* Qs = att_sm;                    // [kAttMaxLen][P]
+  uint16_t* Ks = Qs + kAttMaxLen * P;       // [kAttMaxLen][P]
+  uint16_t* Vt = Ks + kAttMaxLen * P;       // [DK][PV]
+  const int Lp = (len + 15) & ~15;
+  const int64_t s0 = (int64_t)blockIdx.x * len;
+  const int h0 = blockIdx.y * DK;
+  for (int i = threadIdx.x; i < Lp * DK; i += blockDim.x) {
+    const int j = i / DK, c = i - j * DK;
+    uint16_t qv = 0, kv = 0, vv = 0;
+    if (j < len) {
+      const int64_t g = (s0 + j) * d + h0 + c;
+      qv = q[g];
+      kv = k[g];
+      vv = v[g];
+    }
+    Qs[j * P + c] = qv;
+    Ks[j * P + c] = kv;
+    Vt[c * PV + j] = vv;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  if (warp * 16 >= Lp) return;
+  const int r0 = warp * 16;
+  const int ntile = Lp / 8;
+  float acc[NT][4];
+#pragma unroll
+  for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+  // S = Q K^T
+#pragma unroll
+  for (int kk = 0; kk < DK / 16; ++kk) {
+    const uint16_t* qa = Qs + (r0 + g) * P + kk * 16 + 2 * t;
+    const uint32_t a0 = *reinterpret_cast<const uint32_t*>(qa);
+    const uint32_t a1 = *reinterpret_cast<const uint32_t*>(qa + 8 * P);
+    const uint32_t a2 = *reinterpret_cast<const uint32_t*>(qa + 8);
+    const uint32_t a3 = *reinterpret_cast<const uint32_t*>(qa + 8 * P + 8);
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      if (j < ntile) {
+        const uint16_t* kb = Ks + (j * 8 + g) * P + kk * 16 + 2 * t;
+        mma16816(acc[j], a0, a1, a2, a3, *reinterpret_cast<const uint32_t*>(kb),
+                 *reinterpret_cast<const uint32_t*>(kb + 8));
+      }
+    }
+  }
+  // softmax over keys (rows g and g + 8 of the strip; columns 8j + 2t, +1)
+  float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+  for (int j = 0; j < NT; ++j) {
+    if (j < ntile) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int key = j * 8 + 2 * t + (e & 1);
+        acc[j][e] = key < len ? acc[j][e] * inv_sqrt_dk : -INFINITY;
+      }
+      mx0 = fmaxf(mx0, fmaxf(acc[j][0], acc[j][1]));
+      mx1 = fmaxf(mx1, fmaxf(acc[j][2], acc[j][3]));
+    }
+  }
+#pragma unroll
+  for (int o = 1; o < 4; o <<= 1) {
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
+  }
+  float sum0 = 0.f, sum1 = 0.f;
+#pragma unroll
+  for (int j = 0; j < NT; ++j) {
+    if (j < ntile) {
+      acc[j][0] = __expf(acc[j][0] - mx0);
+      acc[j][1] = __expf(acc[j][1] - mx0);
+      acc[j][2] = __expf(acc[j][2] - mx1);
+      acc[j][3] = __expf(acc[j][3] - mx1);
+      sum0 += acc[j][0] + acc[j][1];
+      sum1 += acc[j][2] + acc[j][3];
+    }
+  }
+#pragma unroll
+  for (int o = 1; o < 4; o <<= 1) {
+    sum0 += __shfl_xor_sync(0xffffffffu, sum0, o);
+    sum1 += __shfl_xor_sync(0xffffffffu, sum1, o);
+  }
+  const float is0 = 1.f / sum0, is1 = 1.f / sum1;
+  // O = P V: the S accumulators of key tiles 2u, 2u + 1 are the A fragment
+  // of k-step u
+  float o[DK / 8][4];
+#pragma unroll
+  for (int c8 = 0; c8 < DK / 8; ++c8) o[c8][0] = o[c8][1] = o[c8][2] = o[c8][3] = 0.f;
+#pragma unroll
+  for (int u = 0; u < NT / 2; ++u) {
+    if (2 * u < ntile) {
+      const uint32_t a0 = pack_h2(acc[2 * u][0] * is0, acc[2 * u][1] * is0);
+      const uint32_t a1 = pack_h2(acc[2 * u][2] * is1, acc[2 * u][3] * is1);
+      const uint32_t a2 = pack_h2(acc[2 * u + 1][0] * is0, acc[2 * u + 1][1] * is0);
+      const uint32_t a3 = pack_h2(acc[2 * u + 1][2] * is1, acc[2 * u + 1][3] * is1);
+#pragma unroll
+      for (int c8 = 0; c8 < DK / 8; ++c8) {
+        const uint16_t* vb = Vt + (c8 * 8 + g) * PV + u * 16 + 2 * t;
+        mma16816(o[c8], a0, a1, a2, a3, *reinterpret_cast<const uint32_t*>(vb),
+                 *reinterpret_cast<const uint32_t*>(vb + 8));
+      }
+    }
+  }
+#pragma unroll
+  for (int c8 = 0; c8 < DK / 8; ++c8) {
+    const int col = h0 + c8 * 8 + 2 * t;
+    const int ra = r0 + g, rb2 = r0 + g + 8;
+    if (ra < len)
+      *reinterpret_cast<uint32_t*>(ctx + (s0 + ra) * d + col) = pack_h2(o[c8][0], o[c8][1]);
+    if (rb2 < len)
+      *reinterpret_cast<uint32_t*>(ctx + (s0 + rb2) * d + col) = pack_h2(o[c8][2], o[c8][3]);
+  }
+}
+
 int gemm(EncoderDev* E, const uint16_t* x, int64_t t, const DevLinear& w, int relu, int mode,
          uint16_t* out, cudaStream_t st) {
   GemmArgs g{x, t, w.m, E->problem, 1, w.tiled, nullptr, 16, 1, w.n, w.bias, relu, out,
@@ -320,8 +464,21 @@ extern "C" int moe_encoder_forward(moe_moec* M, const int32_t* tokens, int64_t b
     TRY(gemm(E, E->xn, t, l.q, 0, mode, E->q, st));
     TRY(gemm(E, E->xn, t, l.k, 0, mode, E->k, st));
     TRY(gemm(E, E->xn, t, l.v, 0, mode, E->v, st));
-    attention_kernel<<<dim3((unsigned)batch, (unsigned)E->heads), 256, att_smem, st>>>(
-        E->q, E->k, E->v, (int)len, d, dk, inv_sqrt_dk, E->ctx);
+    if (mode == MOE_MODE_FAST && len <= kAttMaxLen && (dk == 64 || dk == 16 || dk == 32 || dk == 128)) {
+      const dim3 grid((unsigned)batch, (unsigned)E->heads);
+      const size_t tsm = ((size_t)2 * kAttMaxLen * (dk + 8) + (size_t)dk * (kAttMaxLen + 8)) * 2;
+      auto go = [&](auto kern) -> int {
+        if (tsm > 48 * 1024)
+          MOE_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
+        kern<<<grid, 256, tsm, st>>>(E->q, E->k, E->v, (int)len, d, inv_sqrt_dk, E->ctx);
+        return MOE_OK;
+      };
+      TRY(dk == 64 ? go(attention_tc_kernel<64>) : dk == 16 ? go(attention_tc_kernel<16>)
+                   : dk == 32 ? go(attention_tc_kernel<32>) : go(attention_tc_kernel<128>));
+    } else {
+      attention_kernel<<<dim3((unsigned)batch, (unsigned)E->heads), 256, att_smem, st>>>(
+          E->q, E->k, E->v, (int)len, d, dk, inv_sqrt_dk, E->ctx);
+    }
     note_launch();
     TRY(check_launch("encoder attention"));
     TRY(gemm(E, E->ctx, t, l.o, 0, mode, E->o, st));

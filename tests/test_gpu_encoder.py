@@ -74,3 +74,22 @@ def test_encoder_synthetic_checkpoint_matches_reference(cuda, tmp_path, bits):
     m = MoecModel(path)
     got = m.encoder_forward(tok, mode=0).cpu().numpy().view(np.uint16)
     assert np.array_equal(got, want), int((got != want).sum())
+
+
+@pytest.mark.parametrize("length", [128, 100, 17])
+def test_encoder_fast_attention_vs_exact(cuda, tmp_path, length):
+    """FAST mode's tensor-core attention (mma.sync, flash-style in registers;
+    64-wide heads, sentences up to 128 tokens, ragged lengths masked) against
+    the bit-exact EXACT path on the same device, within the layer tolerance."""
+    import ctypes as C
+    from paper_2211_10017_b200 import abi
+    from paper_2211_10017_b200.moec import MoecModel
+    path = str(tmp_path / "syn_wide.moec")
+    cfg = (C.c_uint32 * 9)(256, 512, 2, 1, 4, 4, 64, 2, 128)
+    abi.call("moe_moec_write_synthetic", path.encode(), cfg, 4, 3)
+    m = MoecModel(path)
+    tok = np.random.default_rng(length).integers(0, 64, (3, length)).astype(np.int32)
+    exact = m.encoder_forward(tok, mode=0).cpu().numpy().astype(np.float64)
+    fast = m.encoder_forward(tok, mode=1).cpu().numpy().astype(np.float64)
+    err = np.abs(fast - exact).max() / max(np.abs(exact).max(), 1e-30)
+    assert err <= TOL_FAST, err
