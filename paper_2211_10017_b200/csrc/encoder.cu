@@ -23,7 +23,8 @@ namespace moecu {
 EncoderDev::~EncoderDev() {
   for (void* p : allocs) cudaFree(p);
   for (void* p : {(void*)x, (void*)x2, (void*)xn, (void*)q, (void*)k, (void*)v, (void*)ctx,
-                  (void*)o, (void*)h, (void*)tokens, (void*)problem, (void*)bad})
+                  (void*)o, (void*)h, (void*)tokens, (void*)problem, (void*)bad, (void*)ident,
+                  (void*)ones})
     if (p) cudaFree(p);
 }
 
@@ -375,11 +376,42 @@ __global__ void __launch_bounds__(256) attention_tc_kernel(const uint16_t* __res
   }
 }
 
+int blocks_for(int64_t n);
+
+// y = x W + b (ReLU); residual non-null: out = residual (+) y.  FAST mode
+// folds the residual into the tcgen05 epilogue (its k = 1 combine form with
+// an identity row map and unit scales -- the same fp16 RN add); EXACT keeps
+// the separate add so every op stays the reference's.
 int gemm(EncoderDev* E, const uint16_t* x, int64_t t, const DevLinear& w, int relu, int mode,
-         uint16_t* out, cudaStream_t st) {
+         uint16_t* out, cudaStream_t st, const uint16_t* residual = nullptr,
+         uint16_t* res_out = nullptr) {
   GemmArgs g{x, t, w.m, E->problem, 1, w.tiled, nullptr, 16, 1, w.n, w.bias, relu, out,
              0, t};
-  return mode == MOE_MODE_EXACT ? launch_gemm_exact(g, st) : launch_gemm_tc(g, st);
+  if (mode == MOE_MODE_EXACT) {
+    TRY(launch_gemm_exact(g, st));
+  } else {
+    if (residual) {
+      g.cx = residual;
+      g.cperm = E->ident;
+      g.cscale = E->ones;
+      g.cout = res_out;
+    }
+    TRY(launch_gemm_tc(g, st));
+    if (residual) return MOE_OK;
+  }
+  if (residual) {
+    add_kernel<<<blocks_for(t * w.n), 256, 0, st>>>(residual, out, t * w.n, res_out);
+    note_launch();
+  }
+  return MOE_OK;
+}
+
+__global__ void fill_ident_kernel(uint32_t* ident, uint16_t* ones, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    ident[i] = (uint32_t)i;
+    ones[i] = 0x3C00;  // 1.0
+  }
 }
 
 int blocks_for(int64_t n) { return (int)std::min<int64_t>((n + 255) / 256, 148 * 8); }
@@ -426,10 +458,16 @@ extern "C" int moe_encoder_forward(moe_moec* M, const int32_t* tokens, int64_t b
     for (void* p : {(void*)E->x, (void*)E->x2, (void*)E->xn, (void*)E->q, (void*)E->k, (void*)E->v,
                     (void*)E->ctx, (void*)E->o, (void*)E->h, (void*)E->tokens})
       if (p) cudaFree(p);
+    if (E->ident) cudaFree(E->ident);
+    if (E->ones) cudaFree(E->ones);
     for (uint16_t** p : {&E->x, &E->x2, &E->xn, &E->q, &E->k, &E->v, &E->ctx, &E->o})
       MOE_CUDA_TRY(cudaMalloc(p, t * d * 2));
     MOE_CUDA_TRY(cudaMalloc(&E->h, t * E->f * 2));
     MOE_CUDA_TRY(cudaMalloc(&E->tokens, t * 4));
+    MOE_CUDA_TRY(cudaMalloc(&E->ident, t * 4));
+    MOE_CUDA_TRY(cudaMalloc(&E->ones, t * 2));
+    fill_ident_kernel<<<blocks_for(t), 256, 0, st>>>(E->ident, E->ones, t);
+    note_launch();
     E->cap_t = t;
   }
   if (!E->problem) {
@@ -481,9 +519,7 @@ extern "C" int moe_encoder_forward(moe_moec* M, const int32_t* tokens, int64_t b
     }
     note_launch();
     TRY(check_launch("encoder attention"));
-    TRY(gemm(E, E->ctx, t, l.o, 0, mode, E->o, st));
-    add_kernel<<<blocks_for(t * d), 256, 0, st>>>(x, E->o, t * d, y);
-    note_launch();
+    TRY(gemm(E, E->ctx, t, l.o, 0, mode, E->o, st, x, y));  // y = x (+) O
     std::swap(x, y);
     // the FFN: MoE block (moe_ffn_forward, no finished rows) or dense
     if (l.moe_block >= 0) {
@@ -491,9 +527,7 @@ extern "C" int moe_encoder_forward(moe_moec* M, const int32_t* tokens, int64_t b
     } else {
       TRY(layer_norm(E, x, t, l.fln_g, l.fln_b, E->xn, st));
       TRY(gemm(E, E->xn, t, l.w1, 1, mode, E->h, st));
-      TRY(gemm(E, E->h, t, l.w2, 0, mode, E->o, st));
-      add_kernel<<<blocks_for(t * d), 256, 0, st>>>(x, E->o, t * d, y);
-      note_launch();
+      TRY(gemm(E, E->h, t, l.w2, 0, mode, E->o, st, x, y));  // y = x (+) FFN
     }
     std::swap(x, y);
   }

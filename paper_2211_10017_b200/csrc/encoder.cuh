@@ -36,6 +36,8 @@ struct EncoderDev {
   int32_t* tokens = nullptr;
   uint32_t* problem = nullptr;  // {0, 0, t}: one-problem grouped GEMM
   uint32_t* bad = nullptr;      // token range check
+  uint32_t* ident = nullptr;    // FAST residuals in the GEMM epilogue: identity row map
+  uint16_t* ones = nullptr;     //   and unit scales (x (+) y (*) 1 == x (+) y)
   ~EncoderDev();
 };
 
