@@ -524,7 +524,6 @@ def run_encoder(args, wl):
     cfg = (C.c_uint32 * 9)(d, f, nenc, 1, E, heads, vocab, 2, length)
     abi.call("moe_moec_write_synthetic", path.encode(), cfg, 4, 2024)
     m = MoecModel(path)
-    os.remove(path)
     tok = np.random.default_rng(7).integers(0, vocab, (batch, length)).astype(np.int32)
     for _ in range(args.warmup):
         m.encoder_forward(tok, mode=1)
@@ -563,6 +562,37 @@ def run_encoder(args, wl):
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
+    del m
+    torch.cuda.empty_cache()
+    if not args.no_cpu_baseline:
+        # the reference's encoder_forward (oracle/_ref, compiled from the
+        # reference sources) on the same checkpoint: one sentence of the
+        # batch, all host threads, load excluded
+        try:
+            from oracle.oracle import REF_SO
+            lib = C.CDLL(REF_SO)
+            lib.ref_model_load.restype = C.c_void_p
+            lib.ref_last_error.restype = C.c_char_p
+            h = lib.ref_model_load(path.encode())
+            if not h:
+                raise RuntimeError(lib.ref_last_error().decode())
+            nthr = os.cpu_count() or 1
+            y = np.zeros((length, d), np.uint16)
+            t0 = time.perf_counter()
+            st = lib.ref_model_encoder(C.c_void_p(h), tok[:1].ctypes.data_as(C.c_void_p),
+                                       C.c_size_t(1), C.c_size_t(length), nthr,
+                                       y.ctypes.data_as(C.c_void_p))
+            dt = time.perf_counter() - t0
+            lib.ref_model_free(C.c_void_p(h))
+            if st != 0:
+                raise RuntimeError(lib.ref_last_error().decode())
+            line["cpu_baseline"] = {"value": length / dt, "unit": "tokens/s", "cores": nthr,
+                                    "kind": "reference",
+                                    "sample": f"1 of {batch} sentences ({length} tokens), "
+                                              f"encoder_forward threads={nthr}, {dt:.1f} s"}
+        except Exception as e:  # noqa: BLE001 -- report, do not fail the GPU line
+            line["cpu_baseline"] = {"unavailable": str(e)[:200]}
+    os.remove(path)
     print(json.dumps(line), flush=True)
 
 

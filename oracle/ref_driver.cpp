@@ -491,4 +491,25 @@ int ref_encoder_forward(const char* path, const int32_t* tokens, size_t batch, s
   });
 }
 
+// a loaded model kept across calls (timing encoder_forward without the load)
+void* ref_model_load(const char* path) {
+  try {
+    return new Model(load_model(path));
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+void ref_model_free(void* h) { delete static_cast<Model*>(h); }
+int ref_model_encoder(void* h, const int32_t* tokens, size_t batch, size_t len, int threads,
+                      uint16_t* out) {
+  return guarded([&] {
+    const Model& m = *static_cast<Model*>(h);
+    std::vector<std::vector<int32_t>> src(batch, std::vector<int32_t>(len));
+    for (size_t s = 0; s < batch; ++s)
+      for (size_t p = 0; p < len; ++p) src[s][p] = tokens[s * len + p];
+    out_mat(encoder_forward(m, src, nullptr, threads), out);
+  });
+}
+
 }  // extern "C"
