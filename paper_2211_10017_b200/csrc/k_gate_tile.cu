@@ -335,6 +335,9 @@ int launch_gate_tile(const GateFusedArgs& a, int tr, cudaStream_t st) {
   if (a.T == 0) return MOE_OK;
   if (!gate_tile_supported(a.T, a.d, a.E, a.k)) return set_error(MOE_EINVAL, "gate_tile: unsupported shape");
   if (a.E == 64) {
+    static const int shape = std::getenv("MOE_GATE_TILE_SHAPE") ? std::atoi(std::getenv("MOE_GATE_TILE_SHAPE")) : 0;
+    if (tr == 64 && shape == 1) return launch_tile<8, 2, 8, 32>(a, st);  // dev A/B thread tiles
+    if (tr == 64 && shape == 2) return launch_tile<2, 8, 32, 8>(a, st);
     if (tr == 128) return launch_tile<8, 4, 16, 16>(a, st);
     if (tr == 64) return launch_tile<4, 4, 16, 16>(a, st);
     if (tr == 32) return launch_tile<2, 4, 16, 16>(a, st);
