@@ -11,6 +11,7 @@ python bench.py --impl reference --steps 3 --warmup 1 2>&1 | tail -1 > gpurun_ou
 for w in c1i4 c3_1 c3_8 c3_64 c4 c5; do python bench.py --workload $w --steps 100 --warmup 5 --no-cpu-baseline 2>&1 | tail -1 > gpurun_out/final_$w.json; cat gpurun_out/final_$w.json | cut -c1-200; done
 python bench.py --workload decode_prune --steps 5 --warmup 3 2>&1 | tail -1 > gpurun_out/final_decode.json
 python bench.py --workload c4_stack --steps 10 --warmup 3 2>&1 | tail -1 > gpurun_out/final_c4_stack.json
+python bench.py --workload c4_encoder --steps 5 --warmup 2 2>&1 | tail -1 > gpurun_out/final_c4_encoder.json
 python bench.py --force-ep --workload c5 --steps 20 --warmup 3 2>/dev/null | tail -1 > gpurun_out/final_ep_c5.json
 python scripts/quant_bench.py > gpurun_out/final_quant.jsonl 2>&1
 for w in c2 c3_64 c4; do
