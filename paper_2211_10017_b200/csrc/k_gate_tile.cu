@@ -26,7 +26,6 @@
 namespace moecu {
 
 namespace gt {
-constexpr int kThreads = 256;
 constexpr int KC = 32;  // inputs per staged chunk
 
 __device__ __forceinline__ float2 ffma2(float a, float2 b, float2 c) {
