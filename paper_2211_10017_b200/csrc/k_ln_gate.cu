@@ -597,6 +597,7 @@ __global__ void __launch_bounds__(NT, LNONLY ? 3 : 1) ln_gate_kernel(
     }
   }
   __syncthreads();
+  G3_TRACE(6);
   // ---- expf(l_j - max) for every (row, expert) in parallel (routing.cpp:34)
   for (int i = tid; i < nrow * E; i += NT) {
     const int r = i / E, j = i - r * E;
@@ -606,6 +607,7 @@ __global__ void __launch_bounds__(NT, LNONLY ? 3 : 1) ln_gate_kernel(
     ex[r * lp + j] = moe_glibc_expf_t(__fsub_rn(l[j], l[s0]), tab);
   }
   __syncthreads();
+  G3_TRACE(7);
   // ---- serial sum in expert order, scales, routing keys (routing.cpp:33-38, 55-62)
   if (tid < nrow) {
     const int r = tid;
@@ -744,10 +746,10 @@ static int launch_g3(const GateFusedArgs& a, int rb, cudaStream_t st) {
     std::fprintf(stderr,
                  "ln_gate EPG=%d RPT=%d NT=%d grid=%u rb=%d kc=%d nch=%d tasks=%d wide=%d: "
                  "span=%lld ns cta mean=%lld ns; cta0 clocks rows=%lld chains=%lld norm=%lld "
-                 "logits=%lld tail=%lld [widen %lld, mean chain %lld, sync %lld, sqdev %lld, var chain+ %lld]\n",
+                 "logits=%lld tail=%lld (select %lld, expf %lld, sums %lld) [widen %lld, mean chain %lld, sync %lld, sqdev %lld, var chain+ %lld]\n",
                  EPG, RPT, NT, grid, rb, C.kc, C.nch, C.ntask, C.wide, hi - lo, sum / grid,
                  h[1] - h[0], h[2] - h[1], h[3] - h[2], h[4] - h[3], h[5] - h[4],
-                 h[8] - h[1], h[9] - h[8], h[10] - h[9], h[11] - h[10], h[2] - h[11]);
+                 h[6] - h[4], h[7] - h[6], h[5] - h[7], h[8] - h[1], h[9] - h[8], h[10] - h[9], h[11] - h[10], h[2] - h[11]);
   }
   return check_launch("ln_gate");
 }
