@@ -819,9 +819,24 @@ int moe_layer_forward_host(moe_layer* L, const uint16_t* x_host, const uint8_t* 
       int64_t t0, t1;
       chunk_rows(i, &t0, &t1);
       MOE_CUDA_TRY(cudaStreamWaitEvent(cs, in_done[i], 0));
-      TRY(layer_forward(L, L->dx + t0 * d, fin_host ? L->dfin + t0 : nullptr, t1 - t0, k, mode,
-                        L->dout + t0 * d, cs));
-      MOE_CUDA_TRY(cudaMemcpyAsync(L->dstatus + 2 * i, L->bad_row, 8, cudaMemcpyDeviceToDevice, cs));
+      static const bool d2d = std::getenv("MOE_HOST_D2D") && std::atoi(std::getenv("MOE_HOST_D2D")) == 1;
+      if (d2d) {  // dev A/B: status copied after the chunk (a copy-engine node in the graph)
+        TRY(layer_forward(L, L->dx + t0 * d, fin_host ? L->dfin + t0 : nullptr, t1 - t0, k, mode,
+                          L->dout + t0 * d, cs));
+        MOE_CUDA_TRY(cudaMemcpyAsync(L->dstatus + 2 * i, L->bad_row, 8, cudaMemcpyDeviceToDevice, cs));
+      } else {
+        // the chunk's kernels report straight into its status slot: no
+        // device-to-device copy node between the chunks' kernels
+        uint32_t* const br = L->bad_row;
+        uint32_t* const be = L->bad_expert;
+        L->bad_row = L->dstatus + 2 * i;
+        L->bad_expert = L->dstatus + 2 * i + 1;
+        const int rc = layer_forward(L, L->dx + t0 * d, fin_host ? L->dfin + t0 : nullptr, t1 - t0,
+                                     k, mode, L->dout + t0 * d, cs);
+        L->bad_row = br;
+        L->bad_expert = be;
+        TRY(rc);
+      }
       MOE_CUDA_TRY(cudaEventRecord(comp_done[i], cs));
       MOE_CUDA_TRY(cudaStreamWaitEvent(L->io_out, comp_done[i], 0));
       MOE_CUDA_TRY(cudaMemcpyAsync(out_host + t0 * d, L->dout + t0 * d, (t1 - t0) * d * 2,
