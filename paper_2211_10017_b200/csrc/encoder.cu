@@ -260,28 +260,28 @@ __global__ void __launch_bounds__(256) attention_tc_kernel(const uint16_t* __res
                                                            const uint16_t* __restrict__ v, int len,
                                                            int64_t d, float inv_sqrt_dk,
                                                            uint16_t* __restrict__ ctx) {
-  constexpr int P = DK + 8;                  // Q / K row pitch (halves): conflict-free fragments
+  constexpr int P = DK + 8;                  // Q / K / V row pitch (halves): conflict-free
   constexpr int NT = kAttMaxLen / 8;         // key tiles of 8
-  constexpr int PV = kAttMaxLen + 8;         // V^T row pitch
   extern __shared__ __align__(16) uint16_t att_sm[];
   uint16_t* Qs = att_sm;                    // [kAttMaxLen][P]
   uint16_t* Ks = Qs + kAttMaxLen * P;       // [kAttMaxLen][P]
-  uint16_t* Vt = Ks + kAttMaxLen * P;       // [DK][PV]
+  uint16_t* Vs = Ks + kAttMaxLen * P;       // [kAttMaxLen][P] (row-major; ldmatrix.trans)
   const int Lp = (len + 15) & ~15;
   const int64_t s0 = (int64_t)blockIdx.x * len;
   const int h0 = blockIdx.y * DK;
-  for (int i = threadIdx.x; i < Lp * DK; i += blockDim.x) {
-    const int j = i / DK, c = i - j * DK;
-    uint16_t qv = 0, kv = 0, vv = 0;
+  constexpr int C8 = DK / 8;  // 16-byte pieces per head row
+  for (int i = threadIdx.x; i < Lp * C8; i += blockDim.x) {
+    const int j = i / C8, c = (i - j * C8) * 8;
+    uint4 qv = make_uint4(0, 0, 0, 0), kv = qv, vv = qv;
     if (j < len) {
       const int64_t g = (s0 + j) * d + h0 + c;
-      qv = q[g];
-      kv = k[g];
-      vv = v[g];
+      qv = *reinterpret_cast<const uint4*>(q + g);
+      kv = *reinterpret_cast<const uint4*>(k + g);
+      vv = *reinterpret_cast<const uint4*>(v + g);
     }
-    Qs[j * P + c] = qv;
-    Ks[j * P + c] = kv;
-    Vt[c * PV + j] = vv;
+    *reinterpret_cast<uint4*>(Qs + j * P + c) = qv;
+    *reinterpret_cast<uint4*>(Ks + j * P + c) = kv;
+    *reinterpret_cast<uint4*>(Vs + j * P + c) = vv;
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
@@ -359,9 +359,13 @@ __global__ void __launch_bounds__(256) attention_tc_kernel(const uint16_t* __res
       const uint32_t a3 = pack_h2(acc[2 * u + 1][2] * is1, acc[2 * u + 1][3] * is1);
 #pragma unroll
       for (int c8 = 0; c8 < DK / 8; ++c8) {
-        const uint16_t* vb = Vt + (c8 * 8 + g) * PV + u * 16 + 2 * t;
-        mma16816(o[c8], a0, a1, a2, a3, *reinterpret_cast<const uint32_t*>(vb),
-                 *reinterpret_cast<const uint32_t*>(vb + 8));
+        // B (keys x columns) fragment of V[16u.., 8c8..] by a transposing
+        // matrix load: lanes 0-15 address the 16 key rows
+        uint32_t b0, b1;
+        const uint16_t* vrow = Vs + (u * 16 + (lane & 15)) * P + c8 * 8;
+        asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0, %1}, [%2];"
+                     : "=r"(b0), "=r"(b1) : "r"(smem_u32(vrow)));
+        mma16816(o[c8], a0, a1, a2, a3, b0, b1);
       }
     }
   }
@@ -504,7 +508,7 @@ extern "C" int moe_encoder_forward(moe_moec* M, const int32_t* tokens, int64_t b
     TRY(gemm(E, E->xn, t, l.v, 0, mode, E->v, st));
     if (mode == MOE_MODE_FAST && len <= kAttMaxLen && (dk == 64 || dk == 16 || dk == 32 || dk == 128)) {
       const dim3 grid((unsigned)batch, (unsigned)E->heads);
-      const size_t tsm = ((size_t)2 * kAttMaxLen * (dk + 8) + (size_t)dk * (kAttMaxLen + 8)) * 2;
+      const size_t tsm = (size_t)3 * kAttMaxLen * (dk + 8) * 2;
       auto go = [&](auto kern) -> int {
         if (tsm > 48 * 1024)
           MOE_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
