@@ -93,8 +93,8 @@ __global__ void add_kernel(const uint16_t* __restrict__ a, const uint16_t* __res
 // q rows, the head's K and V slices and the score matrix live in shared
 // memory; the expf table too.
 __global__ void attention_kernel(const uint16_t* __restrict__ q, const uint16_t* __restrict__ k,
-                                 const uint16_t* __restrict__ v, int len, int64_t d, int dk,
-                                 float inv_sqrt_dk, uint16_t* __restrict__ ctx) {
+                                 const uint16_t* __restrict__ v, int len, int64_t d, int64_t ld,
+                                 int dk, float inv_sqrt_dk, uint16_t* __restrict__ ctx) {
   extern __shared__ __align__(16) uint8_t sm[];
   uint64_t* tab = reinterpret_cast<uint64_t*>(sm);
   float* sc = reinterpret_cast<float*>(sm + 32 * 8);  // [len][len + 1]
@@ -112,7 +112,7 @@ __global__ void attention_kernel(const uint16_t* __restrict__ q, const uint16_t*
   for (int i = threadIdx.x; i < 32; i += nt) tab[i] = moe_expf_tab_dev[i];
   for (int i = threadIdx.x; i < len * dk; i += nt) {
     const int j = i / dk, c = i - j * dk;
-    const int64_t g = (s0 + j) * d + h0 + c;
+    const int64_t g = (s0 + j) * ld + h0 + c;
     qs[j * kp + c] = q[g];
     ks[j * kp + c] = k[g];
   }
@@ -169,7 +169,7 @@ __global__ void attention_kernel(const uint16_t* __restrict__ q, const uint16_t*
   // V into the K slots (K is no longer read)
   for (int i = threadIdx.x; i < len * dk; i += nt) {
     const int j = i / dk, c = i - j * dk;
-    vs[j * kp + c] = v[(s0 + j) * d + h0 + c];
+    vs[j * kp + c] = v[(s0 + j) * ld + h0 + c];
   }
   // 2. softmax (attend_one's order where it matters): the row max is exact
   // in any order (a warp per row); every expf in parallel; the row sums
@@ -258,7 +258,8 @@ template <int DK>
 __global__ void __launch_bounds__(256) attention_tc_kernel(const uint16_t* __restrict__ q,
                                                            const uint16_t* __restrict__ k,
                                                            const uint16_t* __restrict__ v, int len,
-                                                           int64_t d, float inv_sqrt_dk,
+                                                           int64_t d, int64_t ld,
+                                                           float inv_sqrt_dk,
                                                            uint16_t* __restrict__ ctx) {
   constexpr int P = DK + 8;                  // Q / K / V row pitch (halves): conflict-free
   constexpr int NT = kAttMaxLen / 8;         // key tiles of 8
@@ -274,7 +275,7 @@ __global__ void __launch_bounds__(256) attention_tc_kernel(const uint16_t* __res
     const int j = i / C8, c = (i - j * C8) * 8;
     uint4 qv = make_uint4(0, 0, 0, 0), kv = qv, vv = qv;
     if (j < len) {
-      const int64_t g = (s0 + j) * d + h0 + c;
+      const int64_t g = (s0 + j) * ld + h0 + c;
       qv = *reinterpret_cast<const uint4*>(q + g);
       kv = *reinterpret_cast<const uint4*>(k + g);
       vv = *reinterpret_cast<const uint4*>(v + g);
@@ -464,8 +465,9 @@ extern "C" int moe_encoder_forward(moe_moec* M, const int32_t* tokens, int64_t b
       if (p) cudaFree(p);
     if (E->ident) cudaFree(E->ident);
     if (E->ones) cudaFree(E->ones);
-    for (uint16_t** p : {&E->x, &E->x2, &E->xn, &E->q, &E->k, &E->v, &E->ctx, &E->o})
+    for (uint16_t** p : {&E->x, &E->x2, &E->xn, &E->ctx, &E->o})
       MOE_CUDA_TRY(cudaMalloc(p, t * d * 2));
+    MOE_CUDA_TRY(cudaMalloc(&E->q, t * 3 * d * 2));  // Q | K | V rows
     MOE_CUDA_TRY(cudaMalloc(&E->h, t * E->f * 2));
     MOE_CUDA_TRY(cudaMalloc(&E->tokens, t * 4));
     MOE_CUDA_TRY(cudaMalloc(&E->ident, t * 4));
@@ -503,23 +505,27 @@ extern "C" int moe_encoder_forward(moe_moec* M, const int32_t* tokens, int64_t b
   for (const EncLayerDev& l : E->layers) {
     // attention_forward (model.cpp:207-256)
     TRY(layer_norm(E, x, t, l.ln_g, l.ln_b, E->xn, st));
-    TRY(gemm(E, E->xn, t, l.q, 0, mode, E->q, st));
-    TRY(gemm(E, E->xn, t, l.k, 0, mode, E->k, st));
-    TRY(gemm(E, E->xn, t, l.v, 0, mode, E->v, st));
+    // Q | K | V as one projection (W_q | W_k | W_v column-concatenated at load:
+    // every output column's chain is unchanged, xn is read once)
+    TRY(gemm(E, E->xn, t, l.qkv, 0, mode, E->q, st));
+    const uint16_t* qp = E->q;
+    const uint16_t* kp = E->q + d;
+    const uint16_t* vp = E->q + 2 * d;
+    const int64_t ld = 3 * d;
     if (mode == MOE_MODE_FAST && len <= kAttMaxLen && (dk == 64 || dk == 16 || dk == 32 || dk == 128)) {
       const dim3 grid((unsigned)batch, (unsigned)E->heads);
       const size_t tsm = (size_t)3 * kAttMaxLen * (dk + 8) * 2;
       auto go = [&](auto kern) -> int {
         if (tsm > 48 * 1024)
           MOE_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
-        kern<<<grid, 256, tsm, st>>>(E->q, E->k, E->v, (int)len, d, inv_sqrt_dk, E->ctx);
+        kern<<<grid, 256, tsm, st>>>(qp, kp, vp, (int)len, d, ld, inv_sqrt_dk, E->ctx);
         return MOE_OK;
       };
       TRY(dk == 64 ? go(attention_tc_kernel<64>) : dk == 16 ? go(attention_tc_kernel<16>)
                    : dk == 32 ? go(attention_tc_kernel<32>) : go(attention_tc_kernel<128>));
     } else {
       attention_kernel<<<dim3((unsigned)batch, (unsigned)E->heads), 256, att_smem, st>>>(
-          E->q, E->k, E->v, (int)len, d, dk, inv_sqrt_dk, E->ctx);
+          qp, kp, vp, (int)len, d, ld, dk, inv_sqrt_dk, E->ctx);
     }
     note_launch();
     TRY(check_launch("encoder attention"));

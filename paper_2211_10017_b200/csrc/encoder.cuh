@@ -18,7 +18,7 @@ struct DevLinear {
 
 struct EncLayerDev {
   uint16_t *ln_g = nullptr, *ln_b = nullptr;  // attention LayerNorm
-  DevLinear q, k, v, o;
+  DevLinear qkv, o;  // Q | K | V concatenated (n = 3 d)
   int moe_block = -1;                         // index into moe_moec::layers, or -1: dense FFN
   uint16_t *fln_g = nullptr, *fln_b = nullptr;
   DevLinear w1, w2;

@@ -144,14 +144,23 @@ int walk(const std::vector<uint8_t>& bytes, moe_moec* M, bool create) {
     auto attn = [&](const std::string& p, EncLayerDev* dev) -> int {
       const uint16_t* g = r.f16(p + ".ln_g", {d});
       const uint16_t* b = r.f16(p + ".ln_b", {d});
-      DevLinear* lin[4] = {dev ? &dev->q : nullptr, dev ? &dev->k : nullptr, dev ? &dev->v : nullptr,
-                           dev ? &dev->o : nullptr};
+      const uint16_t* wv[4];
+      const uint16_t* bv[4];
       int i = 0;
       for (const char* w : {"q", "k", "v", "o"}) {
-        const uint16_t* wp = r.f16(p + ".w" + w, {d, d});
-        const uint16_t* bp = r.f16(p + ".b" + w, {d});
-        if (dev) TRY(enc_linear(M->enc.get(), wp, bp, (int64_t)d, (int64_t)d, lin[i]));
+        wv[i] = r.f16(p + ".w" + w, {d, d});
+        bv[i] = r.f16(p + ".b" + w, {d});
         ++i;
+      }
+      if (dev) {
+        // W_q | W_k | W_v column-concatenated: one (d, 3d) projection
+        std::vector<uint16_t> w3((size_t)d * 3 * d), b3((size_t)3 * d);
+        for (uint64_t row = 0; row < d; ++row)
+          for (int m = 0; m < 3; ++m)
+            std::memcpy(&w3[row * 3 * d + m * d], wv[m] + row * d, d * 2);
+        for (int m = 0; m < 3; ++m) std::memcpy(&b3[m * d], bv[m], d * 2);
+        TRY(enc_linear(M->enc.get(), w3.data(), b3.data(), (int64_t)d, (int64_t)(3 * d), &dev->qkv));
+        TRY(enc_linear(M->enc.get(), wv[3], bv[3], (int64_t)d, (int64_t)d, &dev->o));
       }
       if (dev) {
         TRY(enc_upload(M->enc.get(), g, (int64_t)d, &dev->ln_g));
